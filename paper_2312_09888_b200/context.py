@@ -1,0 +1,181 @@
+"""Thin object wrapper over one libnekb200 context (one per process and GPU,
+confined to one host thread -- reference bridge.py:132-137)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .device import DeviceArray, device_ptr
+
+
+@dataclass(frozen=True)
+class Report:
+    """Per-execute report (the SinkReport payload of the in situ analysis)."""
+
+    n_triangles: int
+    n_triangles_global: int
+    tri_capacity: int
+    range: tuple[float, float]
+    data_range: tuple[float, float]
+    ms_fused: float
+    ms_raster: float
+    ms_composite: float
+    ms_resolve: float
+    reran: bool
+
+    @classmethod
+    def from_native(cls, r: N.NkbReport) -> "Report":
+        return cls(
+            int(r.n_triangles), int(r.n_triangles_global), int(r.tri_capacity),
+            (float(r.range[0]), float(r.range[1])),
+            (float(r.data_range[0]), float(r.data_range[1])),
+            float(r.ms_fused), float(r.ms_raster), float(r.ms_composite), float(r.ms_resolve),
+            bool(r.reran),
+        )
+
+
+def gll(order: int = 7) -> tuple[np.ndarray, np.ndarray]:
+    """GLL nodes and differentiation matrix exactly as the kernels use them."""
+    x = np.zeros(order + 1)
+    D = np.zeros((order + 1, order + 1))
+    N.call("nkb_gll", order, x.ctypes.data, D.ctypes.data)
+    return x, D
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    rc = N.lib().nkb_device_count(C.byref(n))
+    return int(n.value) if rc == N.NKB_OK else 0
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        N.call("nkb_ctx_create", int(device), C.byref(h))
+        self.handle = h.value
+        self.device = int(device)
+        self.rank = 0
+        self.nranks = 1
+
+    # -- lifetime --------------------------------------------------------------
+    def close(self) -> None:
+        if self.handle:
+            N.lib().nkb_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- DataAdaptor ------------------------------------------------------------
+    def mesh_set(self, n_elements: int, x, y, z, order: int = 7, element_offset: int = 0,
+                 n_elements_global: int = 0) -> None:
+        N.call("nkb_mesh_set", self.handle, int(n_elements), int(order), device_ptr(x), device_ptr(y),
+               device_ptr(z), int(element_offset), int(n_elements_global))
+
+    def field_set(self, name: str, base, ncomp: int = 1, comp_stride: int = 0) -> None:
+        N.call("nkb_field_set", self.handle, name.encode(), int(ncomp), device_ptr(base), int(comp_stride))
+
+    def field_clear(self) -> None:
+        N.call("nkb_field_clear", self.handle)
+
+    def set_velocity_name(self, name: str) -> None:
+        N.call("nkb_set_velocity_name", self.handle, name.encode())
+
+    def metadata(self) -> N.NkbMeshMetadata:
+        m = N.NkbMeshMetadata()
+        N.call("nkb_get_mesh_metadata", self.handle, C.byref(m))
+        return m
+
+    def bounds(self, stream: int = 0) -> tuple[float, ...]:
+        out = np.zeros(6)
+        N.call("nkb_mesh_bounds", self.handle, out.ctypes.data, stream or None)
+        return tuple(float(v) for v in out)
+
+    def get_mesh(self, points=None, conn=None, offsets=None, types=None, stream: int = 0) -> None:
+        N.call("nkb_get_mesh", self.handle, device_ptr(points), device_ptr(conn), device_ptr(offsets),
+               device_ptr(types), stream or None)
+
+    def array_components(self, name: str) -> int:
+        n = C.c_int(0)
+        N.call("nkb_array_components", self.handle, name.encode(), C.byref(n))
+        return int(n.value)
+
+    def add_array(self, name: str, out, association: int = N.NKB_ASSOC_POINT, stream: int = 0) -> int:
+        n = C.c_int(0)
+        N.call("nkb_add_array", self.handle, name.encode(), int(association), device_ptr(out), C.byref(n),
+               stream or None)
+        return int(n.value)
+
+    # -- AnalysisAdaptor::Execute ---------------------------------------------------
+    def execute(self, pipeline: N.NkbPipeline, stream: int = 0) -> Report:
+        r = N.NkbReport()
+        N.call("nkb_execute", self.handle, C.byref(pipeline), C.byref(r), stream or None)
+        return Report.from_native(r)
+
+    def image(self, width: int, height: int, depth: bool = False, stream: int = 0):
+        rgba = np.empty((height, width, 4), np.uint8)
+        dep = np.empty((height, width), np.float32) if depth else None
+        N.call("nkb_image_copy", self.handle, rgba.ctypes.data, dep.ctypes.data if depth else None,
+               stream or None)
+        return (rgba, dep) if depth else rgba
+
+    def image_device(self) -> tuple[int, int, int]:
+        a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        N.call("nkb_image_device", self.handle, C.byref(a), C.byref(b), C.byref(c))
+        return a.value or 0, b.value or 0, c.value or 0
+
+    def triangles(self, with_meta: bool = False):
+        """Triangles of the last execute, copied to host: (n, 3, 4) float32 [+ meta uint64]."""
+        t, m, n = C.c_void_p(), C.c_void_p(), C.c_int64()
+        N.call("nkb_triangles_device", self.handle, C.byref(t), C.byref(m), C.byref(n))
+        cnt = int(n.value)
+        tri = np.empty((cnt, 3, 4), np.float32)
+        if cnt:
+            N.call("nkb_memcpy", tri.ctypes.data, t.value, tri.nbytes, 2, None)
+        meta = None
+        if with_meta:
+            meta = np.empty(cnt, np.uint64)
+            if cnt and m.value:
+                N.call("nkb_memcpy", meta.ctypes.data, m.value, meta.nbytes, 2, None)
+        N.call("nkb_stream_sync", None)
+        return (tri, meta) if with_meta else tri
+
+    # -- composite communicator ----------------------------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        N.call("nkb_nccl_unique_id", C.addressof(buf))
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int) -> None:
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        N.call("nkb_comm_init", self.handle, C.addressof(buf), int(nranks), int(rank))
+        self.rank, self.nranks = int(rank), int(nranks)
+
+    def comm_destroy(self) -> None:
+        N.call("nkb_comm_destroy", self.handle)
+        self.rank, self.nranks = 0, 1
+
+    # -- reference 2D renderer -------------------------------------------------------
+    def render_structured(self, blocks, rows: int, comps: int, mode: int, width: int, height: int,
+                          vmin: float, vmax: float, rgb_out, stream: int = 0) -> tuple[float, float]:
+        nb = len(blocks)
+        ptrs = (C.c_void_p * nb)(*[device_ptr(v) for v, _ in blocks])
+        nis = (C.c_int64 * nb)(*[int(ni) for _, ni in blocks])
+        rng = np.zeros(2)
+        N.call("nkb_render_structured", self.handle, nb, C.addressof(ptrs), C.addressof(nis), int(rows),
+               int(comps), int(mode), int(width), int(height), float(vmin), float(vmax), device_ptr(rgb_out),
+               rng.ctypes.data, stream or None)
+        return float(rng[0]), float(rng[1])
+
+    def alloc(self, shape, dtype=np.float64) -> DeviceArray:
+        return DeviceArray.empty(self, shape, dtype)
+
+    def upload(self, arr: np.ndarray, stream: int = 0) -> DeviceArray:
+        return DeviceArray.from_host(self, arr, stream)

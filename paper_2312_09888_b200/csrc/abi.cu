@@ -1,0 +1,855 @@
+// C ABI of libnekb200.so (see include/nekb200.h for the contract and the
+// reference interface each entry point replaces).
+//
+// Host-side orchestration of one in situ step:
+//   reset scan state -> K1 fused (adaptor+grad+Q+classify+emit) -> K2 raster
+//   -> [NCCL min-reduce of packed keys + range words] -> K3 resolve -> report
+// The step is stream-ordered; nkb_execute synchronises once at the end to fill
+// the report (SENSEI's Execute returns after the analysis ran).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "nkb_internal.h"
+
+namespace nkb {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+// ---- NCCL, resolved at runtime so the library loads without it -------------
+struct NcclApi {
+  bool ok = false;
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+
+static int load_nccl() {
+  if (g_nccl.ok) return NKB_OK;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* n : names) {
+    g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.h) break;
+  }
+  if (!g_nccl.h) return fail(NKB_ENCCL, "cannot dlopen libnccl.so.2");
+#define NKB_SYM(field, name)                                             \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(g_nccl.h, name)); \
+  if (!g_nccl.field) return fail(NKB_ENCCL, std::string("missing NCCL symbol ") + name);
+  NKB_SYM(GetUniqueId, "ncclGetUniqueId");
+  NKB_SYM(CommInitRank, "ncclCommInitRank");
+  NKB_SYM(CommDestroy, "ncclCommDestroy");
+  NKB_SYM(Reduce, "ncclReduce");
+  NKB_SYM(AllReduce, "ncclAllReduce");
+  NKB_SYM(GroupStart, "ncclGroupStart");
+  NKB_SYM(GroupEnd, "ncclGroupEnd");
+  NKB_SYM(GetErrorString, "ncclGetErrorString");
+#undef NKB_SYM
+  g_nccl.ok = true;
+  return NKB_OK;
+}
+
+#define NKB_NCCL(call)                                                                  \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      return ::nkb::fail(NKB_ENCCL, std::string(#call) + ": " + g_nccl.GetErrorString(_r)); \
+  } while (0)
+
+// ordered encoding of doubles (monotone as unsigned 64-bit)
+static inline unsigned long long enc_ordered_h(double d) {
+  unsigned long long b;
+  memcpy(&b, &d, 8);
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+static inline double dec_ordered_h(unsigned long long u) {
+  unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+
+// mesh bounds reduction (defined in mesh_export.cu)
+int launch_bounds_kernel(const double* x, const double* y, const double* z, int64_t n,
+                         unsigned long long* enc6, cudaStream_t s);
+
+}  // namespace nkb
+
+using namespace nkb;
+
+struct nkb_ctx {
+  int device = 0;
+  // mesh (borrowed)
+  int64_t E = 0;
+  int N = 0;
+  const double *x = nullptr, *y = nullptr, *z = nullptr;
+  int64_t elem_off = 0, E_global = 0;
+  std::vector<Field> fields;
+  std::string vel_name = "velocity";
+  double gll[kNP], D[kNP * kNP];
+  // step scratch (library-owned)
+  unsigned long long* tile_status = nullptr;
+  int64_t tile_cap = 0;
+  unsigned long long* counters = nullptr;   // [0] ntri [1] enc min [2] enc max [3] ntri global; then ticket
+  unsigned int* ticket = nullptr;
+  float4* tri = nullptr;
+  unsigned long long* meta = nullptr;
+  int64_t tri_cap = 0;
+  bool meta_alloc = false;
+  unsigned long long* zbuf = nullptr;       // W*H + 2 range words
+  unsigned char* rgba = nullptr;
+  float* depth = nullptr;
+  double* range_dev = nullptr;
+  int W = 0, H = 0;
+  bool image_valid = false;
+  int64_t last_ntri = 0;
+  // pinned host staging
+  unsigned long long* h_counters = nullptr;  // 4 + 2 (range)
+  // structured renderer scratch
+  const double** s_ptrs = nullptr;
+  int64_t* s_col0 = nullptr;
+  unsigned long long* s_minmax = nullptr;
+  int s_cap = 0;
+  // comm
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  cudaEvent_t ev[6] = {};
+};
+
+static int ctx_check(nkb_ctx* ctx) {
+  if (!ctx) return fail(NKB_EINVAL, "null context");
+  NKB_CUDA(cudaSetDevice(ctx->device));
+  return NKB_OK;
+}
+#define NKB_TRY(expr)            \
+  do {                           \
+    int _rc = (expr);            \
+    if (_rc != NKB_OK) return _rc; \
+  } while (0)
+
+extern "C" {
+
+int nkb_abi_version(void) { return NKB_ABI_VERSION; }
+const char* nkb_last_error(void) { return g_err.c_str(); }
+
+int nkb_device_count(int* out) {
+  if (!out) return fail(NKB_EINVAL, "null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return fail(NKB_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *out = n;
+  return NKB_OK;
+}
+
+int nkb_gll(int order, double* nodes, double* dmat) {
+  if (order < 1 || order > 30) return fail(NKB_EINVAL, "order must be in [1, 30]");
+  std::vector<double> x(order + 1), D((order + 1) * (order + 1));
+  gll_nodes_dmat(order, x.data(), D.data());
+  if (nodes) memcpy(nodes, x.data(), sizeof(double) * x.size());
+  if (dmat) memcpy(dmat, D.data(), sizeof(double) * D.size());
+  return NKB_OK;
+}
+
+int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
+  if (!out) return fail(NKB_EINVAL, "null out");
+  *out = nullptr;
+  int n = 0;
+  NKB_CUDA(cudaGetDeviceCount(&n));
+  if (cuda_device < 0 || cuda_device >= n)
+    return fail(NKB_EINVAL, "cuda_device " + std::to_string(cuda_device) + " out of range (" +
+                                std::to_string(n) + " devices)");
+  NKB_CUDA(cudaSetDevice(cuda_device));
+  nkb_ctx* c = new nkb_ctx();
+  c->device = cuda_device;
+  gll_nodes_dmat(kN, c->gll, c->D);
+  NKB_CUDA(cudaMalloc(&c->counters, 64));
+  c->ticket = reinterpret_cast<unsigned int*>(c->counters + 4);
+  NKB_CUDA(cudaMalloc(&c->range_dev, 2 * sizeof(double)));
+  NKB_CUDA(cudaMallocHost(&c->h_counters, 8 * sizeof(unsigned long long)));
+  for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
+  *out = c;
+  return NKB_OK;
+}
+
+int nkb_ctx_destroy(nkb_ctx* ctx) {
+  if (!ctx) return NKB_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
+  cudaFree(ctx->tile_status);
+  cudaFree(ctx->counters);
+  cudaFree(ctx->tri);
+  cudaFree(ctx->meta);
+  cudaFree(ctx->zbuf);
+  cudaFree(ctx->rgba);
+  cudaFree(ctx->depth);
+  cudaFree(ctx->range_dev);
+  cudaFree(ctx->s_ptrs);
+  cudaFree(ctx->s_col0);
+  cudaFree(ctx->s_minmax);
+  cudaFreeHost(ctx->h_counters);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+  return NKB_OK;
+}
+
+// ---- DataAdaptor -------------------------------------------------------------
+
+int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order, const double* x, const double* y,
+                 const double* z, int64_t element_offset, int64_t n_elements_global) {
+  NKB_TRY(ctx_check(ctx));
+  if (order != kN)
+    return fail(NKB_EINVAL, "unsupported polynomial order " + std::to_string(order) +
+                                " (this build supports N=" + std::to_string(kN) + ")");
+  if (n_elements < 0) return fail(NKB_EINVAL, "negative element count");
+  if (n_elements > 0 && (!x || !y || !z)) return fail(NKB_EINVAL, "null coordinate pointer");
+  if (n_elements > (int64_t)0x7fffffff) return fail(NKB_EINVAL, "too many elements for one rank");
+  ctx->E = n_elements;
+  ctx->N = order;
+  ctx->x = x;
+  ctx->y = y;
+  ctx->z = z;
+  ctx->elem_off = element_offset;
+  ctx->E_global = n_elements_global > 0 ? n_elements_global : n_elements;
+  NKB_TRY(set_dmat_constant(ctx->D));
+  if (ctx->tile_cap < n_elements) {
+    cudaFree(ctx->tile_status);
+    ctx->tile_status = nullptr;
+    NKB_CUDA(cudaMalloc(&ctx->tile_status, sizeof(unsigned long long) * std::max<int64_t>(n_elements, 1)));
+    ctx->tile_cap = n_elements;
+  }
+  ctx->image_valid = false;
+  return NKB_OK;
+}
+
+int nkb_field_set(nkb_ctx* ctx, const char* name, int ncomp, const double* base, int64_t comp_stride) {
+  NKB_TRY(ctx_check(ctx));
+  if (!name || !*name) return fail(NKB_EINVAL, "empty field name");
+  if (strchr(name, ':')) return fail(NKB_EINVAL, "field names may not contain ':'");
+  if (ncomp < 1 || ncomp > 9) return fail(NKB_EINVAL, "components must be in [1, 9]");
+  if (!base && ctx->E > 0) return fail(NKB_EINVAL, "null field pointer");
+  int64_t npts = ctx->E * kNN;
+  if (ncomp > 1 && comp_stride < npts)
+    return fail(NKB_EINVAL, "comp_stride smaller than the point count");
+  for (auto& f : ctx->fields)
+    if (f.name == name) {
+      f.ncomp = ncomp;
+      f.base = base;
+      f.comp_stride = comp_stride;
+      return NKB_OK;
+    }
+  Field f;
+  f.name = name;
+  f.ncomp = ncomp;
+  f.base = base;
+  f.comp_stride = comp_stride;
+  ctx->fields.push_back(f);
+  return NKB_OK;
+}
+
+int nkb_field_clear(nkb_ctx* ctx) {
+  NKB_TRY(ctx_check(ctx));
+  ctx->fields.clear();
+  return NKB_OK;
+}
+
+int nkb_set_velocity_name(nkb_ctx* ctx, const char* name) {
+  NKB_TRY(ctx_check(ctx));
+  if (!name || !*name) return fail(NKB_EINVAL, "empty velocity name");
+  ctx->vel_name = name;
+  return NKB_OK;
+}
+
+int nkb_get_mesh_metadata(nkb_ctx* ctx, nkb_mesh_metadata* out) {
+  NKB_TRY(ctx_check(ctx));
+  if (!out) return fail(NKB_EINVAL, "null out");
+  out->n_elements = ctx->E;
+  out->order = ctx->N;
+  out->n_points = ctx->E * kNN;
+  out->n_cells = ctx->E * kNC;
+  out->cell_type = NKB_VTK_HEXAHEDRON;
+  out->element_offset = ctx->elem_off;
+  out->n_elements_global = ctx->E_global;
+  out->n_fields = (int)ctx->fields.size();
+  out->rank = ctx->rank;
+  out->nranks = ctx->nranks;
+  return NKB_OK;
+}
+
+int nkb_get_mesh(nkb_ctx* ctx, double* points, int64_t* conn, int64_t* offsets, unsigned char* types,
+                 void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->x) return fail(NKB_ESTATE, "GetMesh before mesh_set");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->E == 0) return NKB_OK;
+  if (points) NKB_TRY(launch_points_aos(ctx->x, ctx->y, ctx->z, ctx->E * kNN, points, s));
+  if (conn || offsets || types) NKB_TRY(launch_connectivity(ctx->E * kNC, conn, offsets, types, s));
+  return NKB_OK;
+}
+
+int nkb_mesh_bounds(nkb_ctx* ctx, double* out6, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!out6) return fail(NKB_EINVAL, "null out");
+  if (!ctx->x) return fail(NKB_ESTATE, "bounds before mesh_set");
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* d6 = nullptr;
+  NKB_CUDA(cudaMallocAsync(&d6, 6 * sizeof(unsigned long long), s));
+  NKB_CUDA(cudaMemsetAsync(d6, 0xff, 6 * sizeof(unsigned long long), s));
+  NKB_TRY(launch_bounds_kernel(ctx->x, ctx->y, ctx->z, ctx->E * kNN, d6, s));
+  if (ctx->comm && ctx->nranks > 1) {
+    NKB_NCCL(g_nccl.AllReduce(d6, d6, 6, ncclUint64, ncclMin, ctx->comm, s));
+  }
+  unsigned long long h6[6];
+  NKB_CUDA(cudaMemcpyAsync(h6, d6, sizeof(h6), cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaFreeAsync(d6, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  // words: enc(min x,y,z), ~enc(max x,y,z)
+  for (int a = 0; a < 3; ++a) {
+    out6[2 * a] = dec_ordered_h(h6[a]);
+    out6[2 * a + 1] = dec_ordered_h(~h6[3 + a]);
+  }
+  return NKB_OK;
+}
+
+static const Field* find_field(nkb_ctx* ctx, const std::string& name) {
+  for (auto& f : ctx->fields)
+    if (f.name == name) return &f;
+  return nullptr;
+}
+
+int nkb_array_components(nkb_ctx* ctx, const char* name, int* ncomp_out) {
+  NKB_TRY(ctx_check(ctx));
+  if (!name || !ncomp_out) return fail(NKB_EINVAL, "null argument");
+  std::string n(name);
+  if (n == "Q" || n == "vorticity:mag") {
+    *ncomp_out = 1;
+    return NKB_OK;
+  }
+  if (n == "vorticity") {
+    *ncomp_out = 3;
+    return NKB_OK;
+  }
+  auto colon = n.find(':');
+  std::string base = n.substr(0, colon);
+  const Field* f = find_field(ctx, base);
+  if (!f) return fail(NKB_EINVAL, "no field named '" + base + "'");
+  if (colon == std::string::npos) {
+    *ncomp_out = f->ncomp;
+    return NKB_OK;
+  }
+  if (n.substr(colon + 1) != "mag") return fail(NKB_EINVAL, "unknown derived scalar '" + n.substr(colon + 1) + "'");
+  *ncomp_out = 1;
+  return NKB_OK;
+}
+
+// forward
+static int fused_params_base(nkb_ctx* ctx, FusedParams& fp);
+
+int nkb_add_array(nkb_ctx* ctx, const char* name, int association, double* out, int* ncomp_out,
+                  void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!name || !out) return fail(NKB_EINVAL, "null argument");
+  if (association != NKB_ASSOC_POINT)
+    return fail(NKB_EINVAL, "only point arrays exist on the SEM mesh");
+  if (!ctx->x) return fail(NKB_ESTATE, "AddArray before mesh_set");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::string n(name);
+  int nc = 0;
+  NKB_TRY(nkb_array_components(ctx, name, &nc));
+  if (ncomp_out) *ncomp_out = nc;
+  const int64_t npts = ctx->E * kNN;
+  if (npts == 0) return NKB_OK;
+  if (n == "Q" || n == "vorticity" || n == "vorticity:mag") {
+    const Field* v = find_field(ctx, ctx->vel_name);
+    if (!v || v->ncomp != 3)
+      return fail(NKB_EINVAL, "derived array '" + n + "' needs a 3-component field '" + ctx->vel_name + "'");
+    FusedParams fp;
+    NKB_TRY(fused_params_base(ctx, fp));
+    fp.need_grad = 1;
+    fp.need_vel = 1;
+    fp.vel[0] = v->base;
+    fp.vel[1] = v->base + v->comp_stride;
+    fp.vel[2] = v->base + 2 * v->comp_stride;
+    fp.color_src = -1;
+    fp.n_surf = 0;
+    if (n == "Q") fp.q_out = out;
+    if (n == "vorticity") fp.vort_out = out;
+    if (n == "vorticity:mag") fp.wmag_out = out;
+    NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
+    NKB_TRY(launch_fused(fp, s));
+    return NKB_OK;
+  }
+  auto colon = n.find(':');
+  const Field* f = find_field(ctx, n.substr(0, colon));
+  if (colon == std::string::npos) return launch_field_aos(f->base, f->comp_stride, f->ncomp, npts, out, s);
+  return launch_field_mag(f->base, f->comp_stride, f->ncomp, npts, out, s);
+}
+
+// ---- AnalysisAdaptor::Execute ---------------------------------------------------
+
+static int fused_params_base(nkb_ctx* ctx, FusedParams& fp) {
+  memset(&fp, 0, sizeof(fp));
+  fp.n_elements = ctx->E;
+  fp.x = ctx->x;
+  fp.y = ctx->y;
+  fp.z = ctx->z;
+  fp.tile_status = ctx->tile_status;
+  fp.ticket = ctx->ticket;
+  fp.counters = ctx->counters;
+  fp.color_src = -1;
+  return NKB_OK;
+}
+
+struct Resolved {
+  FusedParams fp;
+  Colormap cm;
+};
+
+// map a pipeline field name onto a per-node source of the fused kernel
+static int resolve_src(nkb_ctx* ctx, const char* name, FusedParams& fp, int* src) {
+  std::string n(name);
+  if (n.empty()) return fail(NKB_EINVAL, "empty field name in pipeline");
+  auto need_velocity = [&]() -> int {
+    const Field* v = find_field(ctx, ctx->vel_name);
+    if (!v) return fail(NKB_EINVAL, "no field named '" + ctx->vel_name + "' (needed for '" + n + "')");
+    if (v->ncomp != 3)
+      return fail(NKB_EINVAL, "velocity field '" + ctx->vel_name + "' must have 3 components");
+    fp.need_vel = 1;
+    fp.vel[0] = v->base;
+    fp.vel[1] = v->base + v->comp_stride;
+    fp.vel[2] = v->base + 2 * v->comp_stride;
+    return NKB_OK;
+  };
+  if (n == "Q" || n == "vorticity:mag") {
+    NKB_TRY(need_velocity());
+    fp.need_grad = 1;
+    *src = (n == "Q") ? SRC_Q : SRC_WMAG;
+    return NKB_OK;
+  }
+  auto colon = n.find(':');
+  std::string base = n.substr(0, colon);
+  const Field* f = find_field(ctx, base);
+  if (!f) return fail(NKB_EINVAL, "no field named '" + base + "'");
+  if (colon != std::string::npos) {
+    std::string suf = n.substr(colon + 1);
+    if (suf != "mag") return fail(NKB_EINVAL, "unknown derived scalar '" + suf + "'");
+    if (base != ctx->vel_name)
+      return fail(NKB_EINVAL, "':mag' in the fused path is supported for the velocity field '" +
+                                  ctx->vel_name + "' only");
+    NKB_TRY(need_velocity());
+    *src = SRC_UMAG;
+    return NKB_OK;
+  }
+  if (f->ncomp != 1)  // mirrors sinks.scalar_field (sinks.py:234-238)
+    return fail(NKB_EINVAL, "field '" + base + "' has " + std::to_string(f->ncomp) +
+                                " components; request a derived scalar such as '" + base + ":mag'");
+  for (int k = 0; k < fp.n_scalars; ++k)
+    if (fp.scalar[k] == f->base) {
+      *src = SRC_SCALAR0 + k;
+      return NKB_OK;
+    }
+  if (fp.n_scalars >= kMaxScalars)
+    return fail(NKB_EINVAL, "at most " + std::to_string(kMaxScalars) + " distinct scalar fields per pipeline");
+  fp.scalar[fp.n_scalars] = f->base;
+  *src = SRC_SCALAR0 + fp.n_scalars;
+  fp.n_scalars++;
+  return NKB_OK;
+}
+
+static int build_colormap(const nkb_pipeline* p, Colormap& cm) {
+  if (p->n_anchors == 0) {  // DEFAULT_COLORMAP (sinks.py:213)
+    cm.n = 3;
+    const double t[3] = {0.0, 0.5, 1.0};
+    const double c[3][3] = {{59, 76, 192}, {255, 255, 255}, {180, 4, 38}};
+    for (int i = 0; i < 3; ++i) {
+      cm.t[i] = t[i];
+      for (int ch = 0; ch < 3; ++ch) cm.rgb[i][ch] = c[i][ch];
+    }
+    return NKB_OK;
+  }
+  if (p->n_anchors < 2 || p->n_anchors > NKB_MAX_ANCHORS)
+    return fail(NKB_EINVAL, "colormap needs 2..8 anchors");
+  // ColorMap.__post_init__ (sinks.py:196-199)
+  if (p->anchor_t[0] != 0.0 || p->anchor_t[p->n_anchors - 1] != 1.0)
+    return fail(NKB_EINVAL, "anchor positions must strictly increase from 0 to 1");
+  for (int i = 1; i < p->n_anchors; ++i)
+    if (!(p->anchor_t[i] > p->anchor_t[i - 1]))
+      return fail(NKB_EINVAL, "anchor positions must strictly increase from 0 to 1");
+  cm.n = p->n_anchors;
+  for (int i = 0; i < cm.n; ++i) {
+    cm.t[i] = p->anchor_t[i];
+    for (int ch = 0; ch < 3; ++ch) cm.rgb[i][ch] = (double)p->anchor_rgb[i][ch];
+  }
+  return NKB_OK;
+}
+
+static int ensure_image(nkb_ctx* ctx, int W, int H) {
+  if (ctx->W == W && ctx->H == H && ctx->zbuf) return NKB_OK;
+  cudaFree(ctx->zbuf);
+  cudaFree(ctx->rgba);
+  cudaFree(ctx->depth);
+  ctx->zbuf = nullptr;
+  ctx->rgba = nullptr;
+  ctx->depth = nullptr;
+  const size_t npx = (size_t)W * H;
+  NKB_CUDA(cudaMalloc(&ctx->zbuf, (npx + 2) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&ctx->rgba, npx * 4));
+  NKB_CUDA(cudaMalloc(&ctx->depth, npx * sizeof(float)));
+  ctx->W = W;
+  ctx->H = H;
+  return NKB_OK;
+}
+
+static int ensure_tri(nkb_ctx* ctx, int64_t cap, bool meta) {
+  if (cap <= ctx->tri_cap && (!meta || ctx->meta_alloc)) return NKB_OK;
+  cap = std::max(cap, ctx->tri_cap);
+  cudaFree(ctx->tri);
+  cudaFree(ctx->meta);
+  ctx->tri = nullptr;
+  ctx->meta = nullptr;
+  ctx->meta_alloc = false;
+  NKB_CUDA(cudaMalloc(&ctx->tri, (size_t)cap * 3 * sizeof(float4)));
+  if (meta || ctx->meta_alloc) {
+    NKB_CUDA(cudaMalloc(&ctx->meta, (size_t)cap * sizeof(unsigned long long)));
+    ctx->meta_alloc = true;
+  }
+  ctx->tri_cap = cap;
+  return NKB_OK;
+}
+
+static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
+                    cudaStream_t s, bool composite) {
+  const bool timing = p->timing != 0;
+  const int64_t npx = (int64_t)p->width * p->height;
+  fp.tri = ctx->tri;
+  fp.meta = p->emit_meta ? ctx->meta : nullptr;
+  fp.tri_cap = ctx->tri_cap;
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
+  // scan state: tile flags 0, counters {0, enc(+max), 0, 0}, ticket 0
+  if (ctx->E > 0)
+    NKB_CUDA(cudaMemsetAsync(ctx->tile_status, 0, sizeof(unsigned long long) * ctx->E, s));
+  NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
+  NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
+  NKB_TRY(launch_fused(fp, s));
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[1], s));
+  NKB_TRY(launch_zbuf_clear(ctx->zbuf, npx, s));
+  RasterParams rp;
+  rp.tri = ctx->tri;
+  rp.n_tri = reinterpret_cast<const int64_t*>(ctx->counters);
+  rp.tri_cap = ctx->tri_cap;
+  memcpy(rp.view, p->view, sizeof(rp.view));
+  rp.width = p->width;
+  rp.height = p->height;
+  rp.zbuf = ctx->zbuf;
+  NKB_TRY(launch_raster(rp, s));
+  NKB_TRY(launch_range_words(ctx->counters, ctx->zbuf + npx, s));
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[2], s));
+  if (composite) {
+    NKB_NCCL(g_nccl.GroupStart());
+    NKB_NCCL(g_nccl.Reduce(ctx->zbuf, ctx->zbuf, (size_t)npx + 2, ncclUint64, ncclMin, 0, ctx->comm, s));
+    NKB_NCCL(g_nccl.AllReduce(ctx->counters, ctx->counters + 3, 1, ncclUint64, ncclSum, ctx->comm, s));
+    NKB_NCCL(g_nccl.GroupEnd());
+  }
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[3], s));
+  if (!composite || ctx->rank == 0) {
+    ResolveParams rs;
+    rs.zbuf = ctx->zbuf;
+    rs.width = p->width;
+    rs.height = p->height;
+    rs.lo = rs.hi = 0.0;
+    rs.range_words = ctx->zbuf + npx;
+    rs.vmin = p->vmin;
+    rs.vmax = p->vmax;
+    rs.cmap = cm;
+    memcpy(rs.bg, p->background, 4);
+    rs.rgba = ctx->rgba;
+    rs.depth = ctx->depth;
+    rs.range_out = ctx->range_dev;
+    NKB_TRY(launch_resolve(rs, s));
+  }
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[4], s));
+  NKB_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->counters, 4 * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 4, ctx->range_dev, 2 * sizeof(double),
+                           cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  return NKB_OK;
+}
+
+int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!p) return fail(NKB_EINVAL, "null pipeline");
+  if (!ctx->x) return fail(NKB_ESTATE, "Execute before mesh_set");
+  if (p->width < 1 || p->height < 1 || p->width > 16384 || p->height > 16384)
+    return fail(NKB_EINVAL, "image size must be in [1, 16384]");
+  if (p->n_surfaces < 0 || p->n_surfaces > NKB_MAX_SURFACES)
+    return fail(NKB_EINVAL, "n_surfaces must be in [0, 4]");
+  for (int i = 0; i < 12; ++i)
+    if (!isfinite(p->view[i])) return fail(NKB_EINVAL, "view matrix must be finite");
+  cudaStream_t s = (cudaStream_t)stream;
+
+  FusedParams fp;
+  NKB_TRY(fused_params_base(ctx, fp));
+  fp.n_surf = p->n_surfaces;
+  for (int k = 0; k < p->n_surfaces; ++k) {
+    const nkb_surface& sf = p->surfaces[k];
+    char fname[NKB_NAME_MAX + 1];
+    memcpy(fname, sf.field, NKB_NAME_MAX);
+    fname[NKB_NAME_MAX] = 0;
+    if (sf.kind == NKB_SURF_ISO) {
+      NKB_TRY(resolve_src(ctx, fname, fp, &fp.surf_src[k]));
+      if (!isfinite(sf.value)) return fail(NKB_EINVAL, "iso value must be finite");
+      fp.surf_iso[k] = sf.value;
+    } else if (sf.kind == NKB_SURF_SLICE) {
+      if (!(isfinite(sf.normal[0]) && isfinite(sf.normal[1]) && isfinite(sf.normal[2]) &&
+            isfinite(sf.value)))
+        return fail(NKB_EINVAL, "slice plane must be finite");
+      if (sf.normal[0] == 0.0 && sf.normal[1] == 0.0 && sf.normal[2] == 0.0)
+        return fail(NKB_EINVAL, "slice normal must be non-zero");
+      fp.surf_src[k] = SRC_PLANE + k;
+      fp.surf_iso[k] = sf.value;
+      for (int a = 0; a < 3; ++a) fp.surf_n[k][a] = sf.normal[a];
+    } else {
+      return fail(NKB_EINVAL, "unknown surface kind " + std::to_string(sf.kind));
+    }
+  }
+  {
+    char cname[NKB_NAME_MAX + 1];
+    memcpy(cname, p->color_field, NKB_NAME_MAX);
+    cname[NKB_NAME_MAX] = 0;
+    NKB_TRY(resolve_src(ctx, cname, fp, &fp.color_src));
+  }
+  Colormap cm;
+  NKB_TRY(build_colormap(p, cm));
+
+  const bool composite = p->composite && ctx->comm && ctx->nranks > 1;
+  if (p->composite && ctx->nranks > 1 && !ctx->comm) return fail(NKB_ENCCL, "composite without comm");
+
+  NKB_TRY(ensure_image(ctx, p->width, p->height));
+  if (ctx->tri_cap == 0) NKB_TRY(ensure_tri(ctx, std::max<int64_t>(1 << 16, ctx->E * 16), p->emit_meta));
+  else NKB_TRY(ensure_tri(ctx, ctx->tri_cap, p->emit_meta));
+
+  NKB_TRY(run_step(ctx, p, fp, cm, s, composite));
+  int reran = 0;
+  int64_t ntri = (int64_t)ctx->h_counters[0];
+  if (ntri > ctx->tri_cap) {  // grow and re-run once (deterministic result)
+    NKB_TRY(ensure_tri(ctx, ntri + ntri / 4 + 1024, p->emit_meta));
+    NKB_TRY(run_step(ctx, p, fp, cm, s, composite));
+    ntri = (int64_t)ctx->h_counters[0];
+    reran = 1;
+  }
+  ctx->last_ntri = ntri;
+  ctx->image_valid = (!composite || ctx->rank == 0);
+  if (out) {
+    memset(out, 0, sizeof(*out));
+    out->n_triangles = ntri;
+    out->n_triangles_global = composite ? (int64_t)ctx->h_counters[3] : ntri;
+    out->tri_capacity = ctx->tri_cap;
+    double r[2];
+    memcpy(r, ctx->h_counters + 4, sizeof(r));
+    out->range[0] = r[0];
+    out->range[1] = r[1];
+    out->data_range[0] = ctx->h_counters[1] == ~0ULL ? NAN : dec_ordered_h(ctx->h_counters[1]);
+    out->data_range[1] = ctx->h_counters[2] == 0ULL ? NAN : dec_ordered_h(ctx->h_counters[2]);
+    out->reran = reran;
+    if (p->timing) {
+      cudaEventElapsedTime(&out->ms_fused, ctx->ev[0], ctx->ev[1]);
+      cudaEventElapsedTime(&out->ms_raster, ctx->ev[1], ctx->ev[2]);
+      cudaEventElapsedTime(&out->ms_composite, ctx->ev[2], ctx->ev[3]);
+      cudaEventElapsedTime(&out->ms_resolve, ctx->ev[3], ctx->ev[4]);
+    }
+  }
+  return NKB_OK;
+}
+
+int nkb_image_device(nkb_ctx* ctx, const unsigned char** rgba, const float** depth,
+                     const uint64_t** zbuf) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->image_valid) return fail(NKB_ESTATE, "no image (execute not run, or not the composite root)");
+  if (rgba) *rgba = ctx->rgba;
+  if (depth) *depth = ctx->depth;
+  if (zbuf) *zbuf = reinterpret_cast<const uint64_t*>(ctx->zbuf);
+  return NKB_OK;
+}
+
+int nkb_image_copy(nkb_ctx* ctx, unsigned char* rgba, float* depth, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->image_valid) return fail(NKB_ESTATE, "no image (execute not run, or not the composite root)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t npx = (size_t)ctx->W * ctx->H;
+  if (rgba) NKB_CUDA(cudaMemcpyAsync(rgba, ctx->rgba, npx * 4, cudaMemcpyDeviceToHost, s));
+  if (depth) NKB_CUDA(cudaMemcpyAsync(depth, ctx->depth, npx * sizeof(float), cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  return NKB_OK;
+}
+
+int nkb_triangles_device(nkb_ctx* ctx, const float** tri, const uint64_t** meta, int64_t* n) {
+  NKB_TRY(ctx_check(ctx));
+  if (tri) *tri = reinterpret_cast<const float*>(ctx->tri);
+  if (meta) *meta = reinterpret_cast<const uint64_t*>(ctx->meta);
+  if (n) *n = std::min<int64_t>(ctx->last_ntri, ctx->tri_cap);
+  return NKB_OK;
+}
+
+// ---- composite communicator ------------------------------------------------------
+
+int nkb_nccl_unique_id(unsigned char id_out[128]) {
+  if (!id_out) return fail(NKB_EINVAL, "null out");
+  NKB_TRY(load_nccl());
+  ncclUniqueId id;
+  NKB_NCCL(g_nccl.GetUniqueId(&id));
+  memcpy(id_out, id.internal, 128);
+  return NKB_OK;
+}
+
+int nkb_comm_init(nkb_ctx* ctx, const unsigned char id[128], int nranks, int rank) {
+  NKB_TRY(ctx_check(ctx));
+  if (!id) return fail(NKB_EINVAL, "null id");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NKB_EINVAL, "bad rank / nranks");
+  NKB_TRY(load_nccl());
+  if (ctx->comm) {
+    g_nccl.CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, 128);
+  NKB_NCCL(g_nccl.CommInitRank(&ctx->comm, nranks, uid, rank));
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  return NKB_OK;
+}
+
+int nkb_comm_destroy(nkb_ctx* ctx) {
+  NKB_TRY(ctx_check(ctx));
+  if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
+  ctx->comm = nullptr;
+  ctx->rank = 0;
+  ctx->nranks = 1;
+  return NKB_OK;
+}
+
+// ---- reference 2D renderer -------------------------------------------------------
+
+int nkb_render_structured(nkb_ctx* ctx, int n_blocks, const double* const* values, const int64_t* ni,
+                          int64_t rows, int comps, int mode, int width, int height, double vmin,
+                          double vmax, unsigned char* rgb_out, double* range_out, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (n_blocks < 1 || !values || !ni) return fail(NKB_EINVAL, "no blocks to assemble");
+  if (rows < 1 || comps < 1) return fail(NKB_EINVAL, "empty block");
+  if (mode == 0 && comps != 1)
+    return fail(NKB_EINVAL, "field has " + std::to_string(comps) +
+                                " components; request a derived scalar such as 'field:mag'");
+  if (mode != 0 && mode != 1) return fail(NKB_EINVAL, "unknown derived scalar mode");
+  if (width < 1 || height < 1) return fail(NKB_EINVAL, "image size must be positive");
+  if (!rgb_out) return fail(NKB_EINVAL, "null output");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->s_cap < n_blocks) {
+    cudaFree(ctx->s_ptrs);
+    cudaFree(ctx->s_col0);
+    ctx->s_ptrs = nullptr;
+    ctx->s_col0 = nullptr;
+    NKB_CUDA(cudaMalloc(&ctx->s_ptrs, sizeof(double*) * n_blocks));
+    NKB_CUDA(cudaMalloc(&ctx->s_col0, sizeof(int64_t) * (n_blocks + 1)));
+    ctx->s_cap = n_blocks;
+  }
+  if (!ctx->s_minmax) NKB_CUDA(cudaMalloc(&ctx->s_minmax, 4 * sizeof(unsigned long long)));
+  std::vector<int64_t> col0(n_blocks + 1, 0);
+  for (int b = 0; b < n_blocks; ++b) {
+    if (ni[b] < 1 || !values[b]) return fail(NKB_EINVAL, "empty block " + std::to_string(b));
+    col0[b + 1] = col0[b] + ni[b];
+  }
+  NKB_CUDA(cudaMemcpyAsync(ctx->s_ptrs, values, sizeof(double*) * n_blocks, cudaMemcpyHostToDevice, s));
+  NKB_CUDA(cudaMemcpyAsync(ctx->s_col0, col0.data(), sizeof(int64_t) * (n_blocks + 1),
+                           cudaMemcpyHostToDevice, s));
+  unsigned long long init[2] = {~0ULL, 0ULL};
+  NKB_CUDA(cudaMemcpyAsync(ctx->s_minmax, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  StructuredParams sp;
+  sp.n_blocks = n_blocks;
+  sp.values = ctx->s_ptrs;
+  sp.col0 = ctx->s_col0;
+  sp.ni_total = col0[n_blocks];
+  sp.rows = rows;
+  sp.comps = comps;
+  sp.mode = mode;
+  sp.width = width;
+  sp.height = height;
+  nkb_pipeline dummy;
+  memset(&dummy, 0, sizeof(dummy));
+  NKB_TRY(build_colormap(&dummy, sp.cmap));
+  sp.minmax = ctx->s_minmax;
+  sp.vmin = vmin;
+  sp.vmax = vmax;
+  sp.rgb = rgb_out;
+  sp.range_out = ctx->range_dev;
+  if (!(vmin == vmin) || !(vmax == vmax)) NKB_TRY(launch_structured_minmax(sp, s));
+  NKB_TRY(launch_structured_render(sp, s));
+  if (range_out)
+    NKB_CUDA(cudaMemcpyAsync(range_out, ctx->range_dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  return NKB_OK;
+}
+
+// ---- memory helpers ------------------------------------------------------------------
+
+int nkb_device_alloc(nkb_ctx* ctx, int64_t bytes, void** out) {
+  NKB_TRY(ctx_check(ctx));
+  if (!out || bytes < 0) return fail(NKB_EINVAL, "bad allocation request");
+  *out = nullptr;
+  NKB_CUDA(cudaMalloc(out, (size_t)std::max<int64_t>(bytes, 1)));
+  return NKB_OK;
+}
+int nkb_device_free(nkb_ctx* ctx, void* p) {
+  NKB_TRY(ctx_check(ctx));
+  NKB_CUDA(cudaFree(p));
+  return NKB_OK;
+}
+int nkb_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(NKB_EINVAL, "bad allocation request");
+  *out = nullptr;
+  NKB_CUDA(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1)));
+  return NKB_OK;
+}
+int nkb_host_free(void* p) {
+  NKB_CUDA(cudaFreeHost(p));
+  return NKB_OK;
+}
+int nkb_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
+  if (bytes < 0 || kind < 1 || kind > 3) return fail(NKB_EINVAL, "bad memcpy request");
+  if (bytes == 0) return NKB_OK;
+  NKB_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, (cudaMemcpyKind)kind, (cudaStream_t)stream));
+  return NKB_OK;
+}
+int nkb_stream_sync(void* stream) {
+  NKB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return NKB_OK;
+}
+int nkb_device_sync(void) {
+  NKB_CUDA(cudaDeviceSynchronize());
+  return NKB_OK;
+}
+
+}  // extern "C"

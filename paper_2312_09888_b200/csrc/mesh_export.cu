@@ -1,0 +1,156 @@
+// GetMesh / AddArray export kernels: the explicit VTK form of the SEM
+// adaptor (R11).  Pure data movement, HBM-bound.
+//
+// Reference anchors: component-fastest AoS layout `flat = c + comps*point`
+// (data_model.py:8-14), FieldArray export (data_model.py:27-55),
+// scalar_field ':mag' (sinks.py:227-242).  VTK_HEXAHEDRON corner order
+// (0,0,0),(1,0,0),(1,1,0),(0,1,0) then the same at +k is the VTK convention
+// (SURVEY.md §8a R11 [ext]); point ids are element-local GLL ids
+// e*(N+1)^3 + i + (N+1)*(j + (N+1)*k).
+#include <cuda_runtime.h>
+
+#include "nkb_internal.h"
+
+namespace nkb {
+
+namespace {
+
+inline unsigned grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)b;
+}
+
+__global__ void points_aos_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                  const double* __restrict__ z, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double a = __ldcs(x + i), b = __ldcs(y + i), c = __ldcs(z + i);
+    out[3 * i + 0] = a;
+    out[3 * i + 1] = b;
+    out[3 * i + 2] = c;
+  }
+}
+
+__global__ void connectivity_kernel(long long ncells, long long* __restrict__ conn,
+                                    long long* __restrict__ offsets, unsigned char* __restrict__ types) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < ncells;
+       c += (long long)gridDim.x * blockDim.x) {
+    const long long e = c / kNC;
+    const int l = (int)(c - e * kNC);
+    const int a = l % kN, b = (l / kN) % kN, k = l / (kN * kN);
+    const long long n0 = e * kNN + a + kNP * b + kNP * kNP * k;
+    if (conn) {
+      longlong2* dst = reinterpret_cast<longlong2*>(conn + 8 * c);
+      const long long dj = kNP, dk = kNP * kNP;
+      dst[0] = make_longlong2(n0, n0 + 1);
+      dst[1] = make_longlong2(n0 + 1 + dj, n0 + dj);
+      dst[2] = make_longlong2(n0 + dk, n0 + 1 + dk);
+      dst[3] = make_longlong2(n0 + 1 + dj + dk, n0 + dj + dk);
+    }
+    if (offsets) {
+      offsets[c] = 8 * c;
+      if (c == ncells - 1) offsets[ncells] = 8 * ncells;
+    }
+    if (types) types[c] = NKB_VTK_HEXAHEDRON;
+  }
+}
+
+__global__ void field_aos_kernel(const double* __restrict__ base, long long stride, int ncomp,
+                                 long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    for (int c = 0; c < ncomp; ++c) out[(long long)ncomp * i + c] = __ldcs(base + c * stride + i);
+}
+
+__global__ void field_mag_kernel(const double* __restrict__ base, long long stride, int ncomp,
+                                 long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v0 = __ldcs(base + i);
+    double acc = __dmul_rn(v0, v0);
+    for (int c = 1; c < ncomp; ++c) {
+      const double v = __ldcs(base + c * stride + i);
+      acc = __dadd_rn(acc, __dmul_rn(v, v));
+    }
+    out[i] = __dsqrt_rn(acc);
+  }
+}
+
+__device__ __forceinline__ unsigned long long enc_ordered(double d) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+// enc6 = {enc(min x), enc(min y), enc(min z), ~enc(max x), ~enc(max y), ~enc(max z)}:
+// every word is a running minimum, so ranks combine with one ncclMin.
+__global__ void bounds_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                              const double* __restrict__ z, long long n, unsigned long long* enc6) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v[3] = {x[i], y[i], z[i]};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = fmin(mn[a], v[a]);
+      mx[a] = fmax(mx[a], v[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[a] = fmin(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+      mx[a] = fmax(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0 && mn[0] <= mx[0]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&enc6[a], enc_ordered(mn[a]));
+      atomicMin(&enc6[3 + a], ~enc_ordered(mx[a]));
+    }
+  }
+}
+
+}  // namespace
+
+int launch_bounds_kernel(const double* x, const double* y, const double* z, int64_t n,
+                         unsigned long long* enc6, cudaStream_t s) {
+  if (n <= 0) return NKB_OK;
+  bounds_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, y, z, n, enc6);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_points_aos(const double* x, const double* y, const double* z, int64_t npts, double* out,
+                      cudaStream_t s) {
+  points_aos_kernel<<<grid_for(npts, 256), 256, 0, s>>>(x, y, z, npts, out);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_connectivity(int64_t ncells, int64_t* conn, int64_t* offsets, unsigned char* types,
+                        cudaStream_t s) {
+  connectivity_kernel<<<grid_for(ncells, 256), 256, 0, s>>>(
+      ncells, reinterpret_cast<long long*>(conn), reinterpret_cast<long long*>(offsets), types);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_field_aos(const double* base, int64_t stride, int ncomp, int64_t npts, double* out,
+                     cudaStream_t s) {
+  field_aos_kernel<<<grid_for(npts, 256), 256, 0, s>>>(base, stride, ncomp, npts, out);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_field_mag(const double* base, int64_t stride, int ncomp, int64_t npts, double* out,
+                     cudaStream_t s) {
+  field_mag_kernel<<<grid_for(npts, 256), 256, 0, s>>>(base, stride, ncomp, npts, out);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+}  // namespace nkb

@@ -1,0 +1,146 @@
+// Internal declarations shared by the libnekb200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nekb200.h"
+
+namespace nkb {
+
+// ---- error plumbing ------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define NKB_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return ::nkb::fail(NKB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define NKB_CHECK(cond, code, msg) \
+  do {                             \
+    if (!(cond)) return ::nkb::fail((code), (msg)); \
+  } while (0)
+
+// ---- compile-time geometry of the supported element order ------------------
+constexpr int kN = 7;              // polynomial order
+constexpr int kNP = kN + 1;        // GLL nodes per direction
+constexpr int kNN = kNP * kNP * kNP;   // 512 nodes per element
+constexpr int kNC = kN * kN * kN;      // 343 sub-hexes per element
+
+// ---- field registry --------------------------------------------------------
+struct Field {
+  std::string name;
+  int ncomp = 0;
+  const double* base = nullptr;
+  int64_t comp_stride = 0;
+};
+
+// ---- sources of a per-node scalar inside the fused kernel ------------------
+enum Src : int {
+  SRC_Q = 0,        // Q-criterion
+  SRC_WMAG = 1,     // |vorticity|
+  SRC_UMAG = 2,     // |velocity|
+  SRC_SCALAR0 = 3,  // loaded scalar field slot 0
+  SRC_SCALAR1 = 4,  // loaded scalar field slot 1
+  SRC_PLANE = 8,    // plane distance of surface k: SRC_PLANE + k
+};
+constexpr int kMaxScalars = 2;
+
+struct FusedParams {
+  int64_t n_elements;
+  const double* x;
+  const double* y;
+  const double* z;
+  const double* vel[3];
+  const double* scalar[kMaxScalars];
+  int need_grad;                    // compute velocity gradient (Q / vorticity)
+  int need_vel;                     // load velocity
+  int n_scalars;
+  int n_surf;
+  int surf_src[NKB_MAX_SURFACES];
+  double surf_iso[NKB_MAX_SURFACES];
+  double surf_n[NKB_MAX_SURFACES][3];
+  int color_src;                    // -1: no colour (export-only run)
+  // exports (may be null)
+  double* q_out;
+  double* wmag_out;
+  double* vort_out;                 // AoS 3 comps
+  // triangle output
+  float4* tri;                      // 3 float4 per triangle
+  unsigned long long* meta;         // may be null
+  int64_t tri_cap;
+  // single-pass scan state
+  unsigned long long* tile_status;  // [n_elements], zeroed before launch
+  unsigned int* ticket;             // zeroed before launch
+  unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
+};
+
+struct RasterParams {
+  const float4* tri;
+  const int64_t* n_tri;             // device count (clamped to capacity on device)
+  int64_t tri_cap;
+  double view[12];
+  int width, height;
+  unsigned long long* zbuf;
+};
+
+struct Colormap {
+  int n;
+  double t[NKB_MAX_ANCHORS];
+  double rgb[NKB_MAX_ANCHORS][3];
+};
+
+struct ResolveParams {
+  const unsigned long long* zbuf;
+  int width, height;
+  double lo, hi;          // resolved on host when known, else read from range_words
+  const unsigned long long* range_words;  // [2]: enc(lo), ~enc(hi) (after composite), may be null
+  double vmin, vmax;      // NaN => from range_words
+  Colormap cmap;
+  unsigned char bg[4];
+  unsigned char* rgba;
+  float* depth;
+  double* range_out;      // [2] device, range used
+};
+
+// ---- kernel launchers (defined in .cu files) --------------------------------
+int set_dmat_constant(const double* dmat);
+int launch_fused(const FusedParams& p, cudaStream_t s);
+int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
+int launch_raster(const RasterParams& p, cudaStream_t s);
+int launch_range_words(const unsigned long long* counters, unsigned long long* words, cudaStream_t s);
+int launch_resolve(const ResolveParams& p, cudaStream_t s);
+int launch_points_aos(const double* x, const double* y, const double* z, int64_t npts,
+                      double* out, cudaStream_t s);
+int launch_connectivity(int64_t ncells, int64_t* conn, int64_t* offsets, unsigned char* types,
+                        cudaStream_t s);
+int launch_field_aos(const double* base, int64_t stride, int ncomp, int64_t npts, double* out,
+                     cudaStream_t s);
+int launch_field_mag(const double* base, int64_t stride, int ncomp, int64_t npts, double* out,
+                     cudaStream_t s);
+struct StructuredParams {
+  int n_blocks;
+  const double* const* values;  // device array of device pointers
+  const int64_t* col0;          // device [n_blocks+1] prefix of ni
+  int64_t ni_total, rows;
+  int comps, mode;
+  int width, height;
+  Colormap cmap;
+  unsigned long long* minmax;   // device [2] ordered encodings
+  double vmin, vmax;
+  unsigned char* rgb;
+  double* range_out;
+};
+int launch_structured_minmax(const StructuredParams& p, cudaStream_t s);
+int launch_structured_render(const StructuredParams& p, cudaStream_t s);
+
+// GLL nodes / derivative matrix (host, deterministic; see gll.cpp)
+void gll_nodes_dmat(int order, double* nodes, double* dmat);
+
+}  // namespace nkb

@@ -1,0 +1,308 @@
+// K2 raster (triangles -> packed depth|scalar keys, order-independent
+// atomicMin) and K3 resolve (keys -> RGBA8 + depth through the reference
+// colormap).
+//
+// Reference anchors: colormap `ColorMap.apply` / DEFAULT_COLORMAP
+// (sinks.py:190-213: clip, np.interp per channel, floor(v+0.5)); global range
+// and degenerate-range rule of `render` (sinks.py:264-269); row 0 = top of
+// the image (sinks.py:256-257).  Rasterisation itself (R15) has no reference
+// implementation; oracle/sem_oracle.c restates it operation for operation.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "nkb_internal.h"
+
+namespace nkb {
+
+namespace {
+
+constexpr double kGuard = 32768.0;   // |screen coordinate| bound in pixels
+
+__device__ __forceinline__ void xform(const double* V, double x, double y, double z, double& sx,
+                                      double& sy, double& sz) {
+  sx = __dadd_rn(__fma_rn(V[2], z, __fma_rn(V[1], y, __dmul_rn(V[0], x))), V[3]);
+  sy = __dadd_rn(__fma_rn(V[6], z, __fma_rn(V[5], y, __dmul_rn(V[4], x))), V[7]);
+  sz = __dadd_rn(__fma_rn(V[10], z, __fma_rn(V[9], y, __dmul_rn(V[8], x))), V[11]);
+}
+
+__device__ __forceinline__ long long floordiv(long long a, long long b) {  // b > 0
+  long long q = a / b;
+  if ((a % b != 0) && (a < 0)) --q;
+  return q;
+}
+
+__device__ __forceinline__ double dec_ordered(unsigned long long u) {
+  unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
+  return __longlong_as_double((long long)b);
+}
+
+// np.interp on clipped t, then floor(v + 0.5) -> uint8 (sinks.py:201-209)
+__device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double t, int ch) {
+  if (t != t) return 0;
+  const int n = cm.n;
+  double v;
+  if (t >= cm.t[n - 1]) {
+    v = cm.rgb[n - 1][ch];
+  } else {
+    int j = 0;
+    for (int k = 1; k < n - 1; ++k)
+      if (t >= cm.t[k]) j = k;
+    if (t == cm.t[j]) {
+      v = cm.rgb[j][ch];
+    } else {
+      const double slope = __ddiv_rn(__dsub_rn(cm.rgb[j + 1][ch], cm.rgb[j][ch]),
+                                     __dsub_rn(cm.t[j + 1], cm.t[j]));
+      v = __dadd_rn(__dmul_rn(slope, __dsub_rn(t, cm.t[j])), cm.rgb[j][ch]);
+    }
+  }
+  return (unsigned char)floor(__dadd_rn(v, 0.5));
+}
+
+__device__ __forceinline__ double clip01(double t) { return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t); }
+
+__global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    z[i] = ~0ULL;
+}
+
+// one thread per triangle (grid-stride; the count lives on the device)
+__global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
+  long long ntri = (long long)*p.n_tri;
+  if (ntri > p.tri_cap) ntri = p.tri_cap;
+  const int W = p.width, H = p.height;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntri;
+       t += (long long)gridDim.x * blockDim.x) {
+    long long X[3], Y[3];
+    double Z[3], C[3];
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const float4 v = p.tri[3 * t + r];
+      double sx, sy, sz;
+      xform(p.view, (double)v.x, (double)v.y, (double)v.z, sx, sy, sz);
+      if (!(fabs(sx) <= kGuard && fabs(sy) <= kGuard && sz == sz && v.w == v.w)) ok = false;
+      X[r] = __double2ll_rn(__dmul_rn(sx, 256.0));
+      Y[r] = __double2ll_rn(__dmul_rn(sy, 256.0));
+      Z[r] = sz;
+      C[r] = (double)v.w;
+    }
+    if (!ok) continue;
+    long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
+    if (area == 0) continue;
+    if (area < 0) {
+      long long tx = X[1]; X[1] = X[2]; X[2] = tx;
+      long long ty = Y[1]; Y[1] = Y[2]; Y[2] = ty;
+      double tz = Z[1]; Z[1] = Z[2]; Z[2] = tz;
+      double tc = C[1]; C[1] = C[2]; C[2] = tc;
+      area = -area;
+    }
+    const long long xmin = min(X[0], min(X[1], X[2])), xmax = max(X[0], max(X[1], X[2]));
+    const long long ymin = min(Y[0], min(Y[1], Y[2])), ymax = max(Y[0], max(Y[1], Y[2]));
+    long long px0 = -floordiv(-(xmin - 128), 256), px1 = floordiv(xmax - 128, 256);
+    long long py0 = -floordiv(-(ymin - 128), 256), py1 = floordiv(ymax - 128, 256);
+    if (px0 < 0) px0 = 0;
+    if (py0 < 0) py0 = 0;
+    if (px1 > W - 1) px1 = W - 1;
+    if (py1 > H - 1) py1 = H - 1;
+    // edge (a->b) opposite vertex i: w_i(P) = (Xb-Xa)(Py-Ya) - (Yb-Ya)(Px-Xa)
+    const int ea[3] = {1, 2, 0}, eb[3] = {2, 0, 1};
+    long long bias[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const long long dy = Y[eb[i]] - Y[ea[i]], dx = X[eb[i]] - X[ea[i]];
+      bias[i] = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : -1;   // inclusive (top-left) edges
+    }
+    const double dA = (double)area;
+    for (long long py = py0; py <= py1; ++py) {
+      const long long cy = py * 256 + 128;
+      for (long long px = px0; px <= px1; ++px) {
+        const long long cx = px * 256 + 128;
+        long long w[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          w[i] = (X[eb[i]] - X[ea[i]]) * (cy - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx - X[ea[i]]);
+        if (w[0] + bias[0] < 0 || w[1] + bias[1] < 0 || w[2] + bias[2] < 0) continue;
+        double d = __ddiv_rn(__fma_rn((double)w[2], Z[2],
+                                      __fma_rn((double)w[1], Z[1], __dmul_rn((double)w[0], Z[0]))),
+                             dA);
+        if (!(d >= 0.0 && d <= 1.0)) continue;
+        d = __dadd_rn(d, 0.0);
+        const double c = __ddiv_rn(__fma_rn((double)w[2], C[2],
+                                            __fma_rn((double)w[1], C[1], __dmul_rn((double)w[0], C[0]))),
+                                   dA);
+        const unsigned long long key =
+            ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
+            (unsigned long long)__float_as_uint(__double2float_rn(c));
+        atomicMin(p.zbuf + py * W + px, key);
+      }
+    }
+  }
+}
+
+// counters [1]=enc(min) [2]=enc(max) -> composite words: enc(min), ~enc(max)
+__global__ void range_words_kernel(const unsigned long long* counters, unsigned long long* words) {
+  words[0] = counters[1];
+  words[1] = ~counters[2];
+}
+
+__global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
+  double lo = p.vmin, hi = p.vmax;
+  if (p.range_words) {
+    const unsigned long long w0 = p.range_words[0], w1 = ~p.range_words[1];
+    if (!(lo == lo)) lo = (w0 == ~0ULL) ? 0.0 : dec_ordered(w0);
+    if (!(hi == hi)) hi = (w1 == 0ULL) ? 0.0 : dec_ordered(w1);
+  }
+  const long long n = (long long)p.width * p.height;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.range_out) {
+    p.range_out[0] = lo;
+    p.range_out[1] = hi;
+  }
+  const double span = __dsub_rn(hi, lo);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long key = p.zbuf[i];
+    uchar4 o;
+    float dep;
+    if (key == ~0ULL) {
+      o = make_uchar4(p.bg[0], p.bg[1], p.bg[2], p.bg[3]);
+      dep = INFINITY;
+    } else {
+      const double s = (double)__uint_as_float((unsigned)(key & 0xffffffffULL));
+      dep = __uint_as_float((unsigned)(key >> 32));
+      const double t = clip01(hi > lo ? __ddiv_rn(__dsub_rn(s, lo), span) : 0.0);
+      o = make_uchar4(cmap_channel(p.cmap, t, 0), cmap_channel(p.cmap, t, 1),
+                      cmap_channel(p.cmap, t, 2), 255);
+    }
+    reinterpret_cast<uchar4*>(p.rgba)[i] = o;
+    if (p.depth) p.depth[i] = dep;
+  }
+}
+
+// ---- reference 2D renderer (sinks.render) ---------------------------------
+
+__device__ __forceinline__ unsigned long long enc_ordered(double d) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+__device__ __forceinline__ double structured_value(const StructuredParams& p, long long row,
+                                                   long long col) {
+  int b = 0;
+  while (b + 1 < p.n_blocks && col >= p.col0[b + 1]) ++b;
+  const long long ni = p.col0[b + 1] - p.col0[b];
+  const double* v = p.values[b] + (size_t)p.comps * ((col - p.col0[b]) + ni * row);
+  if (p.mode == 0) return v[0];
+  // scalar_field ':mag' = sqrt(sum(grid**2, axis=-1)), left-to-right (sinks.py:240-241)
+  double acc = __dmul_rn(v[0], v[0]);
+  for (int c = 1; c < p.comps; ++c) acc = __dadd_rn(acc, __dmul_rn(v[c], v[c]));
+  return __dsqrt_rn(acc);
+}
+
+__global__ void __launch_bounds__(256) structured_minmax_kernel(const StructuredParams p) {
+  const long long n = p.ni_total * p.rows;
+  double mn = INFINITY, mx = -INFINITY;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double v = structured_value(p, i / p.ni_total, i % p.ni_total);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0 && mn <= mx) {
+    atomicMin(&p.minmax[0], enc_ordered(mn));
+    atomicMax(&p.minmax[1], enc_ordered(mx));
+  }
+}
+
+__global__ void __launch_bounds__(256) structured_render_kernel(const StructuredParams p) {
+  double lo = p.vmin, hi = p.vmax;
+  if (!(lo == lo)) lo = dec_ordered(p.minmax[0]);
+  if (!(hi == hi)) hi = dec_ordered(p.minmax[1]);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.range_out) {
+    p.range_out[0] = lo;
+    p.range_out[1] = hi;
+  }
+  const long long ni = p.ni_total, nj = p.rows;
+  const int W = p.width, H = p.height;
+  const long long npx = (long long)W * H;
+  const bool deg = !(hi > lo);
+  const double span = __dsub_rn(hi, lo);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npx;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long py = i / W, px = i % W;
+    // sinks.py:271-281 pixel -> index space
+    const double xf = (W > 1) ? __ddiv_rn((double)(px * (ni - 1)), (double)(W - 1)) : 0.0;
+    const double yf = (H > 1) ? __ddiv_rn((double)((H - 1 - py) * (nj - 1)), (double)(H - 1)) : 0.0;
+    const long long x0 = (ni > 1) ? min((long long)xf, ni - 2) : 0;
+    const long long y0 = (nj > 1) ? min((long long)yf, nj - 2) : 0;
+    const double ax = __dsub_rn(xf, (double)x0), ay = __dsub_rn(yf, (double)y0);
+    const long long x1 = min(x0 + 1, ni - 1), y1 = min(y0 + 1, nj - 1);
+    auto T = [&](long long r, long long c) {
+      return deg ? 0.0 : __ddiv_rn(__dsub_rn(structured_value(p, r, c), lo), span);
+    };
+    const double t00 = T(y0, x0), t01 = T(y0, x1), t10 = T(y1, x0), t11 = T(y1, x1);
+    const double omay = __dsub_rn(1.0, ay), omax = __dsub_rn(1.0, ax);
+    // sinks.py:288-293, numpy left-to-right evaluation
+    double s = __dmul_rn(__dmul_rn(t00, omay), omax);
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(t01, omay), ax));
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(t10, ay), omax));
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(t11, ay), ax));
+    const double t = clip01(s);
+    p.rgb[3 * i + 0] = cmap_channel(p.cmap, t, 0);
+    p.rgb[3 * i + 1] = cmap_channel(p.cmap, t, 1);
+    p.rgb[3 * i + 2] = cmap_channel(p.cmap, t, 2);
+  }
+}
+
+inline unsigned grid_for(long long n, int threads, int max_blocks) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s) {
+  zbuf_clear_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(zbuf, n);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_raster(const RasterParams& p, cudaStream_t s) {
+  raster_kernel<<<148 * 8, 256, 0, s>>>(p);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_range_words(const unsigned long long* counters, unsigned long long* words,
+                       cudaStream_t s) {
+  range_words_kernel<<<1, 1, 0, s>>>(counters, words);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_resolve(const ResolveParams& p, cudaStream_t s) {
+  resolve_kernel<<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_structured_minmax(const StructuredParams& p, cudaStream_t s) {
+  structured_minmax_kernel<<<grid_for(p.ni_total * p.rows, 256, 148 * 8), 256, 0, s>>>(p);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_structured_render(const StructuredParams& p, cudaStream_t s) {
+  structured_render_kernel<<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+}  // namespace nkb

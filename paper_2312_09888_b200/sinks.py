@@ -1,0 +1,247 @@
+"""Analysis sinks (the AnalysisAdaptors the bridge drives), GPU-backed.
+
+Same plugin contract as the reference (pkg/src/nekmini/sinks.py:310-418):
+``cls(params: dict[str, str])`` creates its output directory and fails fast
+when it is unwritable (:396-402), ``consume(snapshot) -> int`` returns the
+bytes written, ``finalize()`` flushes.  Registered kinds:
+
+* ``render`` -- drop-in for the reference's RenderSink (:327-351): the 2D
+  pseudocolor of a structured snapshot, computed by libnekb200
+  (nkb_render_structured) and byte-identical to the reference's `render`
+  (:245-295); same default two images (temperature, velocity:mag), same
+  file names ``step{step:06d}_{field with ':'->'_'}.ppm``.
+* ``insitu`` -- the SEM hot path: adaptor -> Q -> iso/slice -> raster ->
+  composite (analysis.InsituAnalysis); writes one PPM per trigger on the
+  composite root.
+* ``null`` -- counts invocations (:354-363).
+
+The checkpoint and stats sinks of the reference are outside the hot path
+ and are not provided.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .adaptor import SemDataAdaptor
+from .analysis import InsituAnalysis, pipeline_from_params
+from .context import Context
+from .data_model import CELL, check_assembly
+from .device import DeviceArray, is_device_array
+
+
+@dataclass(frozen=True)
+class ColorMap:
+    """Piecewise-linear RGB colormap over t in [0, 1] (sinks.py:190-209)."""
+
+    anchors: tuple[tuple[float, tuple[int, int, int]], ...]
+
+    def __post_init__(self):
+        ts = [t for t, _ in self.anchors]
+        if ts[0] != 0.0 or ts[-1] != 1.0 or any(b <= a for a, b in zip(ts, ts[1:])):
+            raise ValueError("anchor positions must strictly increase from 0 to 1")
+
+
+DEFAULT_COLORMAP = ColorMap(((0.0, (59, 76, 192)), (0.5, (255, 255, 255)), (1.0, (180, 4, 38))))
+
+
+@dataclass(frozen=True)
+class ImageRGB:
+    width: int
+    height: int
+    pixels: bytes  # row-major 8-bit RGB, top row first
+
+    def __post_init__(self):
+        if len(self.pixels) != 3 * self.width * self.height:
+            raise ValueError("pixel buffer length must be 3 * width * height")
+
+
+def write_ppm(img: ImageRGB, path) -> int:
+    """Binary PPM (P6); returns the exact byte count written (sinks.py:298-303)."""
+    header = f"P6\n{img.width} {img.height}\n255\n".encode("ascii")
+    data = header + img.pixels
+    Path(path).write_bytes(data)
+    return len(data)
+
+
+def _probe_writable(d: Path):
+    probe = d / ".write_probe"
+    try:
+        probe.touch()
+        probe.unlink()
+    except OSError as e:
+        raise OSError(f"output directory {d} is not writable: {e}") from e
+
+
+_CTX: dict[int, Context] = {}
+
+
+def default_context(device: int | None = None) -> Context:
+    """One libnekb200 context per (process, device)."""
+    if device is None:
+        import os
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    if device not in _CTX:
+        _CTX[device] = Context(device)
+    return _CTX[device]
+
+
+class GpuRenderer:
+    """GPU implementation of the reference's `render` (sinks.py:245-295)."""
+
+    def __init__(self, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self._staging: dict[tuple[int, str], DeviceArray] = {}
+        self._rgb: DeviceArray | None = None
+
+    def render(self, s, field: str, cmap: ColorMap = DEFAULT_COLORMAP, width: int = 256, height: int = 256,
+               vmin: float | None = None, vmax: float | None = None) -> ImageRGB:
+        if cmap != DEFAULT_COLORMAP:
+            raise ValueError("the GPU renderer implements the reference DEFAULT_COLORMAP only")
+        blocks = list(s.blocks)
+        if not blocks:
+            raise ValueError("no blocks to assemble")
+        check_assembly(blocks)
+        base, _, derived = field.partition(":")
+        f0 = blocks[0].field_named(base)
+        if f0.association == CELL and len(blocks) == 1:
+            raise ValueError("cell fields cannot be rendered as a point grid")
+        comps = f0.components
+        if derived == "":
+            if comps != 1:
+                raise ValueError(
+                    f"field {base!r} has {comps} components; request a derived scalar such as {base!r}:mag"
+                )
+            mode = 0
+        elif derived == "mag":
+            mode = 1
+        else:
+            raise ValueError(f"unknown derived scalar {derived!r}")
+        ni0, nj, nk = blocks[0].dims
+        dev_blocks = []
+        for bi, b in enumerate(blocks):
+            vals = b.field_named(base).values
+            if is_device_array(vals):
+                d = vals
+            else:
+                a = np.ascontiguousarray(vals, dtype=np.float64)
+                key = (bi, base)
+                d = self._staging.get(key)
+                if d is None or d.size != a.size:
+                    d = DeviceArray.empty(self.ctx, (a.size,), np.float64)
+                    self._staging[key] = d
+                d.upload(a, sync=False)
+            dev_blocks.append((d, b.dims[0]))
+        npx = width * height * 3
+        if self._rgb is None or self._rgb.size < npx:
+            self._rgb = DeviceArray.empty(self.ctx, (npx,), np.uint8)
+        nan = float("nan")
+        self.ctx.render_structured(
+            dev_blocks, nj * nk, comps, mode, width, height,
+            nan if vmin is None else float(vmin), nan if vmax is None else float(vmax), self._rgb,
+        )
+        out = np.empty(npx, np.uint8)
+        N.call("nkb_memcpy", out.ctypes.data, self._rgb.ptr, npx, 2, None)
+        N.call("nkb_stream_sync", None)
+        return ImageRGB(width, height, out.tobytes())
+
+
+_RENDERER: GpuRenderer | None = None
+
+
+def render(s, field: str, cmap: ColorMap = DEFAULT_COLORMAP, width: int = 256, height: int = 256,
+           vmin: float | None = None, vmax: float | None = None) -> ImageRGB:
+    """Drop-in for the reference `render` (sinks.py:245-295), on the GPU."""
+    global _RENDERER
+    if _RENDERER is None:
+        _RENDERER = GpuRenderer()
+    return _RENDERER.render(s, field, cmap, width, height, vmin, vmax)
+
+
+class RenderSink:
+    """Renders per trigger; with no explicit field, renders two images
+    (temperature and velocity magnitude) per snapshot (sinks.py:327-351)."""
+
+    def __init__(self, params: dict[str, str], comm=None):
+        self.dir = Path(params.get("dir", "render_out"))
+        self.width = int(params.get("width", 256))
+        self.height = int(params.get("height", 256))
+        f = params.get("field")
+        self.fields = [f] if f else ["temperature", "velocity:mag"]
+        self.vmin = float(params["vmin"]) if "vmin" in params else None
+        self.vmax = float(params["vmax"]) if "vmax" in params else None
+        self.dir.mkdir(parents=True, exist_ok=True)
+        _probe_writable(self.dir)
+        self._renderer = GpuRenderer()
+
+    def consume(self, s) -> int:
+        total = 0
+        for name in self.fields:
+            img = self._renderer.render(s, name, DEFAULT_COLORMAP, self.width, self.height, self.vmin, self.vmax)
+            fname = f"step{s.step:06d}_{name.replace(':', '_')}.ppm"
+            total += write_ppm(img, self.dir / fname)
+        return total
+
+    def finalize(self):
+        pass
+
+
+class InsituSink:
+    """The SEM in situ analysis as a sink: one image per trigger on the
+    composite root, named like the reference's render images (sinks.py:346)."""
+
+    def __init__(self, params: dict[str, str], comm=None):
+        self.dir = Path(params.get("dir", "insitu_out"))
+        self.pipeline = pipeline_from_params(params)
+        self.comm = comm
+        ctx = comm.ctx if comm is not None else default_context()
+        self.adaptor = SemDataAdaptor(ctx, velocity=params.get("velocity", "velocity"))
+        self.analysis = InsituAnalysis(self.pipeline)
+        self.last = None
+        root = comm is None or comm.rank == 0
+        if root:
+            self.dir.mkdir(parents=True, exist_ok=True)
+            _probe_writable(self.dir)
+
+    def consume(self, s) -> int:
+        self.adaptor.initialize(s)
+        res = self.analysis.execute(self.adaptor)
+        self.last = res
+        if res.rgba is None:
+            return 0
+        img = ImageRGB(self.pipeline.width, self.pipeline.height, res.rgba[..., :3].tobytes())
+        fname = f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}.ppm"
+        return write_ppm(img, self.dir / fname)
+
+    def finalize(self):
+        pass
+
+
+class NullSink:
+    def __init__(self, params: dict[str, str] | None = None, comm=None):
+        self.count = 0
+
+    def consume(self, s) -> int:
+        self.count += 1
+        return 0
+
+    def finalize(self):
+        pass
+
+
+_SINK_TYPES = {
+    "render": RenderSink,
+    "insitu": InsituSink,
+    "null": NullSink,
+}
+
+
+def make_sink(kind: str, params: dict[str, str], comm=None):
+    try:
+        cls = _SINK_TYPES[kind]
+    except KeyError:
+        raise ValueError(f"unknown sink kind {kind!r}") from None
+    return cls(params, comm=comm)
