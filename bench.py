@@ -1,0 +1,347 @@
+"""In situ hot-path benchmark: GLL points/s per in situ step
+(adaptor + Q-criterion + isosurface/slice + render [+ composite]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+
+A step = one AnalysisAdaptor::Execute over the rank's partition of the
+workload, fields resident in HBM (`value`), plus the same step through the
+reference-facing sink with host buffers (`e2e`).  Weak scaling: each GPU owns
+one BASELINE configs[1] worth of elements (C2 RBC cylinder, 32,768 elements,
+16.8M GLL points); at N GPUs the cylinder is N times taller.  `--impl
+reference` times the CPU oracle port (the reference has no implementation of
+this path) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GLL points/sec per in situ step (adaptor+Q-crit+iso+render) at 1/2/4/8 B200"
+UNIT = "GLL points/s"
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _case_arrays(cfg: str, rank: int, world: int):
+    from paper_2312_09888_b200 import synth
+
+    return synth.make_case(cfg, rank, world, scale=world)
+
+
+def _pipeline(case, width):
+    from dataclasses import replace
+
+    from paper_2312_09888_b200.analysis import pipeline_from_params
+
+    p = pipeline_from_params({**case.params, "width": str(width), "height": str(width)})
+    return replace(p, composite=True)
+
+
+def _bytes_read_per_point(case) -> int:
+    return 8 * (3 + sum(v.shape[0] for v in case.fields.values()))
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+
+    from paper_2312_09888_b200.adaptor import SemDataAdaptor
+    from paper_2312_09888_b200.analysis import InsituAnalysis
+    from paper_2312_09888_b200.comm import Communicator
+    from paper_2312_09888_b200.context import Context
+    from paper_2312_09888_b200.data_model import POINT, FieldArray, SemBlock, Snapshot
+    from paper_2312_09888_b200.device import DeviceArray, PinnedBuffer
+    from paper_2312_09888_b200.sinks import InsituSink
+
+    rank, world, local = _env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    ctx = Context(local)
+    comm = Communicator.from_torch(ctx) if world > 1 else None
+
+    case = _case_arrays(a.config, rank, world)
+    npts = case.n_points
+    pipe = _pipeline(case, a.width)
+
+    # ---- device-resident step (value) ----
+    dev = {k: DeviceArray.from_host(ctx, v) for k, v in
+           (("x", case.x), ("y", case.y), ("z", case.z), *case.fields.items())}
+    fields = tuple(FieldArray(k, POINT, case.fields[k].shape[0], dev[k], comp_stride=npts) for k in case.fields)
+    blk = SemBlock(case.n_elements, dev["x"], dev["y"], dev["z"], fields=fields, element_offset=case.e0,
+                   n_elements_global=case.n_elements_global)
+    da = SemDataAdaptor(ctx)
+    da.initialize(Snapshot(0.0, 0, rank, (blk,)))
+    from dataclasses import replace
+
+    an = InsituAnalysis(replace(pipe, timing=True))
+    for _ in range(a.warmup):
+        an.execute(da, fetch_image=False)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.default_stream()
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fused_ms, ntri = [], 0
+    e0.record(stream)
+    for _ in range(a.steps):
+        res = an.execute(da, fetch_image=False)
+        fused_ms.append(res.report.ms_fused)
+        ntri = res.report.n_triangles
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / a.steps
+    value = world * npts / (ms / 1e3)      # every rank holds npts (weak scaling)
+
+    # roofline of the dominant kernel (fused adaptor+grad+Q+MC pass)
+    peaks, peak_kind = _peaks()
+    fused = statistics.mean(fused_ms)
+    alg_bytes = npts * _bytes_read_per_point(case) + 48 * ntri
+    achieved = alg_bytes / (fused / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # ---- end-to-end through the reference-facing sink with host buffers ----
+    names = [("x", case.x), ("y", case.y), ("z", case.z)] + list(case.fields.items())
+    pinned = PinnedBuffer(sum(v.nbytes for _, v in names))
+    off, host = 0, {}
+    for k, v in names:
+        view = np.frombuffer((__import__("ctypes").c_byte * v.nbytes).from_address(pinned.ptr + off), dtype=np.float64)
+        view[:] = v.ravel()
+        host[k] = view.reshape(v.shape)
+        off += v.nbytes
+    hfields = tuple(FieldArray(k, POINT, case.fields[k].shape[0], host[k].ravel(), comp_stride=npts)
+                    for k in case.fields)
+    hblk = SemBlock(case.n_elements, host["x"], host["y"], host["z"], fields=hfields, element_offset=case.e0,
+                    n_elements_global=case.n_elements_global)
+    tmpdir = tempfile.mkdtemp(prefix="nkb_e2e_")
+    params = {**case.params, "width": str(a.width), "height": str(a.width), "dir": tmpdir}
+    sink = InsituSink(params, comm=comm)
+    e2e_steps = max(3, min(a.steps, 10))
+    step = 0
+    for _ in range(2):
+        sink.consume(Snapshot(0.0, step, rank, (hblk,)))
+        step += 1
+    barrier()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        sink.consume(Snapshot(0.0, step, rank, (hblk,)))
+        step += 1
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    h2d = sink.adaptor.h2d_bytes
+    d2h = a.width * a.width * 4 + 48
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded NekRS-layout SEM fields, synth.py)",
+        "config": {
+            "workload": f"{a.config}: RBC cylinder, {case.n_elements_global} elements N=7 "
+                        f"({world} x 32768; configs[1] per GPU)" if a.config == "c2" else a.config,
+            "elements_per_gpu": case.n_elements, "gll_points_per_gpu": npts,
+            "gll_points_total": npts * world,
+            "surfaces": case.params.get("iso", "") + (";slice " + case.params["slice"] if "slice" in case.params else ""),
+            "color": case.params.get("field"), "image": f"{a.width}x{a.width}",
+            "l2": f"inputs {npts * _bytes_read_per_point(case) / 1e9:.2f} GB/GPU >> 126 MB L2 (no flush needed)",
+            "parallelism": f"element partition x{world}, sort-last composite (NCCL min-reduce)",
+        },
+        "e2e": {"value": world * npts / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "InsituSink.consume(host pinned snapshot) -> H2D -> execute -> D2H RGBA -> PPM"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": "fused_kernel",
+                     "kernel_ms": fused, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
+                     "bytes_per_point": _bytes_read_per_point(case), "triangles": ntri},
+        "gpu_launches": 5 * a.steps,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(case, pipe, an.view_for(da), a)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(case, pipe, view, a, reps: int = 2) -> dict:
+    """CPU oracle port (oracle/sem_oracle.c), full step on all host cores."""
+    from oracle import oracle as orc
+
+    orc.build()
+    cores = _cores()
+    cf = orc.CaseFields(case.x, case.y, case.z, case.fields)
+    surf = [("iso", s.field, s.value) if s.kind == "iso" else ("slice", s.normal, s.value) for s in pipe.surfaces]
+    best = math.inf
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.pipeline_mt(cf, surf, pipe.color_field, view, pipe.width, pipe.height, cores)
+        best = min(best, time.perf_counter() - t0)
+    return {"value": case.n_points / best, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"full {case.n_elements}-element step (adaptor+Q+iso/slice+raster+resolve), "
+                      f"best of {reps}, C oracle, {cores} threads", "ms_per_step": best * 1e3}
+
+
+def run_reference(a):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    from paper_2312_09888_b200.analysis import ortho_view
+
+    orc.build()
+    cores = _cores()
+    case = _case_arrays(a.config, 0, 1)
+    pipe = _pipeline(case, a.width)
+    # bounded sample: first ~2 s worth of elements per step (measured rate ~1.3M pts/s/thread)
+    e_sample = min(case.n_elements, max(64, int(2.0 * 1.3e6 * cores / 512)))
+    sl = slice(0, e_sample * 512)
+    cf = orc.CaseFields(case.x[sl], case.y[sl], case.z[sl], {k: v[:, sl] for k, v in case.fields.items()})
+    b = (case.x.min(), case.x.max(), case.y.min(), case.y.max(), case.z.min(), case.z.max())
+    view = ortho_view(b, pipe.width, pipe.height, *pipe.view_dir)
+    surf = [("iso", s.field, s.value) if s.kind == "iso" else ("slice", s.normal, s.value) for s in pipe.surfaces]
+    for _ in range(a.warmup):
+        orc.pipeline_mt(cf, surf, pipe.color_field, view, pipe.width, pipe.height, cores)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        orc.pipeline_mt(cf, surf, pipe.color_field, view, pipe.width, pipe.height, cores)
+    dt = (time.perf_counter() - t0) / a.steps
+    v = e_sample * 512 / dt
+    sample = (f"{e_sample} of {case.n_elements} elements of {a.config} per step, full pipeline, "
+              f"C oracle port on {cores} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{a.config} (bounded CPU sample)", "image": f"{a.width}x{a.width}"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--width", type=int, default=1024)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

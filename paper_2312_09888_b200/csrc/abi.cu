@@ -548,12 +548,12 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   fp.tri = ctx->tri;
   fp.meta = p->emit_meta ? ctx->meta : nullptr;
   fp.tri_cap = ctx->tri_cap;
-  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
   // scan state: tile flags 0, counters {0, enc(+max), 0, 0}, ticket 0
   if (ctx->E > 0)
     NKB_CUDA(cudaMemsetAsync(ctx->tile_status, 0, sizeof(unsigned long long) * ctx->E, s));
   NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
   NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
   NKB_TRY(launch_fused(fp, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[1], s));
   NKB_TRY(launch_zbuf_clear(ctx->zbuf, npx, s));

@@ -93,9 +93,15 @@ class GpuRenderer:
     """GPU implementation of the reference's `render` (sinks.py:245-295)."""
 
     def __init__(self, ctx: Context | None = None):
-        self.ctx = ctx or default_context()
+        self._ctx = ctx
         self._staging: dict[tuple[int, str], DeviceArray] = {}
         self._rgb: DeviceArray | None = None
+
+    @property
+    def ctx(self) -> Context:
+        if self._ctx is None:        # created on first use: constructing a sink needs no GPU
+            self._ctx = default_context()
+        return self._ctx
 
     def render(self, s, field: str, cmap: ColorMap = DEFAULT_COLORMAP, width: int = 256, height: int = 256,
                vmin: float | None = None, vmax: float | None = None) -> ImageRGB:
@@ -197,8 +203,8 @@ class InsituSink:
         self.dir = Path(params.get("dir", "insitu_out"))
         self.pipeline = pipeline_from_params(params)
         self.comm = comm
-        ctx = comm.ctx if comm is not None else default_context()
-        self.adaptor = SemDataAdaptor(ctx, velocity=params.get("velocity", "velocity"))
+        self.velocity = params.get("velocity", "velocity")
+        self.adaptor: SemDataAdaptor | None = None   # created on first consume (needs the GPU)
         self.analysis = InsituAnalysis(self.pipeline)
         self.last = None
         root = comm is None or comm.rank == 0
@@ -207,6 +213,9 @@ class InsituSink:
             _probe_writable(self.dir)
 
     def consume(self, s) -> int:
+        if self.adaptor is None:
+            ctx = self.comm.ctx if self.comm is not None else default_context()
+            self.adaptor = SemDataAdaptor(ctx, velocity=self.velocity)
         self.adaptor.initialize(s)
         res = self.analysis.execute(self.adaptor)
         self.last = res

@@ -1,0 +1,73 @@
+"""Generate golden vectors from the REFERENCE implementation (run here, where
+/root/reference exists; the outputs are committed, the GPU box never reads
+/root/reference).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Fixtures (tests/golden/*.npz):
+  colormap.npz   DEFAULT_COLORMAP.apply (reference sinks.py:201-213) on
+                 seeded t samples incl. anchors, clipping, exact halves
+  render.npz     reference `render` (sinks.py:245-295) on seeded snapshots:
+                 scalar + ':mag', 1..4 blocks (assemble_global,
+                 data_model.py:188-225), explicit ranges, degenerate range,
+                 odd sizes, 1-pixel images, 3D (nk > 1) blocks
+  ppm.npz        write_ppm byte streams (sinks.py:298-303)
+"""
+from __future__ import annotations
+
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+from nekmini.data_model import POINT, Block, FieldArray, Snapshot  # noqa: E402
+from nekmini.sinks import DEFAULT_COLORMAP, ImageRGB, render, write_ppm  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from cases import RENDER_CASES, colormap_samples, snapshot_arrays  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def snapshot(seed, ni, nj, nk=1, nblocks=1, comps=2):
+    blocks = []
+    for temp, vel, ext in snapshot_arrays(seed, ni, nj, nk, nblocks, comps):
+        fields = (FieldArray("temperature", POINT, 1, temp), FieldArray("velocity", POINT, comps, vel))
+        blocks.append(Block((ext[0] * 0.5, 0.0, 0.0), (0.5, 0.25, 1.0), ext, fields))
+    return Snapshot(time=0.0, step=3, producer_id=0, blocks=tuple(blocks))
+
+
+def main():
+    t = colormap_samples()
+    rgb = DEFAULT_COLORMAP.apply(t)
+    np.savez_compressed(os.path.join(HERE, "colormap.npz"), rgb=rgb)
+
+    images = {}
+    for case in RENDER_CASES:
+        seed, ni, nj, nk, nb, comps, field, w, h, vmin, vmax = case
+        s = snapshot(seed, ni, nj, nk, nb, comps)
+        img = render(s, field, DEFAULT_COLORMAP, w, h, vmin, vmax)
+        images[f"case{seed}"] = np.frombuffer(img.pixels, np.uint8).copy()
+    np.savez_compressed(os.path.join(HERE, "render.npz"), **images)
+
+    with tempfile.TemporaryDirectory() as d:
+        ppms = {}
+        for (w, h) in ((1, 1), (3, 2), (256, 256)):
+            rng = np.random.default_rng(w * 1000 + h)
+            px = rng.integers(0, 256, size=3 * w * h, dtype=np.uint8).tobytes()
+            p = os.path.join(d, "x.ppm")
+            n = write_ppm(ImageRGB(w, h, px), p)
+            raw = open(p, "rb").read()
+            assert n == len(raw)
+            ppms[f"ppm_{w}x{h}"] = np.frombuffer(raw, np.uint8).copy()
+    np.savez_compressed(os.path.join(HERE, "ppm.npz"), **ppms)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,83 @@
+"""Multi-GPU sort-last composite over NCCL (libnekb200's ncclReduce of packed
+depth|scalar keys + range words).  The composited image must be bit-identical
+to the one-GPU image of the whole mesh (min is associative and commutative),
+for 2 and 4 ranks.  Needs >= 2 GPUs; the world-size-2/3 protocol on CPU is in
+tests/test_dist.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+W, H = 160, 120
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _image(rank, size, out_dir):
+    import torch.distributed as dist
+
+    from paper_2312_09888_b200 import synth
+    from paper_2312_09888_b200.adaptor import SemDataAdaptor
+    from paper_2312_09888_b200.analysis import InsituAnalysis, pipeline_from_params
+    from paper_2312_09888_b200.comm import Communicator
+    from paper_2312_09888_b200.context import Context
+    from paper_2312_09888_b200.data_model import POINT, FieldArray, SemBlock, Snapshot
+
+    nel = (4, 4, 6)
+    E = nel[0] * nel[1] * nel[2]
+    e0, e1 = synth.partition(E, rank, size)
+    c = synth.box(e0, e1, nel=nel)
+    ctx = Context(rank)
+    comm = Communicator.from_torch(ctx)
+    da = SemDataAdaptor(ctx)
+    fields = tuple(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=c.n_points) for k, v in c.fields.items())
+    da.initialize(Snapshot(0.0, 0, 0, (SemBlock(c.n_elements, c.x, c.y, c.z, fields=fields,
+                                                element_offset=e0, n_elements_global=E),)))
+    params = {**c.params, "width": str(W), "height": str(H)}
+    res = InsituAnalysis(pipeline_from_params(params)).execute(da, depth=True)
+    if rank == 0:
+        np.savez(os.path.join(out_dir, f"g{size}.npz"), rgba=res.rgba, dep=res.depth,
+                 n=res.report.n_triangles_global, rng=np.array(res.report.range))
+    dist.barrier()
+    comm.close()
+
+
+def _worker(rank, size, port, out_dir):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        _image(rank, size, out_dir)
+    finally:
+        dist.destroy_process_group()
+
+
+def _ngpus():
+    from paper_2312_09888_b200.context import device_count
+
+    return device_count()
+
+
+@pytest.mark.parametrize("size", [2, 4])
+def test_nccl_composite_equals_single_gpu(tmp_path, size):
+    if _ngpus() < size:
+        pytest.skip(f"needs {size} GPUs")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / f"g{size}.npz")
+    assert int(a["n"]) == int(b["n"])
+    assert np.array_equal(a["rng"], b["rng"])
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))

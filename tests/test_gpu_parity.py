@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path, called through the C ABI (Context -> ctypes ->
+libnekb200), against the CPU oracle on identical synthetic SEM fields.
+
+Bar (north star): connectivity, case indices, triangle counts bit-exact;
+derived fields bit-exact with the oracle (which is itself within 1e-12 of an
+independent numpy formulation, tests/test_oracle.py); images and depth
+bit-exact (per-pixel tolerance 0).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2312_09888_b200 import synth
+from paper_2312_09888_b200.adaptor import SemDataAdaptor
+from paper_2312_09888_b200.analysis import InsituAnalysis, Pipeline, Surface, ortho_view
+from paper_2312_09888_b200.data_model import POINT, FieldArray, SemBlock, Snapshot
+
+pytestmark = pytest.mark.gpu
+
+
+def _snapshot(case, step=0, aos=False):
+    fields = []
+    for k, v in case.fields.items():
+        if aos and v.shape[0] > 1:
+            fields.append(FieldArray(k, POINT, v.shape[0], v.T.ravel()))        # reference AoS layout
+        else:
+            fields.append(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=case.n_points))
+    blk = SemBlock(case.n_elements, case.x, case.y, case.z, fields=tuple(fields),
+                   element_offset=case.e0, n_elements_global=case.n_elements_global)
+    return Snapshot(0.0, step, 0, (blk,))
+
+
+def _orc_surfaces(pipe):
+    return [("iso", s.field, s.value) if s.kind == "iso" else ("slice", s.normal, s.value) for s in pipe.surfaces]
+
+
+def _run(ctx, case, pipe, aos=False):
+    da = SemDataAdaptor(ctx)
+    da.initialize(_snapshot(case, aos=aos))
+    res = InsituAnalysis(pipe).execute(da, depth=True)
+    return da, res
+
+
+def _check_against_oracle(ctx, case, pipe, res, meta=True):
+    cf = O.CaseFields(case.x, case.y, case.z, case.fields)
+    tri, m, (cmin, cmax) = O.mc(cf, _orc_surfaces(pipe), pipe.color_field)
+    assert res.report.n_triangles == len(tri)
+    gt, gm = ctx.triangles(with_meta=True)
+    if meta:
+        assert np.array_equal(gm, m), "case indices / emission order differ"
+    assert np.array_equal(gt.view(np.uint32), tri.view(np.uint32)), "triangle vertices differ"
+    lo = cmin if pipe.vmin is None else pipe.vmin
+    hi = cmax if pipe.vmax is None else pipe.vmax
+    assert res.report.range == (lo, hi)
+    z = O.raster(tri, res.view, pipe.width, pipe.height)
+    rgba, dep = O.resolve(z, pipe.width, pipe.height, lo, hi, pipe.anchors, pipe.background)
+    assert np.array_equal(res.rgba, rgba), f"{int(np.any(res.rgba != rgba, -1).sum())} pixels differ"
+    assert np.array_equal(res.depth.view(np.uint32), dep.view(np.uint32))
+
+
+BOX_PIPES = {
+    "q_iso": Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="temperature"),
+    "three_surfaces": Pipeline(surfaces=(Surface("iso", "Q", 0.5), Surface("iso", "temperature", 0.6),
+                                         Surface("slice", value=0.9, normal=(0.3, 1.0, 0.2))),
+                               color_field="temperature", view_dir=(30.0, 40.0)),
+    "colour_q": Pipeline(surfaces=(Surface("iso", "temperature", 0.6),), color_field="Q", width=100, height=77),
+    "colour_wmag": Pipeline(surfaces=(Surface("iso", "vorticity:mag", 1.0),), color_field="vorticity:mag"),
+    "colour_umag_range": Pipeline(surfaces=(Surface("iso", "velocity:mag", 0.6),), color_field="velocity:mag",
+                                  vmin=0.2, vmax=0.9),
+    "custom_cmap_bg": Pipeline(surfaces=(Surface("slice", value=0.5, normal=(0, 0, 1)),
+                                         Surface("slice", value=1.0, normal=(1, 0, 0))),
+                               color_field="temperature", background=(10, 20, 30, 40),
+                               anchors=((0.0, (0, 0, 0)), (0.3, (255, 0, 0)), (0.7, (0, 255, 0)),
+                                        (1.0, (255, 255, 255))), view_dir=(-120.0, 10.0)),
+    "four_surfaces": Pipeline(surfaces=(Surface("iso", "Q", -0.5), Surface("iso", "Q", 0.5),
+                                        Surface("iso", "temperature", 0.2),
+                                        Surface("slice", value=0.7, normal=(1, 1, 1))),
+                              color_field="Q", width=300, height=200),
+}
+
+
+@pytest.mark.parametrize("name", list(BOX_PIPES))
+def test_box_pipelines_bit_exact(ctx, name):
+    case = synth.box(nel=(4, 3, 3))
+    pipe = Pipeline(**{**BOX_PIPES[name].__dict__, "emit_meta": True})
+    _, res = _run(ctx, case, pipe)
+    _check_against_oracle(ctx, case, pipe, res)
+
+
+def test_taylor_green_c1_bit_exact(ctx):
+    case = synth.taylor_green()
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.1),), color_field="velocity:mag", width=256, height=256,
+                    view_dir=(35.0, 30.0), emit_meta=True)
+    _, res = _run(ctx, case, pipe)
+    _check_against_oracle(ctx, case, pipe, res)
+
+
+def test_aos_host_velocity_layout(ctx):
+    """Host velocity in the reference's component-fastest AoS layout (data_model.py:8-14)."""
+    case = synth.box(nel=(2, 2, 2))
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="velocity:mag", emit_meta=True)
+    _, res = _run(ctx, case, pipe, aos=True)
+    _check_against_oracle(ctx, case, pipe, res)
+
+
+def test_c2_full_config_matches_oracle(ctx):
+    """BASELINE configs[1] at full size (32,768 elements, 16.8M GLL points)."""
+    case = synth.make_case("c2")
+    from paper_2312_09888_b200.analysis import pipeline_from_params
+
+    pipe = pipeline_from_params({**case.params, "width": "512", "height": "512"})
+    _, res = _run(ctx, case, pipe)
+    cf = O.CaseFields(case.x, case.y, case.z, case.fields)
+    rgba, dep, ntri, rng = O.pipeline_mt(cf, _orc_surfaces(pipe), pipe.color_field, res.view, 512, 512,
+                                         os.cpu_count() or 8)
+    assert res.report.n_triangles == ntri
+    assert res.report.range == rng
+    assert np.array_equal(res.rgba, rgba)
+    assert np.array_equal(res.depth.view(np.uint32), dep.view(np.uint32))
+
+
+def test_triangle_buffer_growth_reruns_deterministically(ctx):
+    case = synth.box(nel=(2, 2, 2))
+    rng = np.random.default_rng(5)
+    noisy = rng.standard_normal(case.n_points)            # ~1 triangle per cell -> > initial capacity
+    case.fields["noise"] = noisy[None]
+    pipe = Pipeline(surfaces=(Surface("iso", "noise", 0.0), Surface("iso", "noise", 0.5),
+                              Surface("iso", "noise", -0.5), Surface("iso", "noise", 1.0)),
+                    color_field="noise", emit_meta=True)
+    from paper_2312_09888_b200.context import Context
+
+    fresh = Context(0)          # new context: initial capacity max(65536, 16 E)
+    _, res = _run(fresh, case, pipe)
+    assert res.report.n_triangles > 65536 and res.report.reran
+    _check_against_oracle(fresh, case, pipe, res)
+    _, res2 = _run(fresh, case, pipe)
+    assert not res2.report.reran and np.array_equal(res.rgba, res2.rgba)
+    fresh.close()
+
+
+def test_no_surfaces_gives_background(ctx):
+    case = synth.box(nel=(2, 1, 1))
+    pipe = Pipeline(surfaces=(), color_field="temperature", width=16, height=8, background=(1, 2, 3, 4))
+    _, res = _run(ctx, case, pipe)
+    assert res.report.n_triangles == 0
+    assert (res.rgba.reshape(-1, 4) == [1, 2, 3, 4]).all() and np.isinf(res.depth).all()
+
+
+def test_zero_elements_rank(ctx):
+    """A rank that owns no elements (E = 0) still executes (empty partition)."""
+    case = synth.box(0, 0, nel=(2, 2, 2))
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="temperature", width=8, height=8,
+                    view=tuple(float(v) for v in ortho_view((0, 2, 0, 1.5, 0, 1), 8, 8)))
+    _, res = _run(ctx, case, pipe)
+    assert res.report.n_triangles == 0 and (res.rgba[..., 3] == 0).all()
+
+
+def test_repeat_is_deterministic(ctx):
+    case = synth.box(nel=(3, 3, 3))
+    pipe = BOX_PIPES["three_surfaces"]
+    da, r1 = _run(ctx, case, pipe)
+    r2 = InsituAnalysis(pipe).execute(da, depth=True)
+    assert np.array_equal(r1.rgba, r2.rgba) and np.array_equal(r1.depth, r2.depth)
+
+
+# ---------------------------------------------------------------- DataAdaptor
+
+
+def test_get_mesh_connectivity_and_points(ctx):
+    case = synth.box(nel=(2, 2, 1))
+    da = SemDataAdaptor(ctx)
+    da.initialize(_snapshot(case))
+    md = da.get_mesh_metadata()
+    assert (md.n_elements, md.n_points, md.n_cells, md.cell_type) == (4, 2048, 1372, 12)
+    g = da.get_mesh()
+    conn = g.connectivity.to_host()
+    e, a, b, c = np.meshgrid(np.arange(4), np.arange(7), np.arange(7), np.arange(7), indexing="ij")
+    # cells ordered (e, c, b, a) with a fastest
+    e, c, b, a = (v.transpose(0, 3, 2, 1).ravel() for v in (e, a, b, c))
+    n0 = e * 512 + a + 8 * b + 64 * c
+    expect = np.stack([n0, n0 + 1, n0 + 9, n0 + 8, n0 + 64, n0 + 65, n0 + 73, n0 + 72], axis=1)
+    assert np.array_equal(conn, expect)
+    assert np.array_equal(g.offsets.to_host(), 8 * np.arange(1373))
+    assert (g.types.to_host() == 12).all()
+    pts = g.points.to_host()
+    assert np.array_equal(pts, np.stack([case.x, case.y, case.z], axis=1))
+
+
+def test_add_array_exports_bit_exact(ctx):
+    case = synth.box(nel=(3, 2, 2))
+    da = SemDataAdaptor(ctx)
+    da.initialize(_snapshot(case))
+    cf = O.CaseFields(case.x, case.y, case.z, case.fields)
+    q, wm, vort, um = O.derived(cf)
+    assert np.array_equal(da.add_array("mesh", POINT, "Q").values.to_host(), q)
+    assert np.array_equal(da.add_array("mesh", POINT, "vorticity:mag").values.to_host(), wm)
+    v = da.add_array("mesh", POINT, "vorticity")
+    assert v.components == 3 and np.array_equal(v.values.to_host(), vort)
+    assert np.array_equal(da.add_array("mesh", POINT, "velocity:mag").values.to_host(), um)
+    vel = da.add_array("mesh", POINT, "velocity")
+    assert np.array_equal(vel.values.to_host(), case.fields["velocity"].T.ravel())   # AoS
+    x, y, z = case.x, case.y, case.z
+    u = case.fields["velocity"]
+    qn, _, _, g2 = O.derived_numpy(x, y, z, u[0], u[1], u[2])
+    assert np.max(np.abs(q - qn)) <= 1e-12 * g2.max()
+
+
+def test_errors_map_to_reference_exceptions(ctx):
+    case = synth.box(nel=(1, 1, 1))
+    da = SemDataAdaptor(ctx)
+    da.initialize(_snapshot(case))
+    an = InsituAnalysis(Pipeline(surfaces=(Surface("iso", "nope", 0.0),), color_field="temperature"))
+    with pytest.raises(ValueError, match="no field named"):
+        an.execute(da)
+    an = InsituAnalysis(Pipeline(surfaces=(), color_field="velocity"))
+    with pytest.raises(ValueError, match="components"):
+        an.execute(da)
+    an = InsituAnalysis(Pipeline(surfaces=(), color_field="temperature:grad"))
+    with pytest.raises(ValueError, match="derived scalar"):
+        an.execute(da)
+    with pytest.raises(ValueError, match="order"):
+        ctx.mesh_set(1, 0, 0, 0, order=5)

@@ -18,8 +18,10 @@ Lorensen/Bourke table is third-party data we do not vendor.  So the table is
   share a face make the same choice and the surface is crack-free;
 * segments are oriented with the inside region on their left when the face is
   viewed from outside the cube, chained into closed loops, and each loop is
-  fan-triangulated from its first vertex; the resulting triangle normals
-  (right-hand rule) point from the inside region to the outside.
+  fan-triangulated from the first vertex whose fan has no diagonal lying in
+  a cube face (so neighbouring sub-hexes never stack triangles on a shared
+  face segment); triangle normals (right-hand rule) point from the inside
+  region to the outside.
 
 Output: the same text to `paper_2312_09888_b200/csrc/mc_tables.h` (product)
 and `oracle/mc_tables.h` (checker).  `tests/test_mc_tables.py` checks the two
@@ -113,11 +115,33 @@ def case_polygons(mask: int) -> list[list[int]]:
     return loops
 
 
+def _share_face(e1: int, e2: int) -> bool:
+    va, vb = set(EDGES[e1]), set(EDGES[e2])
+    return any(va <= set(fv) and vb <= set(fv) for fv, _ in FACES)
+
+
+def _fan_start(loop: list[int]) -> int:
+    """First loop vertex whose fan has no diagonal lying in a cube face.
+
+    A diagonal between two crossing points of the same face would lie in
+    that face; the neighbouring sub-hex can make the same choice from its
+    side, giving four triangles on one segment (a non-manifold seam).
+    """
+    n = len(loop)
+    for s0 in range(n):
+        diags = [loop[(s0 + i) % n] for i in range(2, n - 1)]
+        if not any(_share_face(loop[s0], d) for d in diags):
+            return s0
+    raise AssertionError(f"no face-free fan for loop {loop}")
+
+
 def case_triangles(mask: int) -> list[tuple[int, int, int]]:
     tris = []
     for loop in case_polygons(mask):
-        for i in range(1, len(loop) - 1):
-            tris.append((loop[0], loop[i], loop[i + 1]))
+        s0 = _fan_start(loop)
+        lp = loop[s0:] + loop[:s0]
+        for i in range(1, len(lp) - 1):
+            tris.append((lp[0], lp[i], lp[i + 1]))
     return tris
 
 
