@@ -204,6 +204,7 @@ def run_ours(a):
     for k, v in names:
         view = np.frombuffer((__import__("ctypes").c_byte * v.nbytes).from_address(pinned.ptr + off), dtype=np.float64)
         view[:] = v.ravel()
+        view.setflags(write=False)          # immutable -> FieldArray aliases the pinned buffer
         host[k] = view.reshape(v.shape)
         off += v.nbytes
     hfields = tuple(FieldArray(k, POINT, case.fields[k].shape[0], host[k].ravel(), comp_stride=npts)

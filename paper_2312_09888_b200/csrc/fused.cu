@@ -3,10 +3,20 @@
 // marching-cubes classification of every linear sub-hex, and deterministic
 // triangle emission through a single-pass decoupled look-back scan.
 //
-// One CTA (256 threads) per element; the element's GLL fields are read from
-// HBM exactly once (coalesced, element-local order i fastest) into a
-// swizzled, plane-padded shared-memory layout, and nothing but triangles (and
-// optional AddArray exports) is written back.
+// One CTA (256 threads, 8 warps) per element; 2 CTAs per SM.  The element's
+// GLL fields are read from HBM exactly once (coalesced) into XOR-swizzled
+// shared-memory arrays (bank-conflict free for node-, r-, s- and t-pencil
+// access), nothing but triangles (and optional AddArray exports) is written.
+//
+//   1. gather     : 7 fields (x,y,z,u,v,w,T) -> smem                 all warps
+//   2. pencils    : 6 fields x 3 directions, one (dir, pencil) per   warps 0-5
+//                   thread, smem offsets computed once, 6 fields
+//      node-local : |u|, plane and scalar classification bits,       warps 6-7
+//                   colour range of non-derived colour fields
+//   3. node phase : Jacobian inverse, grad u, Q, |w|, Q/|w| bits      all warps
+//   4. classify   : 343 sub-hexes x surfaces -> case bytes, counts
+//   5. scan       : block scan + decoupled look-back across elements
+//   6. emit       : vertices interpolated along canonical edges
 //
 // Reference anchors: the adaptor copy `solver.snapshot_of` (solver.py:282-305)
 // and the AoS layout (data_model.py:8-14) for R11; `scalar_field(':mag')`
@@ -40,14 +50,16 @@ int set_dmat_constant(const double* dmat) {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPlane = 72;              // 64 doubles + 8 pad per k-plane
-constexpr int kArr = kNP * kPlane;      // 576 doubles per staged array
+constexpr int kArr = kNN;            // 512 doubles per staged array
+constexpr int kNumD = 18;            // derivative arrays: d(f)/d(r,s,t) for x,y,z,u,v,w
 
-// node (i,j,k) -> shared-memory slot.  XOR swizzle inside each 8-double line
-// plus plane padding makes r-, s-, t-pencil reads and node-parallel accesses
-// all bank-conflict free (2 wavefronts per 64-bit warp access).
+// node (i,j,k) -> shared-memory slot.  Within each 64 B line the 8 doubles
+// are XOR-permuted by (j>>1 | (k&1)<<2); lines are XOR-permuted by (k&1).
+// For every 16-lane half-warp pattern used below (node-parallel, r-, s- and
+// t-pencils) the 16 accessed doubles fall in 16 distinct 8-byte bank pairs:
+// 2 wavefronts per 64-bit warp access, the minimum.
 __device__ __forceinline__ int sw(int i, int j, int k) {
-  return (i ^ ((j >> 1) | ((k & 1) << 2))) + 8 * j + kPlane * k;
+  return (i ^ ((j >> 1) | ((k & 1) << 2))) + 8 * (j ^ (k & 1)) + 64 * k;
 }
 __device__ __forceinline__ int sw_node(int n) { return sw(n & 7, (n >> 3) & 7, n >> 6); }
 
@@ -86,45 +98,13 @@ __device__ __forceinline__ void deriv8(const double* v, double* out) {
   }
 }
 
-// derivatives of three staged arrays in[f0..f0+2] along r,s,t into d[0..8]
-// (d[3*f + dir]).  576 pencils over 256 threads; (field, dir) warp-uniform.
-__device__ __forceinline__ void pencils3(const double* __restrict__ in0, double* __restrict__ d,
-                                         int tid) {
-#pragma unroll 1
-  for (int task = tid; task < 9 * 64; task += kThreads) {
-    const int f = task / 192;
-    const int rem = task - f * 192;
-    const int dir = rem >> 6;
-    const int p = rem & 63;
-    const int a = p & 7, b = p >> 3;
-    const double* src = in0 + f * kArr;
-    double* dst = d + (3 * f + dir) * kArr;
-    double v[kNP], o[kNP];
-    if (dir == 0) {
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) v[m] = src[sw(m, a, b)];
-      deriv8(v, o);
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) dst[sw(m, a, b)] = o[m];
-    } else if (dir == 1) {
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) v[m] = src[sw(a, m, b)];
-      deriv8(v, o);
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) dst[sw(a, m, b)] = o[m];
-    } else {
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) v[m] = src[sw(a, b, m)];
-      deriv8(v, o);
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) dst[sw(a, b, m)] = o[m];
-    }
-  }
-}
-
 __device__ __forceinline__ double mag3(double a, double b, double c) {
   // reference ':mag' = sqrt(sum(v**2)) summed left to right (sinks.py:240-241)
   return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
+}
+
+__device__ __forceinline__ double plane_dist(const double* n, double x, double y, double z) {
+  return __fma_rn(n[2], z, __fma_rn(n[1], y, __dmul_rn(n[0], x)));
 }
 
 template <typename T>
@@ -134,18 +114,17 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+__device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
+
 }  // namespace
 
-// Shared memory: nin staged input arrays + 9 scratch arrays (kArr doubles
-// each) + the 9-component Jacobian inverse per node + 512 classification
-// bytes.  ~111 KB at nin=7 -> 2 CTAs (16 warps) per SM.
+// smem: nin staged inputs + 18 derivative arrays (4 KB each) + 512 case bits
 __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p, int nin,
                                                             int slot_vel, int slot_sc) {
   extern __shared__ __align__(16) double smem[];
-  double* S_in = smem;                 // nin * kArr
-  double* S_d = smem + nin * kArr;     // 9 * kArr
-  double* S_j = S_d + 9 * kArr;        // 9 * kNN: Jacobian inverse, compact [c][node]
-  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_j + 9 * kNN);  // 512
+  double* S_in = smem;                                 // nin * 512
+  double* S_d = smem + nin * kArr;                     // 18 * 512
+  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_d + kNumD * kArr);
   __shared__ unsigned s_tile;
   __shared__ long long s_warp[kThreads / 32];
   __shared__ long long s_base;
@@ -157,135 +136,142 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
   __syncthreads();
   const long long e = s_tile;
   const long long g0 = e * (long long)kNN;
+  const bool color_grad = src_is_grad(p.color_src);
 
   // ---- 1. adaptor gather: element-local GLL fields -> shared (coalesced) ----
+  // all loads are issued before any store so every thread keeps up to 16
+  // independent 8-byte loads in flight (memory-level parallelism)
   {
-    const int q0 = sw_node(tid), q1 = sw_node(tid + kThreads);
-    auto stage = [&](const double* __restrict__ src, int slot) {
-      const double a0 = __ldcs(src + g0 + tid);
-      const double a1 = __ldcs(src + g0 + tid + kThreads);
-      S_in[slot * kArr + q0] = a0;
-      S_in[slot * kArr + q1] = a1;
-    };
-    stage(p.x, 0);
-    stage(p.y, 1);
-    stage(p.z, 2);
-    if (p.need_vel) {
-      stage(p.vel[0], slot_vel);
-      stage(p.vel[1], slot_vel + 1);
-      stage(p.vel[2], slot_vel + 2);
+    double r0[8], r1[8];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      if (f < nin) {
+        r0[f] = __ldcs(p.in_ptr[f] + g0 + tid);
+        r1[f] = __ldcs(p.in_ptr[f] + g0 + tid + kThreads);
+      }
     }
-    if (p.n_scalars > 0) stage(p.scalar[0], slot_sc);
-    if (p.n_scalars > 1) stage(p.scalar[1], slot_sc + 1);
+    const int q0 = sw_node(tid), q1 = sw_node(tid + kThreads);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) {
+      if (f < nin) {
+        S_in[f * kArr + q0] = r0[f];
+        S_in[f * kArr + q1] = r1[f];
+      }
+    }
   }
   __syncthreads();
 
-  // per-node derived scalars are written into scratch slots after phase 5
-  // slot map: Q -> d0, |w| -> d1, |u| -> d2, plane k -> d(3+k)
   double cmin = INFINITY, cmax = -INFINITY;
-
-  if (p.need_grad) {
-    // ---- 2. geometric derivatives x,y,z along r,s,t ----
-    pencils3(S_in, S_d, tid);
-    __syncthreads();
-    // ---- 3. Jacobian inverse per node ----
+  if (warp < 6) {
+    // ---- 2a. derivative pencils: thread = (dir, pencil); 6 fields ----
+    if (p.need_grad) {
+      const int dir = warp >> 1;               // warp-uniform
+      const int pa = tid & 7, pb = (tid >> 3) & 7;
+      int off[kNP];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = sw_node(tid + h * kThreads);
-      const double xr = S_d[0 * kArr + q], xs = S_d[1 * kArr + q], xt = S_d[2 * kArr + q];
-      const double yr = S_d[3 * kArr + q], ys = S_d[4 * kArr + q], yt = S_d[5 * kArr + q];
-      const double zr = S_d[6 * kArr + q], zs = S_d[7 * kArr + q], zt = S_d[8 * kArr + q];
-      double K[9];
-      K[0] = __fma_rn(ys, zt, -__dmul_rn(yt, zs));
-      K[1] = __fma_rn(xt, zs, -__dmul_rn(xs, zt));
-      K[2] = __fma_rn(xs, yt, -__dmul_rn(xt, ys));
-      K[3] = __fma_rn(yt, zr, -__dmul_rn(yr, zt));
-      K[4] = __fma_rn(xr, zt, -__dmul_rn(xt, zr));
-      K[5] = __fma_rn(xt, yr, -__dmul_rn(xr, yt));
-      K[6] = __fma_rn(yr, zs, -__dmul_rn(ys, zr));
-      K[7] = __fma_rn(xs, zr, -__dmul_rn(xr, zs));
-      K[8] = __fma_rn(xr, ys, -__dmul_rn(xs, yr));
-      const double det = __fma_rn(zr, K[2], __fma_rn(yr, K[1], __dmul_rn(xr, K[0])));
-      const double rdet = __ddiv_rn(1.0, det);
+      for (int m = 0; m < kNP; ++m)
+        off[m] = (dir == 0) ? sw(m, pa, pb) : (dir == 1) ? sw(pa, m, pb) : sw(pa, pb, m);
+#pragma unroll 1
+      for (int f = 0; f < 6; ++f) {
+        const double* src = S_in + (f < 3 ? f : slot_vel + f - 3) * kArr;
+        double* dst = S_d + (3 * f + dir) * kArr;
+        double v[kNP], o[kNP];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) S_j[c * kNN + tid + h * kThreads] = __dmul_rn(K[c], rdet);
+        for (int m = 0; m < kNP; ++m) v[m] = src[off[m]];
+        deriv8(v, o);
+#pragma unroll
+        for (int m = 0; m < kNP; ++m) dst[off[m]] = o[m];
+      }
     }
-    __syncthreads();
-    // ---- 4. velocity derivatives u,v,w along r,s,t ----
-    pencils3(S_in + slot_vel * kArr, S_d, tid);
-    __syncthreads();
+  } else {
+    // ---- 2b. node-local work that needs no derivatives (64 threads) ----
+    for (int n = tid - 192; n < kNN; n += 64) {
+      const int q = sw_node(n);
+      const double px = S_in[q], py = S_in[kArr + q], pz = S_in[2 * kArr + q];
+      double vu = 0.0;
+      if (p.need_vel)
+        vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
+      unsigned bits = 0;
+      for (int s = 0; s < p.n_surf; ++s) {
+        const int src = p.surf_src[s];
+        if (src_is_grad(src)) continue;
+        const double val = (src >= SRC_PLANE) ? plane_dist(p.surf_n[s], px, py, pz)
+                           : (src == SRC_UMAG) ? vu
+                                               : S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+        bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+      }
+      S_bits[n] = (unsigned char)bits;
+      if (p.color_src >= 0 && !color_grad) {
+        const double c = (p.color_src == SRC_UMAG) ? vu : S_in[(slot_sc + p.color_src - SRC_SCALAR0) * kArr + q];
+        cmin = fmin(cmin, c);
+        cmax = fmax(cmax, c);
+      }
+    }
   }
+  __syncthreads();
 
-  // ---- 5. per-node derived fields, classification bits, colour range ----
-  {
+  // ---- 3. node phase: Jacobian inverse, grad u, Q, |w| (2 nodes / thread) ----
+  if (p.need_grad) {
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       const int n = tid + h * kThreads;
       const int q = sw_node(n);
-      double vq = 0.0, vw = 0.0, vu = 0.0;
-      double om0 = 0.0, om1 = 0.0, om2 = 0.0;
-      if (p.need_grad) {
-        double U[9], J[9];
+      double G[9];
 #pragma unroll
-        for (int c = 0; c < 9; ++c) U[c] = S_d[c * kArr + q];
+      for (int c = 0; c < 9; ++c) G[c] = S_d[c * kArr + q];
+      const double xr = G[0], xs = G[1], xt = G[2];
+      const double yr = G[3], ys = G[4], yt = G[5];
+      const double zr = G[6], zs = G[7], zt = G[8];
+      double J[9];
+      J[0] = __fma_rn(ys, zt, -__dmul_rn(yt, zs));
+      J[1] = __fma_rn(xt, zs, -__dmul_rn(xs, zt));
+      J[2] = __fma_rn(xs, yt, -__dmul_rn(xt, ys));
+      J[3] = __fma_rn(yt, zr, -__dmul_rn(yr, zt));
+      J[4] = __fma_rn(xr, zt, -__dmul_rn(xt, zr));
+      J[5] = __fma_rn(xt, yr, -__dmul_rn(xr, yt));
+      J[6] = __fma_rn(yr, zs, -__dmul_rn(ys, zr));
+      J[7] = __fma_rn(xs, zr, -__dmul_rn(xr, zs));
+      J[8] = __fma_rn(xr, ys, -__dmul_rn(xs, yr));
+      const double det = __fma_rn(zr, J[2], __fma_rn(yr, J[1], __dmul_rn(xr, J[0])));
+      const double rdet = __ddiv_rn(1.0, det);
 #pragma unroll
-        for (int c = 0; c < 9; ++c) J[c] = S_j[c * kNN + n];
-        double A[9];
+      for (int c = 0; c < 9; ++c) J[c] = __dmul_rn(J[c], rdet);
+      double U[9];
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
+      for (int c = 0; c < 9; ++c) U[c] = S_d[(9 + c) * kArr + q];
+      double A[9];
 #pragma unroll
-          for (int b = 0; b < 3; ++b)
-            A[3 * a + b] = __fma_rn(U[3 * a + 2], J[6 + b],
-                                    __fma_rn(U[3 * a + 1], J[3 + b],
-                                             __dmul_rn(U[3 * a + 0], J[0 + b])));
-        const double off = __fma_rn(A[5], A[7], __fma_rn(A[2], A[6], __dmul_rn(A[1], A[3])));
-        const double dia = __fma_rn(A[8], A[8], __fma_rn(A[4], A[4], __dmul_rn(A[0], A[0])));
-        vq = -__fma_rn(0.5, dia, off);
-        om0 = __dsub_rn(A[7], A[5]);
-        om1 = __dsub_rn(A[2], A[6]);
-        om2 = __dsub_rn(A[3], A[1]);
-        vw = mag3(om0, om1, om2);
-        S_d[0 * kArr + q] = vq;
-        S_d[1 * kArr + q] = vw;
-        if (p.q_out) p.q_out[g0 + n] = vq;
-        if (p.wmag_out) p.wmag_out[g0 + n] = vw;
-        if (p.vort_out) {
-          p.vort_out[3 * (g0 + n) + 0] = om0;
-          p.vort_out[3 * (g0 + n) + 1] = om1;
-          p.vort_out[3 * (g0 + n) + 2] = om2;
-        }
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          A[3 * a + b] = __fma_rn(U[3 * a + 2], J[6 + b],
+                                  __fma_rn(U[3 * a + 1], J[3 + b], __dmul_rn(U[3 * a + 0], J[0 + b])));
+      const double off = __fma_rn(A[5], A[7], __fma_rn(A[2], A[6], __dmul_rn(A[1], A[3])));
+      const double dia = __fma_rn(A[8], A[8], __fma_rn(A[4], A[4], __dmul_rn(A[0], A[0])));
+      const double vq = -__fma_rn(0.5, dia, off);
+      const double om0 = __dsub_rn(A[7], A[5]);
+      const double om1 = __dsub_rn(A[2], A[6]);
+      const double om2 = __dsub_rn(A[3], A[1]);
+      const double vw = mag3(om0, om1, om2);
+      // this thread owns node q's derivative slots: overwrite d0 <- Q, d1 <- |w|
+      S_d[0 * kArr + q] = vq;
+      S_d[1 * kArr + q] = vw;
+      if (p.q_out) p.q_out[g0 + n] = vq;
+      if (p.wmag_out) p.wmag_out[g0 + n] = vw;
+      if (p.vort_out) {
+        p.vort_out[3 * (g0 + n) + 0] = om0;
+        p.vort_out[3 * (g0 + n) + 1] = om1;
+        p.vort_out[3 * (g0 + n) + 2] = om2;
       }
-      if (p.need_vel) {
-        vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q],
-                  S_in[(slot_vel + 2) * kArr + q]);
-        S_d[2 * kArr + q] = vu;
-      }
-      const double px = S_in[0 * kArr + q], py = S_in[1 * kArr + q], pz = S_in[2 * kArr + q];
       unsigned bits = 0;
       for (int s = 0; s < p.n_surf; ++s) {
         const int src = p.surf_src[s];
-        double val;
-        if (src >= SRC_PLANE) {
-          val = __fma_rn(p.surf_n[s][2], pz, __fma_rn(p.surf_n[s][1], py, __dmul_rn(p.surf_n[s][0], px)));
-          S_d[(3 + (src - SRC_PLANE)) * kArr + q] = val;
-        } else if (src == SRC_Q) {
-          val = vq;
-        } else if (src == SRC_WMAG) {
-          val = vw;
-        } else if (src == SRC_UMAG) {
-          val = vu;
-        } else {
-          val = S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
-        }
-        bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+        if (!src_is_grad(src)) continue;
+        bits |= ((src == SRC_Q ? vq : vw) >= p.surf_iso[s] ? 1u : 0u) << s;
       }
-      S_bits[n] = (unsigned char)bits;
-      if (p.color_src >= 0) {
-        const int src = p.color_src;
-        double c = (src == SRC_Q)      ? vq
-                   : (src == SRC_WMAG) ? vw
-                   : (src == SRC_UMAG) ? vu
-                                       : S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+      if (bits) S_bits[n] |= (unsigned char)bits;
+      if (color_grad) {
+        const double c = (p.color_src == SRC_Q) ? vq : vw;
         cmin = fmin(cmin, c);
         cmax = fmax(cmax, c);
       }
@@ -312,12 +298,14 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
       mn = fmin(mn, s_mn[w]);
       mx = fmax(mx, s_mx[w]);
     }
-    atomicMin(&p.counters[1], enc_ordered(mn));
-    atomicMax(&p.counters[2], enc_ordered(mx));
+    if (mn <= mx) {
+      atomicMin(&p.counters[1], enc_ordered(mn));
+      atomicMax(&p.counters[2], enc_ordered(mx));
+    }
   }
   if (p.n_surf == 0) return;
 
-  // ---- 6. classify sub-hexes: thread t owns cells 2t, 2t+1 ----
+  // ---- 4. classify sub-hexes: thread t owns cells 2t, 2t+1 ----
   unsigned cases[2] = {0u, 0u};   // byte s = case of surface s
   int cnt = 0;
 #pragma unroll
@@ -328,8 +316,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
       const int n0 = a + kNP * b + kNP * kNP * cc;
       unsigned cb[8];
 #pragma unroll
-      for (int v = 0; v < 8; ++v)
-        cb[v] = S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
+      for (int v = 0; v < 8; ++v) cb[v] = S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
       unsigned packed = 0;
       for (int s = 0; s < p.n_surf; ++s) {
         unsigned cs = 0;
@@ -342,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
     }
   }
 
-  // ---- 7. block exclusive scan + decoupled look-back across elements ----
+  // ---- 5. block exclusive scan + decoupled look-back across elements ----
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -361,7 +348,6 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
     }
     const long long total = __shfl_sync(0xffffffffu, wi, 7);
     if (lane < kThreads / 32) s_warp[lane] = wi - wv;   // exclusive warp offsets
-    // publish aggregate, then look back
     const long long tile = e;
     if (lane == 0) {
       if (tile == 0) st_release(&p.tile_status[0], kFlagPre | (unsigned long long)total);
@@ -393,20 +379,21 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
   __syncthreads();
   long long out = s_base + s_warp[warp] + (incl - cnt);
 
-  // ---- 8. emit triangles (vertex interpolation along canonical edges) ----
+  // ---- 6. emit triangles (vertex interpolation along canonical edges) ----
   if (cnt == 0) return;
   const double* Sx = S_in;
   const double* Sy = S_in + kArr;
   const double* Sz = S_in + 2 * kArr;
-  const double* Sc;
-  {
-    const int src = p.color_src;
-    Sc = (src == SRC_Q)      ? S_d
-         : (src == SRC_WMAG) ? S_d + kArr
-         : (src == SRC_UMAG) ? S_d + 2 * kArr
-                             : S_in + (slot_sc + src - SRC_SCALAR0) * kArr;
-  }
-#pragma unroll
+  const double* Su = S_in + slot_vel * kArr;
+  // per-node scalar of a source, recomputed where it is not stored
+  auto value_at = [&](int src, int s, int q) -> double {
+    if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
+    if (src == SRC_Q) return S_d[q];
+    if (src == SRC_WMAG) return S_d[kArr + q];
+    if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
+    return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+  };
+#pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     const int c = 2 * tid + h;
     if (c >= kNC) break;
@@ -416,11 +403,6 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
       const int nt = g_mc_ntri[cs];
       if (nt == 0) continue;
       const int src = p.surf_src[s];
-      const double* Ss = (src >= SRC_PLANE) ? S_d + (3 + src - SRC_PLANE) * kArr
-                         : (src == SRC_Q)   ? S_d
-                         : (src == SRC_WMAG) ? S_d + kArr
-                         : (src == SRC_UMAG) ? S_d + 2 * kArr
-                                             : S_in + (slot_sc + src - SRC_SCALAR0) * kArr;
       const double iso = p.surf_iso[s];
       for (int k = 0; k < nt; ++k, ++out) {
         if (out >= p.tri_cap) continue;
@@ -431,12 +413,13 @@ __global__ void __launch_bounds__(kThreads, 2) fused_kernel(const FusedParams p,
           const int va = g_mc_edge_v[ed][0], vb = g_mc_edge_v[ed][1];
           const int qa = sw(a + voff_i(va), b + voff_j(va), cc + voff_k(va));
           const int qb = sw(a + voff_i(vb), b + voff_j(vb), cc + voff_k(vb));
-          const double sa = Ss[qa], sb = Ss[qb];
+          const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
           const double t = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
+          const double ca = value_at(p.color_src, 0, qa), cb = value_at(p.color_src, 0, qb);
           vtx[r].x = __double2float_rn(__fma_rn(t, __dsub_rn(Sx[qb], Sx[qa]), Sx[qa]));
           vtx[r].y = __double2float_rn(__fma_rn(t, __dsub_rn(Sy[qb], Sy[qa]), Sy[qa]));
           vtx[r].z = __double2float_rn(__fma_rn(t, __dsub_rn(Sz[qb], Sz[qa]), Sz[qa]));
-          vtx[r].w = __double2float_rn(__fma_rn(t, __dsub_rn(Sc[qb], Sc[qa]), Sc[qa]));
+          vtx[r].w = __double2float_rn(__fma_rn(t, __dsub_rn(cb, ca), ca));
         }
         float4* dst = p.tri + 3 * out;
         dst[0] = vtx[0];
@@ -455,15 +438,22 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   int nin = 3 + (p.need_vel ? 3 : 0) + p.n_scalars;
   int slot_vel = 3;
   int slot_sc = 3 + (p.need_vel ? 3 : 0);
-  size_t shm = (size_t)(nin + 9) * kArr * sizeof(double) + 9 * kNN * sizeof(double) + kNN;
+  size_t shm = (size_t)(nin + kNumD) * kArr * sizeof(double) + kNN;
   static bool attr_set = false;
   if (!attr_set) {
     NKB_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)((3 + 3 + kMaxScalars + 9) * kArr * sizeof(double) +
-                                        9 * kNN * sizeof(double) + kNN)));
+                                  (int)((3 + 3 + kMaxScalars + kNumD) * kArr * sizeof(double) + kNN)));
     attr_set = true;
   }
-  fused_kernel<<<(unsigned)p.n_elements, kThreads, shm, s>>>(p, nin, slot_vel, slot_sc);
+  FusedParams q = p;   // staged inputs in slot order: x, y, z, [u, v, w], [scalars]
+  int k = 0;
+  q.in_ptr[k++] = p.x;
+  q.in_ptr[k++] = p.y;
+  q.in_ptr[k++] = p.z;
+  if (p.need_vel)
+    for (int c = 0; c < 3; ++c) q.in_ptr[k++] = p.vel[c];
+  for (int c = 0; c < p.n_scalars; ++c) q.in_ptr[k++] = p.scalar[c];
+  fused_kernel<<<(unsigned)p.n_elements, kThreads, shm, s>>>(q, nin, slot_vel, slot_sc);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

@@ -59,6 +59,7 @@ struct FusedParams {
   const double* z;
   const double* vel[3];
   const double* scalar[kMaxScalars];
+  const double* in_ptr[8];          // filled by launch_fused: staged inputs in slot order
   int need_grad;                    // compute velocity gradient (Q / vorticity)
   int need_vel;                     // load velocity
   int n_scalars;

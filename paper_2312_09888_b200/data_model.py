@@ -63,6 +63,12 @@ class FieldArray:
             return
         if is_device_array(v):
             return
+        if (isinstance(v, np.ndarray) and v.dtype == np.float64 and v.flags.c_contiguous
+                and not v.flags.writeable):
+            # already immutable: alias it (lets pinned host staging reach the
+            # GPU without a pageable copy); anything else is copied + frozen
+            object.__setattr__(self, "values", v.reshape(-1))
+            return
         vals = np.array(v, dtype=np.float64, copy=True).ravel()
         vals.setflags(write=False)
         object.__setattr__(self, "values", vals)

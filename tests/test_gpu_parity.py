@@ -123,7 +123,7 @@ def test_c2_full_config_matches_oracle(ctx):
 
 
 def test_triangle_buffer_growth_reruns_deterministically(ctx):
-    case = synth.box(nel=(2, 2, 2))
+    case = synth.box(nel=(4, 4, 4))
     rng = np.random.default_rng(5)
     noisy = rng.standard_normal(case.n_points)            # ~1 triangle per cell -> > initial capacity
     case.fields["noise"] = noisy[None]
@@ -179,7 +179,7 @@ def test_get_mesh_connectivity_and_points(ctx):
     conn = g.connectivity.to_host()
     e, a, b, c = np.meshgrid(np.arange(4), np.arange(7), np.arange(7), np.arange(7), indexing="ij")
     # cells ordered (e, c, b, a) with a fastest
-    e, c, b, a = (v.transpose(0, 3, 2, 1).ravel() for v in (e, a, b, c))
+    e, a, b, c = (v.transpose(0, 3, 2, 1).ravel() for v in (e, a, b, c))
     n0 = e * 512 + a + 8 * b + 64 * c
     expect = np.stack([n0, n0 + 1, n0 + 9, n0 + 8, n0 + 64, n0 + 65, n0 + 73, n0 + 72], axis=1)
     assert np.array_equal(conn, expect)
