@@ -108,8 +108,9 @@ struct nkb_ctx {
   std::string vel_name = "velocity";
   double gll[kNP], D[kNP * kNP];
   // step scratch (library-owned)
-  unsigned long long* tile_status = nullptr;
-  int64_t tile_cap = 0;
+  int* elem_count = nullptr;                  // ordered mode: per-element triangle counts
+  long long* elem_offset = nullptr;           // ordered mode: exclusive scan
+  int64_t elem_cap = 0;
   unsigned long long* counters = nullptr;   // [0] ntri [1] enc min [2] enc max [3] ntri global; then ticket
   unsigned int* ticket = nullptr;
   float4* tri = nullptr;
@@ -199,7 +200,8 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
-  cudaFree(ctx->tile_status);
+  cudaFree(ctx->elem_count);
+  cudaFree(ctx->elem_offset);
   cudaFree(ctx->counters);
   cudaFree(ctx->tri);
   cudaFree(ctx->meta);
@@ -236,12 +238,6 @@ int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order, const double* x, c
   ctx->elem_off = element_offset;
   ctx->E_global = n_elements_global > 0 ? n_elements_global : n_elements;
   NKB_TRY(set_dmat_constant(ctx->D));
-  if (ctx->tile_cap < n_elements) {
-    cudaFree(ctx->tile_status);
-    ctx->tile_status = nullptr;
-    NKB_CUDA(cudaMalloc(&ctx->tile_status, sizeof(unsigned long long) * std::max<int64_t>(n_elements, 1)));
-    ctx->tile_cap = n_elements;
-  }
   ctx->image_valid = false;
   return NKB_OK;
 }
@@ -417,8 +413,7 @@ static int fused_params_base(nkb_ctx* ctx, FusedParams& fp) {
   fp.x = ctx->x;
   fp.y = ctx->y;
   fp.z = ctx->z;
-  fp.tile_status = ctx->tile_status;
-  fp.ticket = ctx->ticket;
+  fp.mode = FUSED_FAST;
   fp.counters = ctx->counters;
   fp.color_src = -1;
   return NKB_OK;
@@ -548,13 +543,33 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   fp.tri = ctx->tri;
   fp.meta = p->emit_meta ? ctx->meta : nullptr;
   fp.tri_cap = ctx->tri_cap;
-  // scan state: tile flags 0, counters {0, enc(+max), 0, 0}, ticket 0
-  if (ctx->E > 0)
-    NKB_CUDA(cudaMemsetAsync(ctx->tile_status, 0, sizeof(unsigned long long) * ctx->E, s));
+  // counters {0, enc(+max), 0, 0}
   NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
   NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
-  NKB_TRY(launch_fused(fp, s));
+  if (p->emit_meta && ctx->E > 0) {
+    // deterministic (element, cell, surface, table) order: count, scan, emit
+    if (ctx->elem_cap < ctx->E) {
+      cudaFree(ctx->elem_count);
+      cudaFree(ctx->elem_offset);
+      ctx->elem_count = nullptr;
+      ctx->elem_offset = nullptr;
+      NKB_CUDA(cudaMalloc(&ctx->elem_count, sizeof(int) * ctx->E));
+      NKB_CUDA(cudaMalloc(&ctx->elem_offset, sizeof(long long) * ctx->E));
+      ctx->elem_cap = ctx->E;
+    }
+    FusedParams fc = fp;
+    fc.mode = FUSED_COUNT;
+    fc.elem_count = ctx->elem_count;
+    NKB_TRY(launch_fused(fc, s));
+    NKB_TRY(launch_count_scan(ctx->elem_count, ctx->E, ctx->elem_offset, ctx->counters, s));
+    FusedParams fo = fp;
+    fo.mode = FUSED_ORDERED;
+    fo.elem_offset = ctx->elem_offset;
+    NKB_TRY(launch_fused(fo, s));
+  } else {
+    NKB_TRY(launch_fused(fp, s));
+  }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[1], s));
   NKB_TRY(launch_zbuf_clear(ctx->zbuf, npx, s));
   RasterParams rp;

@@ -76,11 +76,13 @@ struct FusedParams {
   float4* tri;                      // 3 float4 per triangle
   unsigned long long* meta;         // may be null
   int64_t tri_cap;
-  // single-pass scan state
-  unsigned long long* tile_status;  // [n_elements], zeroed before launch
-  unsigned int* ticket;             // zeroed before launch
+  // output slot allocation
+  int mode;                         // FUSED_FAST | FUSED_COUNT | FUSED_ORDERED
+  int* elem_count;                  // [n_elements] (COUNT mode)
+  const long long* elem_offset;     // [n_elements] exclusive scan (ORDERED mode)
   unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
 };
+enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
 
 struct RasterParams {
   const float4* tri;
@@ -113,6 +115,7 @@ struct ResolveParams {
 // ---- kernel launchers (defined in .cu files) --------------------------------
 int set_dmat_constant(const double* dmat);
 int launch_fused(const FusedParams& p, cudaStream_t s);
+int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long long* total, cudaStream_t s);
 int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
 int launch_raster(const RasterParams& p, cudaStream_t s);
 int launch_range_words(const unsigned long long* counters, unsigned long long* words, cudaStream_t s);

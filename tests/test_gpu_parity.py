@@ -90,6 +90,26 @@ def test_box_pipelines_bit_exact(ctx, name):
     _check_against_oracle(ctx, case, pipe, res)
 
 
+def _rows(t):
+    return sorted(bytes(r) for r in np.ascontiguousarray(t).reshape(len(t), -1).view(np.uint8))
+
+
+@pytest.mark.parametrize("name", ["three_surfaces", "four_surfaces"])
+def test_fast_path_triangle_set_and_image(ctx, name):
+    """Unordered fast path (atomic slot allocation): same triangle multiset,
+    identical image (order-independent raster)."""
+    case = synth.box(nel=(4, 3, 3))
+    pipe = BOX_PIPES[name]
+    _, res = _run(ctx, case, pipe)
+    cf = O.CaseFields(case.x, case.y, case.z, case.fields)
+    tri, _, (cmin, cmax) = O.mc(cf, _orc_surfaces(pipe), pipe.color_field)
+    gt = ctx.triangles()
+    assert len(gt) == len(tri) and _rows(gt) == _rows(tri)
+    z = O.raster(tri, res.view, pipe.width, pipe.height)
+    rgba, _ = O.resolve(z, pipe.width, pipe.height, cmin, cmax)
+    assert np.array_equal(res.rgba, rgba)
+
+
 def test_taylor_green_c1_bit_exact(ctx):
     case = synth.taylor_green()
     pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.1),), color_field="velocity:mag", width=256, height=256,

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--width", type=int, default=1024)
+    ap.add_argument("--no-surfaces", action="store_true")
+    ap.add_argument("--color", default=None)
     a = ap.parse_args()
     t0 = time.time()
     case = synth.make_case(a.config) if a.config != "box" else synth.box()
@@ -41,6 +43,10 @@ def main():
     pipe = pipeline_from_params(params)
     from dataclasses import replace
     pipe = replace(pipe, timing=True, emit_meta=a.oracle)
+    if a.no_surfaces:
+        pipe = replace(pipe, surfaces=())
+    if a.color:
+        pipe = replace(pipe, color_field=a.color)
     an = InsituAnalysis(pipe)
     for r in range(a.reps):
         res = an.execute(da)
