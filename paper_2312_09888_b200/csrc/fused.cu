@@ -157,25 +157,50 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     const long long g0 = e * (long long)kNN;
 
     // ---- A. derivative pencils: thread = (group, dir, pencil); 3 fields ----
+    // the three fields share the smem offsets and every D coefficient feeds
+    // three independent DFMAs (one per field) back to back
     if (p.need_grad) {
       const int g = tid / 192;                      // 0: x,y,z   1: u,v,w  (warp-uniform)
       const int dir = (tid % 192) >> 6;             // warp-uniform
       const int pa = tid & 7, pb = (tid >> 3) & 7;
       int off[kNP];
+      if (dir == 0) {
 #pragma unroll
-      for (int m = 0; m < kNP; ++m)
-        off[m] = (dir == 0) ? sw(m, pa, pb) : (dir == 1) ? sw(pa, m, pb) : sw(pa, pb, m);
-#pragma unroll 1
-      for (int ff = 0; ff < 3; ++ff) {
-        const int f = 3 * g + ff;                   // staged slot == field index (x,y,z,u,v,w)
-        const double* src = S_in + f * kArr;
-        double* dst = S_d + (3 * f + dir) * kArr;
-        double v[kNP], o[kNP];
+        for (int m = 0; m < kNP; ++m) off[m] = sw(m, pa, pb);
+      } else if (dir == 1) {
 #pragma unroll
-        for (int m = 0; m < kNP; ++m) v[m] = src[off[m]];
-        deriv8(v, o);
+        for (int m = 0; m < kNP; ++m) off[m] = sw(pa, m, pb);
+      } else {
 #pragma unroll
-        for (int m = 0; m < kNP; ++m) dst[off[m]] = o[m];
+        for (int m = 0; m < kNP; ++m) off[m] = sw(pa, pb, m);
+      }
+      const double* s0 = S_in + (3 * g + 0) * kArr;   // staged slot == field index
+      const double* s1 = S_in + (3 * g + 1) * kArr;
+      const double* s2 = S_in + (3 * g + 2) * kArr;
+      double* d0 = S_d + (3 * (3 * g + 0) + dir) * kArr;
+      double* d1 = S_d + (3 * (3 * g + 1) + dir) * kArr;
+      double* d2 = S_d + (3 * (3 * g + 2) + dir) * kArr;
+      double v0[kNP], v1[kNP], v2[kNP];
+#pragma unroll
+      for (int m = 0; m < kNP; ++m) {
+        v0[m] = s0[off[m]];
+        v1[m] = s1[off[m]];
+        v2[m] = s2[off[m]];
+      }
+#pragma unroll
+      for (int i = 0; i < kNP; ++i) {
+        const double c0 = c_D[i * kNP];
+        double a0 = __dmul_rn(c0, v0[0]), a1 = __dmul_rn(c0, v1[0]), a2 = __dmul_rn(c0, v2[0]);
+#pragma unroll
+        for (int m = 1; m < kNP; ++m) {
+          const double cm = c_D[i * kNP + m];
+          a0 = __fma_rn(cm, v0[m], a0);
+          a1 = __fma_rn(cm, v1[m], a1);
+          a2 = __fma_rn(cm, v2[m], a2);
+        }
+        d0[off[i]] = a0;
+        d1[off[i]] = a1;
+        d2[off[i]] = a2;
       }
       __syncthreads();
     }
