@@ -3,16 +3,17 @@
 // marching-cubes classification of every linear sub-hex and triangle
 // emission, in ONE read of the element's GLL fields.
 //
-// Persistent: one CTA (384 threads, 12 warps) per SM walks the elements
+// Persistent: one CTA (512 threads, 16 warps) per SM walks the elements
 // e = blockIdx.x, blockIdx.x + gridDim.x, ...  The next element's fields are
 // prefetched with cp.async (LDGSTS) into the second half of a double buffer
 // while the current element is computed, so HBM streams continuously.
 //
 // Per element:
 //   A. pencils    : 2 field groups (x,y,z | u,v,w) x 3 directions x 64
-//                   pencils = 384 threads x 3 fields; smem offsets computed
-//                   once per thread, 8-point derivatives with D in constants
-//   B. node phase : Jacobian inverse, grad u, Q, |w|, |u|, plane distances,
+//                   pencils = warps 0-11 x 3 fields; smem offsets computed
+//                   once per thread, 8-point derivatives with D in constants;
+//                   warps 12-15 issue the next element's cp.async prefetch
+//   B. node phase : (one node per thread) Jacobian inverse, grad u, Q, |w|, |u|, plane distances,
 //                   classification bits of every surface, colour range
 //   C. classify   : one sub-hex per thread (343), case byte per surface
 //   D. emit       : triangles interpolated along canonical edges
@@ -55,7 +56,8 @@ int set_dmat_constant(const double* dmat) {
 
 namespace {
 
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
+constexpr int kPencilThreads = 384;   // 2 groups x 3 dirs x 64 pencils
 constexpr int kWarps = kThreads / 32;
 constexpr int kArr = kNN;            // 512 doubles per staged array
 constexpr int kNumD = 18;            // derivative arrays: d(f)/d(r,s,t) for x,y,z,u,v,w
@@ -127,19 +129,22 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   const long long G = gridDim.x;
   double cmin = INFINITY, cmax = -INFINITY;
 
-  // prefetch element `e` into buffer `b`: coalesced 8-byte cp.async into the
-  // swizzled slots (nodes tid and tid + 384)
+  // prefetch element `e` into buffer `b`: warps 12-15 issue coalesced 8-byte
+  // cp.async into the swizzled slots (4 nodes per thread and field); the
+  // pencil warps never spend issue slots on the copy
   auto prefetch = [&](long long e, int b) {
+    if (tid < kPencilThreads) return;
     double* dst = S_buf + b * nin * kArr;
     const long long g0 = e * (long long)kNN;
-    const int q0 = sw_node(tid);
-    const int n1 = tid + kThreads;
-    const int q1 = sw_node(n1 & (kNN - 1));
+    const int t = tid - kPencilThreads;
 #pragma unroll
     for (int f = 0; f < kMaxIn; ++f) {
       if (f < nin) {
-        cp_async8(dst + f * kArr + q0, p.in_ptr[f] + g0 + tid);
-        if (n1 < kNN) cp_async8(dst + f * kArr + q1, p.in_ptr[f] + g0 + n1);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int n = t + 128 * h;
+          cp_async8(dst + f * kArr + sw_node(n), p.in_ptr[f] + g0 + n);
+        }
       }
     }
   };
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     // ---- A. derivative pencils: thread = (group, dir, pencil); 3 fields ----
     // the three fields share the smem offsets and every D coefficient feeds
     // three independent DFMAs (one per field) back to back
-    if (p.need_grad) {
+    if (p.need_grad && tid < kPencilThreads) {
       const int g = tid / 192;                      // 0: x,y,z   1: u,v,w  (warp-uniform)
       const int dir = (tid % 192) >> 6;             // warp-uniform
       const int pa = tid & 7, pb = (tid >> 3) & 7;
@@ -202,12 +207,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         d1[off[i]] = a1;
         d2[off[i]] = a2;
       }
-      __syncthreads();
     }
+    if (p.need_grad) __syncthreads();
 
-    // ---- B. node phase (nodes tid and tid + 384) ----
-#pragma unroll 1
-    for (int n = tid; n < kNN; n += kThreads) {
+    // ---- B. node phase: one node per thread ----
+    {
+      const int n = tid;
       const int q = sw_node(n);
       double vq = 0.0, vw = 0.0, vu = 0.0;
       if (p.need_grad) {
