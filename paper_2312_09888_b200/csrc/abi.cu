@@ -547,7 +547,7 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
   NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
-  if (p->emit_meta && ctx->E > 0) {
+  if (p->emit_meta && ctx->E > 0 && p->n_surfaces > 0) {
     // deterministic (element, cell, surface, table) order: count, scan, emit
     if (ctx->elem_cap < ctx->E) {
       cudaFree(ctx->elem_count);

@@ -3,24 +3,27 @@
 // marching-cubes classification of every linear sub-hex and triangle
 // emission, in ONE read of the element's GLL fields.
 //
-// Persistent: one CTA (512 threads, 16 warps) per SM walks the elements
-// e = blockIdx.x, blockIdx.x + gridDim.x, ...  The next element's fields are
-// prefetched with cp.async (LDGSTS) into the second half of a double buffer
-// while the current element is computed, so HBM streams continuously.
+// Persistent, warp-specialised: one CTA (512 threads, 16 warps) per SM walks
+// the elements e_it = blockIdx.x + it*gridDim.x.  Iteration `it`:
 //
-// Per element:
-//   A. pencils    : 2 field groups (x,y,z | u,v,w) x 3 directions x 64
-//                   pencils = warps 0-11 x 3 fields; smem offsets computed
-//                   once per thread, 8-point derivatives with D in constants;
-//                   warps 12-15 issue the next element's cp.async prefetch
-//   B. node phase : (one node per thread) Jacobian inverse, grad u, Q, |w|, |u|, plane distances,
-//                   classification bits of every surface, colour range
-//   C. classify   : one sub-hex per thread (343), case byte per surface
-//   D. emit       : triangles interpolated along canonical edges
-// Output slots: FAST mode allocates with one atomicAdd per warp (order of
-// triangles in the buffer is arbitrary, the image is not -- the raster is an
-// order-independent min).  Deterministic order (emit_meta) runs COUNT mode,
-// an exclusive scan of the per-element counts, then ORDERED mode.
+//   warps 0-11  (pencils)  : 8-point derivatives of x,y,z | u,v,w along r,s,t
+//                            for element it (384 threads x 3 fields)
+//   warps 12-15 (MC + DMA) : cp.async prefetch of element it+1 (3-stage ring)
+//                            and classify / allocate / emit the triangles of
+//                            element it-1 (one triangle per thread)
+//   ---- barrier ----
+//   all 16 warps (nodes)   : one GLL node per thread: Jacobian inverse, grad u,
+//                            Q, |w|, |u|, plane distances, case bits, colour range
+//   ---- barrier ----
+//
+// The latency-bound MC work runs in the shadow of the FP64-bound pencils;
+// the fields of every element are read from HBM exactly once.
+//
+// Output slots: FAST mode allocates one contiguous slot range per element with
+// a single atomicAdd (element order in the buffer is arbitrary, the image is
+// not -- the raster is an order-independent min); inside an element the order
+// is (cell, surface, table) always.  Deterministic global order (emit_meta)
+// runs COUNT mode, an exclusive scan of the per-element counts, then ORDERED.
 //
 // Shared memory is XOR-swizzled so node-parallel and r/s/t-pencil accesses
 // are bank-conflict free (2 wavefronts per 64-bit warp access).
@@ -58,10 +61,11 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kPencilThreads = 384;   // 2 groups x 3 dirs x 64 pencils
-constexpr int kWarps = kThreads / 32;
-constexpr int kArr = kNN;            // 512 doubles per staged array
-constexpr int kNumD = 18;            // derivative arrays: d(f)/d(r,s,t) for x,y,z,u,v,w
+constexpr int kMcThreads = kThreads - kPencilThreads;   // 128
+constexpr int kArr = kNN;             // 512 doubles per staged array
+constexpr int kNumD = 18;             // derivative arrays: d(f)/d(r,s,t) for x,y,z,u,v,w
 constexpr int kMaxIn = 8;
+constexpr int kRing = 3;              // input ring: compute it, emit it-1, prefetch it+1
 
 // node (i,j,k) -> shared-memory slot.  Within each 64 B line the 8 doubles
 // are XOR-permuted by (j>>1 | (k&1)<<2); lines are XOR-permuted by (k&1).
@@ -87,19 +91,9 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-// 8-point derivative of one pencil: out[i] = sum_m D[i][m] v[m], m ascending,
-// first term a plain product then fma -- mirrored by oracle deriv8().
-__device__ __forceinline__ void deriv8(const double* v, double* out) {
-#pragma unroll
-  for (int i = 0; i < kNP; ++i) {
-    double acc = __dmul_rn(c_D[i * kNP + 0], v[0]);
-#pragma unroll
-    for (int m = 1; m < kNP; ++m) acc = __fma_rn(c_D[i * kNP + m], v[m], acc);
-    out[i] = acc;
-  }
-}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// barrier among the 4 MC warps only (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void mc_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kMcThreads) : "memory"); }
 
 __device__ __forceinline__ double mag3(double a, double b, double c) {
   // reference ':mag' = sqrt(sum(v**2)) summed left to right (sinks.py:240-241)
@@ -112,59 +106,198 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
 
 __device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
 
+struct McScratch {
+  unsigned cases[kNC];          // byte s = case of surface s
+  unsigned coff[kNC + 1];       // exclusive triangle offset of each cell (+ total)
+  int wtot[kMcThreads / 32];
+  unsigned long long base;
+};
+
 }  // namespace
 
 // mode: FUSED_FAST / FUSED_COUNT / FUSED_ORDERED (nkb_internal.h)
 __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nin, int slot_sc) {
   extern __shared__ __align__(16) double smem[];
-  double* S_buf = smem;                                // 2 * nin * 512 (double buffer)
-  double* S_d = smem + 2 * nin * kArr;                 // 18 * 512
-  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_d + kNumD * kArr);
-  __shared__ int s_wcount[kWarps];
-  __shared__ double s_mn[kWarps], s_mx[kWarps];
+  double* S_ring = smem;                               // kRing * nin * 512
+  double* S_d = S_ring + kRing * nin * kArr;           // 18 * 512 derivatives
+  double* S_q = S_d + kNumD * kArr;                    // 2 x (Q, |w|) * 512, by element parity
+  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 4 * kArr);   // 2 x 512
+  __shared__ McScratch mc;
+  __shared__ double s_mn[kThreads / 32], s_mx[kThreads / 32];
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const bool is_mc = tid >= kPencilThreads;
+  const int t = tid - kPencilThreads;                  // MC-warp thread index
   const long long E = p.n_elements;
   const long long G = gridDim.x;
+  const long long n_it = (E > blockIdx.x) ? (E - blockIdx.x + G - 1) / G : 0;
   double cmin = INFINITY, cmax = -INFINITY;
 
-  // prefetch element `e` into buffer `b`: warps 12-15 issue coalesced 8-byte
-  // cp.async into the swizzled slots (4 nodes per thread and field); the
-  // pencil warps never spend issue slots on the copy
+  // MC warps: coalesced 8-byte cp.async of element `e` into ring slot `b`
   auto prefetch = [&](long long e, int b) {
-    if (tid < kPencilThreads) return;
-    double* dst = S_buf + b * nin * kArr;
+    double* dst = S_ring + b * nin * kArr;
     const long long g0 = e * (long long)kNN;
-    const int t = tid - kPencilThreads;
 #pragma unroll
     for (int f = 0; f < kMaxIn; ++f) {
       if (f < nin) {
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          const int n = t + 128 * h;
+          const int n = t + kMcThreads * h;
           cp_async8(dst + f * kArr + sw_node(n), p.in_ptr[f] + g0 + n);
         }
       }
     }
   };
 
-  int buf = 0;
-  long long e = blockIdx.x;
-  if (e < E) prefetch(e, 0);
-  cp_async_commit();
-  for (; e < E; e += G) {
-    if (e + G < E) prefetch(e + G, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();
-    const double* S_in = S_buf + buf * nin * kArr;
-    const long long g0 = e * (long long)kNN;
+  // MC warps: classify, allocate and emit the triangles of element `e`
+  auto mc_element = [&](long long e, const double* S_in, const double* Sq, const unsigned char* bits) {
+    // classify cells 3t .. 3t+2
+    int cnt = 0, cc3[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = 3 * t + j;
+      if (c < kNC) {
+        const int a = c % kN, b = (c / kN) % kN, k = c / (kN * kN);
+        const int n0 = a + kNP * b + kNP * kNP * k;
+        unsigned cb[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) cb[v] = bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
+        unsigned packed = 0;
+        int nc = 0;
+        for (int s = 0; s < p.n_surf; ++s) {
+          unsigned cs = 0;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) cs |= ((cb[v] >> s) & 1u) << v;
+          packed |= cs << (8 * s);
+          nc += g_mc_ntri[cs];
+        }
+        mc.cases[c] = packed;
+        cc3[j] = nc;
+        cnt += nc;
+      }
+    }
+    // exclusive scan over the 128 MC threads (cell-major order)
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int mw = warp - kPencilThreads / 32;
+    if (lane == 31) mc.wtot[mw] = incl;
+    mc_bar();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kMcThreads / 32; ++w) {
+      const int v = mc.wtot[w];
+      before += (w < mw) ? v : 0;
+      total += v;
+    }
+    int run = before + incl - cnt;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = 3 * t + j;
+      if (c < kNC) {
+        mc.coff[c] = run;
+        run += cc3[j];
+      }
+    }
+    if (t == 0) {
+      mc.coff[kNC] = total;
+      unsigned long long base = 0;
+      if (p.mode == FUSED_FAST) {
+        if (total) base = atomicAdd(&p.counters[0], (unsigned long long)total);
+      } else if (p.mode == FUSED_COUNT) {
+        p.elem_count[e] = total;
+      } else {
+        base = (unsigned long long)p.elem_offset[e];
+      }
+      mc.base = base;
+    }
+    mc_bar();
+    if (p.mode == FUSED_COUNT || total == 0) return;
+    const unsigned long long base = mc.base;
+    const double* Sx = S_in;
+    const double* Sy = S_in + kArr;
+    const double* Sz = S_in + 2 * kArr;
+    const double* Su = S_in + 3 * kArr;
+    auto value_at = [&](int src, int s, int q) -> double {
+      if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
+      if (src == SRC_Q) return Sq[q];
+      if (src == SRC_WMAG) return Sq[kArr + q];
+      if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
+      return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+    };
+    for (int tt = t; tt < total; tt += kMcThreads) {
+      // cell owning triangle tt: last c with coff[c] <= tt
+      int lo = 0, hi = kNC - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((int)mc.coff[mid] <= tt) lo = mid;
+        else hi = mid - 1;
+      }
+      const int c = lo;
+      int li = tt - (int)mc.coff[c];
+      const unsigned packed = mc.cases[c];
+      int s = 0;
+      unsigned cs = packed & 0xffu;
+      for (;;) {
+        const int nt = g_mc_ntri[cs];
+        if (li < nt) break;
+        li -= nt;
+        ++s;
+        cs = (packed >> (8 * s)) & 0xffu;
+      }
+      const int k = li;
+      const long long out = (long long)base + tt;
+      if (out >= p.tri_cap) continue;
+      const int ca = c % kN, cb = (c / kN) % kN, ck = c / (kN * kN);
+      const int src = p.surf_src[s];
+      const double iso = p.surf_iso[s];
+      float4 vtx[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int ed = g_mc_tri[cs][3 * k + r];
+        const int va = g_mc_edge_v[ed][0], vb = g_mc_edge_v[ed][1];
+        const int qa = sw(ca + voff_i(va), cb + voff_j(va), ck + voff_k(va));
+        const int qb = sw(ca + voff_i(vb), cb + voff_j(vb), ck + voff_k(vb));
+        const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
+        const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
+        const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
+        vtx[r].x = __double2float_rn(__fma_rn(tv, __dsub_rn(Sx[qb], Sx[qa]), Sx[qa]));
+        vtx[r].y = __double2float_rn(__fma_rn(tv, __dsub_rn(Sy[qb], Sy[qa]), Sy[qa]));
+        vtx[r].z = __double2float_rn(__fma_rn(tv, __dsub_rn(Sz[qb], Sz[qa]), Sz[qa]));
+        vtx[r].w = __double2float_rn(__fma_rn(tv, __dsub_rn(clb, cla), cla));
+      }
+      float4* dst = p.tri + 3 * out;
+      dst[0] = vtx[0];
+      dst[1] = vtx[1];
+      dst[2] = vtx[2];
+      if (p.meta)
+        p.meta[out] = ((unsigned long long)e << 32) | ((unsigned long long)c << 16) |
+                      ((unsigned long long)s << 12) | ((unsigned long long)k << 8) | cs;
+    }
+  };
 
-    // ---- A. derivative pencils: thread = (group, dir, pencil); 3 fields ----
-    // the three fields share the smem offsets and every D coefficient feeds
-    // three independent DFMAs (one per field) back to back
-    if (p.need_grad && tid < kPencilThreads) {
+  if (is_mc && n_it > 0) prefetch(blockIdx.x, 0);
+  cp_async_commit();
+  for (long long it = 0; it <= n_it; ++it) {
+    const long long e = blockIdx.x + it * G;
+    const int slot = (int)(it % kRing);
+    const int par = (int)(it & 1);
+    if (is_mc) cp_async_wait_all();
+    __syncthreads();                                   // element `it` staged; node phase it-1 done
+    const double* S_in = S_ring + slot * nin * kArr;
+    if (is_mc) {
+      if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
+      cp_async_commit();
+      if (it > 0 && p.n_surf > 0) {
+        const int ps = (int)((it - 1) % kRing), pp = (int)((it - 1) & 1);
+        mc_element(e - G, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr, S_bits + pp * kNN);
+      }
+    } else if (it < n_it && p.need_grad) {
+      // ---- pencils: thread = (group, dir, pencil); 3 fields share offsets ----
       const int g = tid / 192;                      // 0: x,y,z   1: u,v,w  (warp-uniform)
       const int dir = (tid % 192) >> 6;             // warp-uniform
       const int pa = tid & 7, pb = (tid >> 3) & 7;
@@ -192,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         v1[m] = s1[off[m]];
         v2[m] = s2[off[m]];
       }
+      // out[i] = D[i][0]*v[0] then fma over m = 1..7 (oracle deriv8)
 #pragma unroll
       for (int i = 0; i < kNP; ++i) {
         const double c0 = c_D[i * kNP];
@@ -208,12 +342,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         d2[off[i]] = a2;
       }
     }
-    if (p.need_grad) __syncthreads();
+    if (it == n_it) break;
+    __syncthreads();                                   // derivatives of element `it` ready
 
-    // ---- B. node phase: one node per thread ----
+    // ---- node phase: one node per thread ----
     {
       const int n = tid;
       const int q = sw_node(n);
+      const long long g0 = e * (long long)kNN;
+      double* Sq = S_q + par * 2 * kArr;
+      unsigned char* bits_out = S_bits + par * kNN;
       double vq = 0.0, vw = 0.0, vu = 0.0;
       if (p.need_grad) {
         double G9[9];
@@ -253,9 +391,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         const double om1 = __dsub_rn(A[2], A[6]);
         const double om2 = __dsub_rn(A[3], A[1]);
         vw = mag3(om0, om1, om2);
-        // this thread owns node q's derivative slots: d0 <- Q, d1 <- |w|
-        S_d[0 * kArr + q] = vq;
-        S_d[1 * kArr + q] = vw;
+        Sq[q] = vq;
+        Sq[kArr + q] = vw;
         if (p.q_out) p.q_out[g0 + n] = vq;
         if (p.wmag_out) p.wmag_out[g0 + n] = vw;
         if (p.vort_out) {
@@ -276,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         else val = S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
         bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
       }
-      S_bits[n] = (unsigned char)bits;
+      bits_out[n] = (unsigned char)bits;
       if (p.color_src >= 0) {
         const int src = p.color_src;
         const double c = (src == SRC_Q)      ? vq
@@ -287,112 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         cmax = fmax(cmax, c);
       }
     }
-    if (p.n_surf == 0) {
-      __syncthreads();     // S_in[buf] / S_d reuse
-      buf ^= 1;
-      continue;
-    }
-    __syncthreads();
-
-    // ---- C. classify: one sub-hex per thread ----
-    const int c = tid;
-    unsigned packed = 0;
-    int cnt = 0;
-    const int ca = c % kN, cb_ = (c / kN) % kN, cc = c / (kN * kN);
-    if (c < kNC) {
-      const int n0 = ca + kNP * cb_ + kNP * kNP * cc;
-      unsigned cbits[8];
-#pragma unroll
-      for (int v = 0; v < 8; ++v) cbits[v] = S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
-      for (int s = 0; s < p.n_surf; ++s) {
-        unsigned cs = 0;
-#pragma unroll
-        for (int v = 0; v < 8; ++v) cs |= ((cbits[v] >> s) & 1u) << v;
-        packed |= cs << (8 * s);
-        cnt += g_mc_ntri[cs];
-      }
-    }
-    // warp inclusive scan of the per-cell counts
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
-    long long out = 0;
-    if (p.mode == FUSED_FAST) {
-      unsigned long long base = 0;
-      if (lane == 0 && wtotal) base = atomicAdd(&p.counters[0], (unsigned long long)wtotal);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      out = (long long)base + (incl - cnt);
-    } else {
-      if (lane == 0) s_wcount[warp] = wtotal;
-      __syncthreads();
-      int wexcl = 0, etotal = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const int v = s_wcount[w];
-        if (w < warp) wexcl += v;
-        etotal += v;
-      }
-      if (p.mode == FUSED_COUNT) {
-        if (tid == 0) p.elem_count[e] = etotal;
-        __syncthreads();
-        buf ^= 1;
-        continue;
-      }
-      out = p.elem_offset[e] + wexcl + (incl - cnt);
-    }
-
-    // ---- D. emit triangles (vertex interpolation along canonical edges) ----
-    if (cnt) {
-      const double* Sx = S_in;
-      const double* Sy = S_in + kArr;
-      const double* Sz = S_in + 2 * kArr;
-      const double* Su = S_in + 3 * kArr;
-      auto value_at = [&](int src, int s, int q) -> double {
-        if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
-        if (src == SRC_Q) return S_d[q];
-        if (src == SRC_WMAG) return S_d[kArr + q];
-        if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
-        return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
-      };
-      for (int s = 0; s < p.n_surf; ++s) {
-        const unsigned cs = (packed >> (8 * s)) & 0xffu;
-        const int nt = g_mc_ntri[cs];
-        if (nt == 0) continue;
-        const int src = p.surf_src[s];
-        const double iso = p.surf_iso[s];
-        for (int k = 0; k < nt; ++k, ++out) {
-          if (out >= p.tri_cap) continue;
-          float4 vtx[3];
-#pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            const int ed = g_mc_tri[cs][3 * k + r];
-            const int va = g_mc_edge_v[ed][0], vb = g_mc_edge_v[ed][1];
-            const int qa = sw(ca + voff_i(va), cb_ + voff_j(va), cc + voff_k(va));
-            const int qb = sw(ca + voff_i(vb), cb_ + voff_j(vb), cc + voff_k(vb));
-            const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
-            const double t = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
-            const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
-            vtx[r].x = __double2float_rn(__fma_rn(t, __dsub_rn(Sx[qb], Sx[qa]), Sx[qa]));
-            vtx[r].y = __double2float_rn(__fma_rn(t, __dsub_rn(Sy[qb], Sy[qa]), Sy[qa]));
-            vtx[r].z = __double2float_rn(__fma_rn(t, __dsub_rn(Sz[qb], Sz[qa]), Sz[qa]));
-            vtx[r].w = __double2float_rn(__fma_rn(t, __dsub_rn(clb, cla), cla));
-          }
-          float4* dst = p.tri + 3 * out;
-          dst[0] = vtx[0];
-          dst[1] = vtx[1];
-          dst[2] = vtx[2];
-          if (p.meta)
-            p.meta[out] = ((unsigned long long)e << 32) | ((unsigned long long)c << 16) |
-                          ((unsigned long long)s << 12) | ((unsigned long long)k << 8) | cs;
-        }
-      }
-    }
-    __syncthreads();     // S_in[buf], S_d, S_bits are rewritten next iteration
-    buf ^= 1;
   }
 
   // colour range of all elements this CTA processed: one ordered atomic pair
@@ -409,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     __syncthreads();
     if (tid == 0) {
       double mn = s_mn[0], mx = s_mx[0];
-      for (int w = 1; w < kWarps; ++w) {
+      for (int w = 1; w < kThreads / 32; ++w) {
         mn = fmin(mn, s_mn[w]);
         mx = fmax(mx, s_mx[w]);
       }
@@ -436,8 +467,8 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict_
     long long x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const long long t = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += t;
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
@@ -445,8 +476,8 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict_
       long long w = s_w[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += t;
+        const long long y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
       }
       s_w[lane] = w;
     }
@@ -463,15 +494,19 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict_
 
 static int g_num_sms = 0;
 
+static size_t fused_smem_bytes(int nin) {
+  return (size_t)(kRing * nin + kNumD + 4) * kArr * sizeof(double) + 2 * kNN;
+}
+
 int launch_fused(const FusedParams& p, cudaStream_t s) {
   if (p.n_elements <= 0) return NKB_OK;
   const int nin = 3 + (p.need_vel ? 3 : 0) + p.n_scalars;
   const int slot_sc = 3 + (p.need_vel ? 3 : 0);
-  const size_t shm = (size_t)(2 * nin + kNumD) * kArr * sizeof(double) + kNN;
+  const size_t shm = fused_smem_bytes(nin);
   static bool attr_set = false;
   if (!attr_set) {
     NKB_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)((2 * kMaxIn + kNumD) * kArr * sizeof(double) + kNN)));
+                                  (int)fused_smem_bytes(kMaxIn)));
     int dev = 0;
     NKB_CUDA(cudaGetDevice(&dev));
     NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
