@@ -89,6 +89,8 @@ static inline double dec_ordered_h(unsigned long long u) {
   return d;
 }
 
+constexpr int kMaxRegions = 1024;   // >= SM count: one triangle region per fused CTA
+
 // mesh bounds reduction (defined in mesh_export.cu)
 int launch_bounds_kernel(const double* x, const double* y, const double* z, int64_t n,
                          unsigned long long* enc6, cudaStream_t s);
@@ -115,8 +117,15 @@ struct nkb_ctx {
   unsigned int* ticket = nullptr;
   float4* tri = nullptr;
   unsigned long long* meta = nullptr;
-  int64_t tri_cap = 0;
+  int64_t tri_cap = 0;                      // = n_regions * region_cap in FAST mode
   bool meta_alloc = false;
+  unsigned long long* region_count = nullptr;   // [kMaxRegions] FAST-mode per-CTA fill
+  int64_t region_cap = 0;
+  int n_regions = 0;
+  bool last_fast = false;
+  float4* tri_export = nullptr;             // compacted FAST-mode triangles (on request)
+  unsigned long long* meta_export = nullptr;
+  int64_t export_cap = 0;
   unsigned long long* zbuf = nullptr;       // W*H + 2 range words
   unsigned char* rgba = nullptr;
   float* depth = nullptr;
@@ -189,7 +198,8 @@ int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
   NKB_CUDA(cudaMalloc(&c->counters, 64));
   c->ticket = reinterpret_cast<unsigned int*>(c->counters + 4);
   NKB_CUDA(cudaMalloc(&c->range_dev, 2 * sizeof(double)));
-  NKB_CUDA(cudaMallocHost(&c->h_counters, 8 * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMallocHost(&c->h_counters, (8 + kMaxRegions) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&c->region_count, kMaxRegions * sizeof(unsigned long long)));
   for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
   *out = c;
   return NKB_OK;
@@ -205,6 +215,9 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->counters);
   cudaFree(ctx->tri);
   cudaFree(ctx->meta);
+  cudaFree(ctx->region_count);
+  cudaFree(ctx->tri_export);
+  cudaFree(ctx->meta_export);
   cudaFree(ctx->zbuf);
   cudaFree(ctx->rgba);
   cudaFree(ctx->depth);
@@ -537,17 +550,22 @@ static int ensure_tri(nkb_ctx* ctx, int64_t cap, bool meta) {
 }
 
 static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
-                    cudaStream_t s, bool composite) {
+                    cudaStream_t s, bool composite, bool ordered) {
   const bool timing = p->timing != 0;
   const int64_t npx = (int64_t)p->width * p->height;
   fp.tri = ctx->tri;
   fp.meta = p->emit_meta ? ctx->meta : nullptr;
   fp.tri_cap = ctx->tri_cap;
+  ctx->n_regions = fused_grid(ctx->E);
+  ctx->region_cap = ctx->tri_cap / ctx->n_regions;
+  fp.region_cap = ctx->region_cap;
+  fp.region_count = ctx->region_count;
+  NKB_CUDA(cudaMemsetAsync(ctx->region_count, 0, sizeof(unsigned long long) * ctx->n_regions, s));
   // counters {0, enc(+max), 0, 0}
   NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
   NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
-  if (p->emit_meta && ctx->E > 0 && p->n_surfaces > 0) {
+  if (ordered) {
     // deterministic (element, cell, surface, table) order: count, scan, emit
     if (ctx->elem_cap < ctx->E) {
       cudaFree(ctx->elem_count);
@@ -574,8 +592,15 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   NKB_TRY(launch_zbuf_clear(ctx->zbuf, npx, s));
   RasterParams rp;
   rp.tri = ctx->tri;
-  rp.n_tri = reinterpret_cast<const int64_t*>(ctx->counters);
-  rp.tri_cap = ctx->tri_cap;
+  if (ordered) {          // one contiguous region; its count is the scan total
+    rp.region_count = ctx->counters;
+    rp.n_regions = 1;
+    rp.region_cap = ctx->tri_cap;
+  } else {
+    rp.region_count = ctx->region_count;
+    rp.n_regions = ctx->n_regions;
+    rp.region_cap = ctx->region_cap;
+  }
   memcpy(rp.view, p->view, sizeof(rp.view));
   rp.width = p->width;
   rp.height = p->height;
@@ -611,8 +636,21 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
                            cudaMemcpyDeviceToHost, s));
   NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 4, ctx->range_dev, 2 * sizeof(double),
                            cudaMemcpyDeviceToHost, s));
+  if (!ordered)
+    NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 8, ctx->region_count,
+                             sizeof(unsigned long long) * ctx->n_regions, cudaMemcpyDeviceToHost, s));
   NKB_CUDA(cudaStreamSynchronize(s));
+  ctx->last_fast = !ordered;
   return NKB_OK;
+}
+
+// capacity the step needed (per-region maximum in FAST mode)
+static int64_t needed_capacity(nkb_ctx* ctx, bool ordered) {
+  const int64_t total = (int64_t)ctx->h_counters[0];
+  if (ordered) return total;
+  int64_t mx = 0;
+  for (int r = 0; r < ctx->n_regions; ++r) mx = std::max<int64_t>(mx, (int64_t)ctx->h_counters[8 + r]);
+  return mx * ctx->n_regions;
 }
 
 int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stream) {
@@ -668,12 +706,14 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   if (ctx->tri_cap == 0) NKB_TRY(ensure_tri(ctx, std::max<int64_t>(1 << 16, ctx->E * 16), p->emit_meta));
   else NKB_TRY(ensure_tri(ctx, ctx->tri_cap, p->emit_meta));
 
-  NKB_TRY(run_step(ctx, p, fp, cm, s, composite));
+  const bool ordered = p->emit_meta && ctx->E > 0 && p->n_surfaces > 0;
+  NKB_TRY(run_step(ctx, p, fp, cm, s, composite, ordered));
   int reran = 0;
   int64_t ntri = (int64_t)ctx->h_counters[0];
-  if (ntri > ctx->tri_cap) {  // grow and re-run once (deterministic result)
-    NKB_TRY(ensure_tri(ctx, ntri + ntri / 4 + 1024, p->emit_meta));
-    NKB_TRY(run_step(ctx, p, fp, cm, s, composite));
+  const int64_t need = needed_capacity(ctx, ordered);
+  if (need > ctx->tri_cap) {  // grow and re-run once (deterministic result)
+    NKB_TRY(ensure_tri(ctx, need + need / 4 + 1024 * ctx->n_regions, p->emit_meta));
+    NKB_TRY(run_step(ctx, p, fp, cm, s, composite, ordered));
     ntri = (int64_t)ctx->h_counters[0];
     reran = 1;
   }
@@ -724,9 +764,30 @@ int nkb_image_copy(nkb_ctx* ctx, unsigned char* rgba, float* depth, void* stream
 
 int nkb_triangles_device(nkb_ctx* ctx, const float** tri, const uint64_t** meta, int64_t* n) {
   NKB_TRY(ctx_check(ctx));
-  if (tri) *tri = reinterpret_cast<const float*>(ctx->tri);
-  if (meta) *meta = reinterpret_cast<const uint64_t*>(ctx->meta);
-  if (n) *n = std::min<int64_t>(ctx->last_ntri, ctx->tri_cap);
+  const int64_t cnt = std::min<int64_t>(ctx->last_ntri, ctx->tri_cap);
+  if (!ctx->last_fast) {
+    if (tri) *tri = reinterpret_cast<const float*>(ctx->tri);
+    if (meta) *meta = reinterpret_cast<const uint64_t*>(ctx->meta);
+    if (n) *n = cnt;
+    return NKB_OK;
+  }
+  // FAST mode wrote per-CTA regions: compact them into one array
+  if (ctx->export_cap < cnt) {
+    cudaFree(ctx->tri_export);
+    cudaFree(ctx->meta_export);
+    ctx->tri_export = nullptr;
+    ctx->meta_export = nullptr;
+    NKB_CUDA(cudaMalloc(&ctx->tri_export, (size_t)std::max<int64_t>(cnt, 1) * 3 * sizeof(float4)));
+    NKB_CUDA(cudaMalloc(&ctx->meta_export, (size_t)std::max<int64_t>(cnt, 1) * sizeof(unsigned long long)));
+    ctx->export_cap = cnt;
+  }
+  NKB_TRY(launch_compact(ctx->tri, ctx->meta_alloc ? ctx->meta : nullptr, ctx->region_count, ctx->n_regions,
+                         ctx->region_cap, ctx->tri_export, ctx->meta_alloc ? ctx->meta_export : nullptr, cnt,
+                         nullptr));
+  NKB_CUDA(cudaStreamSynchronize(nullptr));
+  if (tri) *tri = reinterpret_cast<const float*>(ctx->tri_export);
+  if (meta) *meta = ctx->meta_alloc ? reinterpret_cast<const uint64_t*>(ctx->meta_export) : nullptr;
+  if (n) *n = cnt;
   return NKB_OK;
 }
 

@@ -19,10 +19,12 @@
 // The latency-bound MC work runs in the shadow of the FP64-bound pencils;
 // the fields of every element are read from HBM exactly once.
 //
-// Output slots: FAST mode allocates one contiguous slot range per element with
-// a single atomicAdd (element order in the buffer is arbitrary, the image is
-// not -- the raster is an order-independent min); inside an element the order
-// is (cell, surface, table) always.  Deterministic global order (emit_meta)
+// Output slots: FAST mode appends each element's triangles to a region of the
+// triangle buffer private to the CTA (a shared counter, no global atomics);
+// the raster walks the regions, an export compacts them.  Triangle order in
+// the buffer therefore depends on the CTA schedule -- the image does not (the
+// raster is an order-independent min); inside an element the order is
+// (cell, surface, table) always.  Deterministic global order (emit_meta)
 // runs COUNT mode, an exclusive scan of the per-element counts, then ORDERED.
 //
 // Shared memory is XOR-swizzled so node-parallel and r/s/t-pencil accesses
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   const long long G = gridDim.x;
   const long long n_it = (E > blockIdx.x) ? (E - blockIdx.x + G - 1) / G : 0;
   double cmin = INFINITY, cmax = -INFINITY;
+  unsigned long long cta_fill = 0;     // FAST mode: triangles in this CTA's region (MC thread 0)
 
   // MC warps: coalesced 8-byte cp.async of element `e` into ring slot `b`
   auto prefetch = [&](long long e, int b) {
@@ -207,7 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       mc.coff[kNC] = total;
       unsigned long long base = 0;
       if (p.mode == FUSED_FAST) {
-        if (total) base = atomicAdd(&p.counters[0], (unsigned long long)total);
+        // CTA-private region of the triangle buffer: no global atomics
+        base = (unsigned long long)blockIdx.x * (unsigned long long)p.region_cap + cta_fill;
+        cta_fill += (unsigned long long)total;
       } else if (p.mode == FUSED_COUNT) {
         p.elem_count[e] = total;
       } else {
@@ -251,7 +256,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
       const int k = li;
       const long long out = (long long)base + tt;
-      if (out >= p.tri_cap) continue;
+      if (p.mode == FUSED_FAST ? (out - (long long)blockIdx.x * p.region_cap >= p.region_cap)
+                               : (out >= p.tri_cap))
+        continue;   // overflow: counted, not written; the host grows the buffer and re-runs
       const int ca = c % kN, cb = (c / kN) % kN, ck = c / (kN * kN);
       const int src = p.surf_src[s];
       const double iso = p.surf_iso[s];
@@ -426,6 +433,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   }
 
+  if (p.mode == FUSED_FAST && tid == kPencilThreads) {
+    p.region_count[blockIdx.x] = cta_fill;
+    if (cta_fill) atomicAdd(&p.counters[0], cta_fill);
+  }
   // colour range of all elements this CTA processed: one ordered atomic pair
   if (p.color_src >= 0 && p.mode != FUSED_ORDERED) {
 #pragma unroll
@@ -494,6 +505,46 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict_
 
 static int g_num_sms = 0;
 
+int fused_grid(int64_t n_elements) {
+  if (g_num_sms <= 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      g_num_sms = 148;
+  }
+  int64_t g = g_num_sms;
+  if (g > n_elements) g = n_elements;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// gather the CTA regions of a FAST-mode run into one contiguous array
+__global__ void compact_kernel(const float4* __restrict__ tri, const unsigned long long* __restrict__ meta,
+                               const unsigned long long* __restrict__ region_count, int n_regions,
+                               long long region_cap, float4* __restrict__ out_tri,
+                               unsigned long long* __restrict__ out_meta) {
+  const int r = blockIdx.y;
+  long long dst0 = 0;
+  for (int i = 0; i < r; ++i) dst0 += (long long)min(region_count[i], (unsigned long long)region_cap);
+  const long long n = (long long)min(region_count[r], (unsigned long long)region_cap);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long src = r * region_cap + i;
+    out_tri[3 * (dst0 + i) + 0] = tri[3 * src + 0];
+    out_tri[3 * (dst0 + i) + 1] = tri[3 * src + 1];
+    out_tri[3 * (dst0 + i) + 2] = tri[3 * src + 2];
+    if (meta && out_meta) out_meta[dst0 + i] = meta[src];
+  }
+}
+
+int launch_compact(const float4* tri, const unsigned long long* meta, const unsigned long long* region_count,
+                   int n_regions, int64_t region_cap, float4* out_tri, unsigned long long* out_meta,
+                   int64_t n_total, cudaStream_t s) {
+  if (n_regions <= 0 || n_total <= 0) return NKB_OK;
+  compact_kernel<<<dim3(8, n_regions), 256, 0, s>>>(tri, meta, region_count, n_regions, region_cap, out_tri,
+                                                    out_meta);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
 static size_t fused_smem_bytes(int nin) {
   return (size_t)(kRing * nin + kNumD + 4) * kArr * sizeof(double) + 2 * kNN;
 }
@@ -520,8 +571,7 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   if (p.need_vel)
     for (int c = 0; c < 3; ++c) q.in_ptr[k++] = p.vel[c];
   for (int c = 0; c < p.n_scalars; ++c) q.in_ptr[k++] = p.scalar[c];
-  long long grid = g_num_sms > 0 ? g_num_sms : 148;
-  if (grid > p.n_elements) grid = p.n_elements;
+  const int grid = fused_grid(p.n_elements);
   fused_kernel<<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;

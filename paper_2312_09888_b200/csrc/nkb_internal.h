@@ -78,6 +78,8 @@ struct FusedParams {
   int64_t tri_cap;
   // output slot allocation
   int mode;                         // FUSED_FAST | FUSED_COUNT | FUSED_ORDERED
+  long long region_cap;             // FAST: triangles per CTA region (CTA b owns [b*cap, (b+1)*cap))
+  unsigned long long* region_count; // FAST: [gridDim.x] triangles each CTA produced
   int* elem_count;                  // [n_elements] (COUNT mode)
   const long long* elem_offset;     // [n_elements] exclusive scan (ORDERED mode)
   unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
@@ -86,8 +88,9 @@ enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
 
 struct RasterParams {
   const float4* tri;
-  const int64_t* n_tri;             // device count (clamped to capacity on device)
-  int64_t tri_cap;
+  const unsigned long long* region_count;   // [n_regions] triangles in each region
+  int n_regions;
+  int64_t region_cap;               // region r = tri[r*region_cap, r*region_cap + count)
   double view[12];
   int width, height;
   unsigned long long* zbuf;
@@ -114,7 +117,11 @@ struct ResolveParams {
 
 // ---- kernel launchers (defined in .cu files) --------------------------------
 int set_dmat_constant(const double* dmat);
+int fused_grid(int64_t n_elements);       // CTAs (= triangle regions) of launch_fused
 int launch_fused(const FusedParams& p, cudaStream_t s);
+int launch_compact(const float4* tri, const unsigned long long* meta, const unsigned long long* region_count,
+                   int n_regions, int64_t region_cap, float4* out_tri, unsigned long long* out_meta,
+                   int64_t n_total, cudaStream_t s);
 int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long long* total, cudaStream_t s);
 int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
 int launch_raster(const RasterParams& p, cudaStream_t s);

@@ -66,10 +66,12 @@ __global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
     z[i] = ~0ULL;
 }
 
-// one thread per triangle (grid-stride; the count lives on the device)
+// one thread per triangle; blockIdx.y = triangle region (the count lives on the device)
 __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
-  long long ntri = (long long)*p.n_tri;
-  if (ntri > p.tri_cap) ntri = p.tri_cap;
+  const int r = blockIdx.y;
+  long long ntri = (long long)p.region_count[r];
+  if (ntri > p.region_cap) ntri = p.region_cap;
+  const float4* tri = p.tri + 3 * (long long)r * p.region_cap;
   const int W = p.width, H = p.height;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntri;
        t += (long long)gridDim.x * blockDim.x) {
@@ -77,15 +79,15 @@ __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
     double Z[3], C[3];
     bool ok = true;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const float4 v = p.tri[3 * t + r];
+    for (int q = 0; q < 3; ++q) {
+      const float4 v = tri[3 * t + q];
       double sx, sy, sz;
       xform(p.view, (double)v.x, (double)v.y, (double)v.z, sx, sy, sz);
       if (!(fabs(sx) <= kGuard && fabs(sy) <= kGuard && sz == sz && v.w == v.w)) ok = false;
-      X[r] = __double2ll_rn(__dmul_rn(sx, 256.0));
-      Y[r] = __double2ll_rn(__dmul_rn(sy, 256.0));
-      Z[r] = sz;
-      C[r] = (double)v.w;
+      X[q] = __double2ll_rn(__dmul_rn(sx, 256.0));
+      Y[q] = __double2ll_rn(__dmul_rn(sy, 256.0));
+      Z[q] = sz;
+      C[q] = (double)v.w;
     }
     if (!ok) continue;
     long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
@@ -275,7 +277,8 @@ int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s) {
 }
 
 int launch_raster(const RasterParams& p, cudaStream_t s) {
-  raster_kernel<<<148 * 8, 256, 0, s>>>(p);
+  const int bx = p.n_regions >= 148 ? 8 : (148 * 8 + p.n_regions - 1) / p.n_regions;
+  raster_kernel<<<dim3(bx, p.n_regions), 256, 0, s>>>(p);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

@@ -161,6 +161,29 @@ def test_triangle_buffer_growth_reruns_deterministically(ctx):
     fresh.close()
 
 
+def test_fast_path_region_overflow_reruns(ctx):
+    """FAST mode (per-CTA triangle regions): a region that overflows triggers
+    one re-run with larger regions; image and triangle multiset still exact."""
+    case = synth.box(nel=(4, 4, 4))
+    rng = np.random.default_rng(6)
+    case.fields["noise"] = rng.standard_normal(case.n_points)[None]
+    pipe = Pipeline(surfaces=(Surface("iso", "noise", 0.0), Surface("iso", "noise", 0.7)),
+                    color_field="noise")
+    from paper_2312_09888_b200.context import Context
+
+    fresh = Context(0)
+    _, res = _run(fresh, case, pipe)
+    assert res.report.reran
+    cf = O.CaseFields(case.x, case.y, case.z, case.fields)
+    tri, _, (cmin, cmax) = O.mc(cf, _orc_surfaces(pipe), pipe.color_field)
+    gt = fresh.triangles()
+    assert len(gt) == len(tri) == res.report.n_triangles and _rows(gt) == _rows(tri)
+    z = O.raster(tri, res.view, pipe.width, pipe.height)
+    rgba, _ = O.resolve(z, pipe.width, pipe.height, cmin, cmax)
+    assert np.array_equal(res.rgba, rgba)
+    fresh.close()
+
+
 def test_no_surfaces_gives_background(ctx):
     case = synth.box(nel=(2, 1, 1))
     pipe = Pipeline(surfaces=(), color_field="temperature", width=16, height=8, background=(1, 2, 3, 4))
