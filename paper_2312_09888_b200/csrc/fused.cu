@@ -9,12 +9,14 @@
 //   warps 0-11  (pencils)  : 8-point derivatives of x,y,z | u,v,w along r,s,t
 //                            for element it (384 threads x 3 fields)
 //   warps 12-15 (MC + DMA) : cp.async prefetch of element it+1 (3-stage ring)
-//                            and classify / allocate / emit the triangles of
-//                            element it-1 (one triangle per thread)
+//                            and allocate / emit the triangles of element it-1
+//                            (one triangle per thread)
 //   ---- barrier ----
 //   all 16 warps (nodes)   : one GLL node per thread: Jacobian inverse, grad u,
 //                            Q, |w|, |u|, plane distances, case bits, colour range
 //   ---- barrier ----
+//   all warps (classify)   : one sub-hex per thread: case byte per surface and
+//                            triangle count, kept for the MC warps of it+1
 //
 // The latency-bound MC work runs in the shadow of the FP64-bound pencils;
 // the fields of every element are read from HBM exactly once.
@@ -109,7 +111,8 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
 __device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
 
 struct McScratch {
-  unsigned cases[kNC];          // byte s = case of surface s
+  unsigned cases[2][kNC];       // by element parity: byte s = case of surface s
+  unsigned char ntri[2][kNC];   // triangles of each cell (all surfaces)
   unsigned coff[kNC + 1];       // exclusive triangle offset of each cell (+ total)
   int wtot[kMcThreads / 32];
   unsigned long long base;
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   double* S_ring = smem;                               // kRing * nin * 512
   double* S_d = S_ring + kRing * nin * kArr;           // 18 * 512 derivatives
   double* S_q = S_d + kNumD * kArr;                    // 2 x (Q, |w|) * 512, by element parity
-  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 4 * kArr);   // 2 x 512
+  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 4 * kArr);   // 512 case bits
   __shared__ McScratch mc;
   __shared__ double s_mn[kThreads / 32], s_mx[kThreads / 32];
 
@@ -138,46 +141,33 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   unsigned long long cta_fill = 0;     // FAST mode: triangles in this CTA's region (MC thread 0)
 
   // MC warps: coalesced 8-byte cp.async of element `e` into ring slot `b`
+  int qn[4];                                          // swizzled slots of my 4 nodes
+#pragma unroll
+  for (int h = 0; h < 4; ++h) qn[h] = sw_node(t + kMcThreads * h);
   auto prefetch = [&](long long e, int b) {
     double* dst = S_ring + b * nin * kArr;
-    const long long g0 = e * (long long)kNN;
+    const long long g0 = e * (long long)kNN + t;
 #pragma unroll
     for (int f = 0; f < kMaxIn; ++f) {
       if (f < nin) {
+        const double* src = p.in_ptr[f] + g0;
+        double* d = dst + f * kArr;
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const int n = t + kMcThreads * h;
-          cp_async8(dst + f * kArr + sw_node(n), p.in_ptr[f] + g0 + n);
-        }
+        for (int h = 0; h < 4; ++h) cp_async8(d + qn[h], src + kMcThreads * h);
       }
     }
   };
 
-  // MC warps: classify, allocate and emit the triangles of element `e`
-  auto mc_element = [&](long long e, const double* S_in, const double* Sq, const unsigned char* bits) {
-    // classify cells 3t .. 3t+2
+  // MC warps: allocate and emit the triangles of element `e` (cases and
+  // per-cell counts were classified by all warps at the end of its iteration)
+  auto mc_element = [&](long long e, int par, const double* S_in, const double* Sq) {
     int cnt = 0, cc3[3] = {0, 0, 0};
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       const int c = 3 * t + j;
       if (c < kNC) {
-        const int a = c % kN, b = (c / kN) % kN, k = c / (kN * kN);
-        const int n0 = a + kNP * b + kNP * kNP * k;
-        unsigned cb[8];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) cb[v] = bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
-        unsigned packed = 0;
-        int nc = 0;
-        for (int s = 0; s < p.n_surf; ++s) {
-          unsigned cs = 0;
-#pragma unroll
-          for (int v = 0; v < 8; ++v) cs |= ((cb[v] >> s) & 1u) << v;
-          packed |= cs << (8 * s);
-          nc += g_mc_ntri[cs];
-        }
-        mc.cases[c] = packed;
-        cc3[j] = nc;
-        cnt += nc;
+        cc3[j] = mc.ntri[par][c];
+        cnt += cc3[j];
       }
     }
     // exclusive scan over the 128 MC threads (cell-major order)
@@ -244,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
       const int c = lo;
       int li = tt - (int)mc.coff[c];
-      const unsigned packed = mc.cases[c];
+      const unsigned packed = mc.cases[par][c];
       int s = 0;
       unsigned cs = packed & 0xffu;
       for (;;) {
@@ -301,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       cp_async_commit();
       if (it > 0 && p.n_surf > 0) {
         const int ps = (int)((it - 1) % kRing), pp = (int)((it - 1) & 1);
-        mc_element(e - G, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr, S_bits + pp * kNN);
+        mc_element(e - G, pp, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr);
       }
     } else if (it < n_it && p.need_grad) {
       // ---- pencils: thread = (group, dir, pencil); 3 fields share offsets ----
@@ -358,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       const int q = sw_node(n);
       const long long g0 = e * (long long)kNN;
       double* Sq = S_q + par * 2 * kArr;
-      unsigned char* bits_out = S_bits + par * kNN;
+      unsigned char* bits_out = S_bits;
       double vq = 0.0, vw = 0.0, vu = 0.0;
       if (p.need_grad) {
         double G9[9];
@@ -431,9 +421,32 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         cmax = fmax(cmax, c);
       }
     }
+    if (p.n_surf == 0) continue;
+    __syncthreads();                                   // case bits of element `it` ready
+
+    // ---- classify: one sub-hex per thread (all warps) ----
+    if (tid < kNC) {
+      const int c = tid;
+      const int a = c % kN, b = (c / kN) % kN, k = c / (kN * kN);
+      const int n0 = a + kNP * b + kNP * kNP * k;
+      unsigned cb[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) cb[v] = S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
+      unsigned packed = 0;
+      int nc = 0;
+      for (int s = 0; s < p.n_surf; ++s) {
+        unsigned cs = 0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) cs |= ((cb[v] >> s) & 1u) << v;
+        packed |= cs << (8 * s);
+        nc += g_mc_ntri[cs];
+      }
+      mc.cases[par][c] = packed;
+      mc.ntri[par][c] = (unsigned char)nc;
+    }
   }
 
-  if (p.mode == FUSED_FAST && tid == kPencilThreads) {
+  if (p.mode == FUSED_FAST && p.region_count != nullptr && tid == kPencilThreads) {
     p.region_count[blockIdx.x] = cta_fill;
     if (cta_fill) atomicAdd(&p.counters[0], cta_fill);
   }
