@@ -8,11 +8,9 @@
 //
 //   warps 0-11  (pencils)  : 8-point derivatives of x,y,z | u,v,w along r,s,t
 //                            for element it (384 threads x 3 fields)
-//   warps 12-15 (MC + DMA) : cp.async prefetch of element it+1 (3-stage ring),
-//                            scan + slot allocation of element it-1, then emit
-//                            its triangles; pencil warps join the emission as
-//                            soon as their pencils are done (32-triangle chunks
-//                            claimed from a shared cursor)
+//   warps 12-15 (MC + DMA) : cp.async prefetch of element it+1 (3-stage ring)
+//                            and allocate / emit the triangles of element it-1
+//                            (one triangle per thread)
 //   ---- barrier ----
 //   all 16 warps (nodes)   : one GLL node per thread: Jacobian inverse, grad u,
 //                            Q, |w|, |u|, plane distances, case bits, colour range
@@ -100,10 +98,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // barrier among the 4 MC warps only (id 1; id 0 is __syncthreads)
 __device__ __forceinline__ void mc_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kMcThreads) : "memory"); }
-// producer/consumer barrier 2 over all threads: MC warps arrive after
-// publishing the scan, pencil warps sync before joining the emission
-__device__ __forceinline__ void bar_arrive_all() { asm volatile("bar.arrive 2, %0;" ::"n"(kThreads) : "memory"); }
-__device__ __forceinline__ void bar_sync_all() { asm volatile("bar.sync 2, %0;" ::"n"(kThreads) : "memory"); }
 
 __device__ __forceinline__ double mag3(double a, double b, double c) {
   // reference ':mag' = sqrt(sum(v**2)) summed left to right (sinks.py:240-241)
@@ -116,22 +110,12 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
 
 __device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
 
-constexpr int kMaxTriPerElem = kNC * NKB_MC_MAX_TRI * NKB_MAX_SURFACES;   // 6860
-
 struct McScratch {
   unsigned cases[2][kNC];       // by element parity: byte s = case of surface s
   unsigned char ntri[2][kNC];   // triangles of each cell (all surfaces)
-  unsigned short coff[kNC];     // exclusive triangle offset of each cell
-  unsigned short tri_cell[kMaxTriPerElem];   // cell of each triangle of the element
+  unsigned coff[kNC + 1];       // exclusive triangle offset of each cell (+ total)
   int wtot[kMcThreads / 32];
-  unsigned long long base;      // output slot of the element's first triangle
-  long long elem;               // element being emitted
-  int total;                    // its triangle count (0: nothing to emit)
-  int next;                     // work-sharing cursor (claimed 32 at a time)
-  // marching-cubes tables, copied once per CTA
-  unsigned char t_ntri[256];
-  signed char t_tri[256][3 * NKB_MC_MAX_TRI];
-  unsigned char t_edge[12][2];
+  unsigned long long base;
 };
 
 }  // namespace
@@ -174,10 +158,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   };
 
-  // MC warps: scan the per-cell triangle counts of element `e` (classified
-  // by all warps at the end of its iteration), allocate its output slots and
-  // publish a triangle -> cell map for the work-shared emission
-  auto mc_scan = [&](long long e, int par) {
+  // MC warps: allocate and emit the triangles of element `e` (cases and
+  // per-cell counts were classified by all warps at the end of its iteration)
+  auto mc_element = [&](long long e, int par, const double* S_in, const double* Sq) {
     int cnt = 0, cc3[3] = {0, 0, 0};
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -187,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         cnt += cc3[j];
       }
     }
+    // exclusive scan over the 128 MC threads (cell-major order)
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -208,37 +192,27 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     for (int j = 0; j < 3; ++j) {
       const int c = 3 * t + j;
       if (c < kNC) {
-        mc.coff[c] = (unsigned short)run;
-        for (int q = 0; q < cc3[j]; ++q) mc.tri_cell[run + q] = (unsigned short)c;
+        mc.coff[c] = run;
         run += cc3[j];
       }
     }
     if (t == 0) {
+      mc.coff[kNC] = total;
       unsigned long long base = 0;
-      int emit_total = total;
       if (p.mode == FUSED_FAST) {
         // CTA-private region of the triangle buffer: no global atomics
         base = (unsigned long long)blockIdx.x * (unsigned long long)p.region_cap + cta_fill;
         cta_fill += (unsigned long long)total;
       } else if (p.mode == FUSED_COUNT) {
         p.elem_count[e] = total;
-        emit_total = 0;
       } else {
         base = (unsigned long long)p.elem_offset[e];
       }
       mc.base = base;
-      mc.elem = e;
-      mc.total = emit_total;
-      mc.next = 0;
     }
-  };
-
-  // any warp: emit triangles of the published element, 32 at a time
-  auto emit_chunks = [&](int par, const double* S_in, const double* Sq) {
-    const int total = mc.total;
-    if (total == 0) return;
+    mc_bar();
+    if (p.mode == FUSED_COUNT || total == 0) return;
     const unsigned long long base = mc.base;
-    const long long e = mc.elem;
     const double* Sx = S_in;
     const double* Sy = S_in + kArr;
     const double* Sz = S_in + 2 * kArr;
@@ -250,20 +224,21 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
       return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
     };
-    for (;;) {
-      int b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&mc.next, 32);
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-      if (b0 >= total) break;
-      const int tt = b0 + lane;
-      if (tt >= total) continue;
-      const int c = mc.tri_cell[tt];
+    for (int tt = t; tt < total; tt += kMcThreads) {
+      // cell owning triangle tt: last c with coff[c] <= tt
+      int lo = 0, hi = kNC - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((int)mc.coff[mid] <= tt) lo = mid;
+        else hi = mid - 1;
+      }
+      const int c = lo;
       int li = tt - (int)mc.coff[c];
       const unsigned packed = mc.cases[par][c];
       int s = 0;
       unsigned cs = packed & 0xffu;
       for (;;) {
-        const int nt = mc.t_ntri[cs];
+        const int nt = g_mc_ntri[cs];
         if (li < nt) break;
         li -= nt;
         ++s;
@@ -280,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       float4 vtx[3];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        const int ed = mc.t_tri[cs][3 * k + r];
-        const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
+        const int ed = g_mc_tri[cs][3 * k + r];
+        const int va = g_mc_edge_v[ed][0], vb = g_mc_edge_v[ed][1];
         const int qa = sw(ca + voff_i(va), cb + voff_j(va), ck + voff_k(va));
         const int qb = sw(ca + voff_i(vb), cb + voff_j(vb), ck + voff_k(vb));
         const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
@@ -302,11 +277,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   };
 
-  for (int i = tid; i < 256; i += kThreads) mc.t_ntri[i] = g_mc_ntri[i];
-  for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kThreads) (&mc.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
-  if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
-  if (tid == 0) mc.total = 0;
-
   if (is_mc && n_it > 0) prefetch(blockIdx.x, 0);
   cp_async_commit();
   for (long long it = 0; it <= n_it; ++it) {
@@ -316,19 +286,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     if (is_mc) cp_async_wait_all();
     __syncthreads();                                   // element `it` staged; node phase it-1 done
     const double* S_in = S_ring + slot * nin * kArr;
-    const int ps = it > 0 ? (int)((it - 1) % kRing) : 0, pp = it > 0 ? (int)((it - 1) & 1) : 0;
-    const double* S_em = S_ring + ps * nin * kArr;     // element it-1 (emitted this iteration)
-    const double* Sq_em = S_q + pp * 2 * kArr;
     if (is_mc) {
       if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
       cp_async_commit();
-      if (it > 0 && p.n_surf > 0) mc_scan(e - G, pp);
-      else if (t == 0) mc.total = 0;
-      mc_bar();                                        // scan results visible to the MC warps
-      bar_arrive_all();                                // ... and published to the pencil warps
-      emit_chunks(pp, S_em, Sq_em);
-    } else {
-      if (it < n_it && p.need_grad) {
+      if (it > 0 && p.n_surf > 0) {
+        const int ps = (int)((it - 1) % kRing), pp = (int)((it - 1) & 1);
+        mc_element(e - G, pp, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr);
+      }
+    } else if (it < n_it && p.need_grad) {
       // ---- pencils: thread = (group, dir, pencil); 3 fields share offsets ----
       const int g = tid / 192;                      // 0: x,y,z   1: u,v,w  (warp-uniform)
       const int dir = (tid % 192) >> 6;             // warp-uniform
@@ -373,9 +338,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         d1[off[i]] = a1;
         d2[off[i]] = a2;
       }
-      }
-      bar_sync_all();                                  // wait for the MC warps' scan
-      emit_chunks(pp, S_em, Sq_em);                    // then help emitting element it-1
     }
     if (it == n_it) break;
     __syncthreads();                                   // derivatives of element `it` ready
@@ -477,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
 #pragma unroll
         for (int v = 0; v < 8; ++v) cs |= ((cb[v] >> s) & 1u) << v;
         packed |= cs << (8 * s);
-        nc += mc.t_ntri[cs];
+        nc += g_mc_ntri[cs];
       }
       mc.cases[par][c] = packed;
       mc.ntri[par][c] = (unsigned char)nc;
