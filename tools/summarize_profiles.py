@@ -1,0 +1,78 @@
+"""Summarise gpurun_out/<tag>_* ncu outputs into profiles/ (committed).
+
+    python tools/summarize_profiles.py r01
+"""
+import csv
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def launches(tag):
+    path = os.path.join(ROOT, "gpurun_out", f"{tag}_launches.csv")
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    iN, iV, iM = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
+    per = defaultdict(list)
+    for r in rows[1:]:
+        if r[iM] == "gpu__time_duration.sum":
+            per[r[iN].split("(")[0]].append(float(r[iV].replace(",", "")))
+    tot = sum(sum(v) for v in per.values())
+    lines = [f"# ncu launch list ({tag}): bench.py --steps 3 --warmup 3, gpu__time_duration.sum",
+             "# cold-cache, serialised per-launch times; compare SHARES, not absolutes",
+             f"{'kernel':60s} {'launches':>8s} {'mean_us':>10s} {'share':>7s}"]
+    for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"{k[:60]:60s} {len(v):8d} {sum(v) / len(v) / 1e3:10.2f} {sum(v) / tot * 100:6.1f}%")
+    return "\n".join(lines) + "\n"
+
+
+def full(tag):
+    rep = os.path.join(ROOT, "gpurun_out", f"{tag}_fused.ncu-rep")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, units, vals = rows[0], rows[1], rows[2]
+    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+            "launch__grid_size", "launch__block_size"]
+    out = {}
+    for w in want:
+        if w in h:
+            i = h.index(w)
+            out[w] = (vals[i], units[i])
+    return out
+
+
+def main(tag):
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    txt = launches(tag)
+    open(os.path.join(ROOT, "profiles", f"{tag}_launches.txt"), "w").write(txt)
+    print(txt)
+    m = full(tag)
+    lines = [f"# ncu --set full, fused_kernel, C2 (32768 elements, 16.8M GLL points), tag {tag}"]
+    for k, (v, u) in m.items():
+        lines.append(f"{k:70s} {v} {u}")
+    open(os.path.join(ROOT, "profiles", f"{tag}_fused_full.txt"), "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+    def num(k):
+        v, u = m[k]
+        f = float(v.replace(",", ""))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        return f * scale
+    if "dram__bytes_read.sum" in m:
+        traffic = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+        json.dump({"dram_bytes_per_launch": traffic, "source": f"profiles/{tag}_fused_full.txt"},
+                  open(os.path.join(ROOT, "profiles", "traffic_c2.json"), "w"), indent=1)
+        print("traffic", traffic)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
