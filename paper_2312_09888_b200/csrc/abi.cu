@@ -407,7 +407,10 @@ int nkb_add_array(nkb_ctx* ctx, const char* name, int association, double* out, 
     fp.n_surf = 0;
     if (n == "Q") fp.q_out = out;
     if (n == "vorticity") fp.vort_out = out;
-    if (n == "vorticity:mag") fp.wmag_out = out;
+    if (n == "vorticity:mag") {
+      fp.wmag_out = out;
+      fp.need_wmag = 1;
+    }
     NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
     NKB_TRY(launch_fused(fp, s));
     return NKB_OK;
@@ -456,6 +459,7 @@ static int resolve_src(nkb_ctx* ctx, const char* name, FusedParams& fp, int* src
     NKB_TRY(need_velocity());
     fp.need_grad = 1;
     *src = (n == "Q") ? SRC_Q : SRC_WMAG;
+    if (n != "Q") fp.need_wmag = 1;
     return NKB_OK;
   }
   auto colon = n.find(':');
@@ -469,6 +473,7 @@ static int resolve_src(nkb_ctx* ctx, const char* name, FusedParams& fp, int* src
       return fail(NKB_EINVAL, "':mag' in the fused path is supported for the velocity field '" +
                                   ctx->vel_name + "' only");
     NKB_TRY(need_velocity());
+    fp.need_umag = 1;
     *src = SRC_UMAG;
     return NKB_OK;
   }

@@ -50,6 +50,8 @@
 namespace nkb {
 
 __constant__ double c_D[kNP * kNP];
+__constant__ double c_Ae[4][4];   // even half: 0.5*(D[i][m] + D[i][7-m])
+__constant__ double c_Ao[4][4];   // odd half:  0.5*(D[i][m] - D[i][7-m])
 
 // MC tables in global memory (read-only path; divergent indices)
 __device__ const unsigned char g_mc_ntri[256] = {NKB_MC_NTRI_DATA};
@@ -58,6 +60,14 @@ __device__ const unsigned char g_mc_edge_v[12][2] = {NKB_MC_EDGE_V_DATA};
 
 int set_dmat_constant(const double* dmat) {
   NKB_CUDA(cudaMemcpyToSymbol(c_D, dmat, sizeof(double) * kNP * kNP));
+  double ae[4][4], ao[4][4];
+  for (int i = 0; i < 4; ++i)
+    for (int m = 0; m < 4; ++m) {   // host code, -ffp-contract=off (same as the oracle)
+      ae[i][m] = 0.5 * (dmat[i * kNP + m] + dmat[i * kNP + (kNP - 1 - m)]);
+      ao[i][m] = 0.5 * (dmat[i * kNP + m] - dmat[i * kNP + (kNP - 1 - m)]);
+    }
+  NKB_CUDA(cudaMemcpyToSymbol(c_Ae, ae, sizeof(ae)));
+  NKB_CUDA(cudaMemcpyToSymbol(c_Ao, ao, sizeof(ao)));
   return NKB_OK;
 }
 
@@ -322,21 +332,39 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         v1[m] = s1[off[m]];
         v2[m] = s2[off[m]];
       }
-      // out[i] = D[i][0]*v[0] then fma over m = 1..7 (oracle deriv8)
+      // even-odd form (oracle deriv8): e_m = v_m + v_{7-m}, o_m = v_m - v_{7-m},
+      // out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 fields
+      double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
 #pragma unroll
-      for (int i = 0; i < kNP; ++i) {
-        const double c0 = c_D[i * kNP];
-        double a0 = __dmul_rn(c0, v0[0]), a1 = __dmul_rn(c0, v1[0]), a2 = __dmul_rn(c0, v2[0]);
+      for (int m = 0; m < 4; ++m) {
+        e0[m] = __dadd_rn(v0[m], v0[kNP - 1 - m]);
+        o0[m] = __dsub_rn(v0[m], v0[kNP - 1 - m]);
+        e1[m] = __dadd_rn(v1[m], v1[kNP - 1 - m]);
+        o1[m] = __dsub_rn(v1[m], v1[kNP - 1 - m]);
+        e2[m] = __dadd_rn(v2[m], v2[kNP - 1 - m]);
+        o2[m] = __dsub_rn(v2[m], v2[kNP - 1 - m]);
+      }
 #pragma unroll
-        for (int m = 1; m < kNP; ++m) {
-          const double cm = c_D[i * kNP + m];
-          a0 = __fma_rn(cm, v0[m], a0);
-          a1 = __fma_rn(cm, v1[m], a1);
-          a2 = __fma_rn(cm, v2[m], a2);
+      for (int i = 0; i < 4; ++i) {
+        const double ce = c_Ae[i][0], co = c_Ao[i][0];
+        double E0 = __dmul_rn(ce, e0[0]), E1 = __dmul_rn(ce, e1[0]), E2 = __dmul_rn(ce, e2[0]);
+        double O0 = __dmul_rn(co, o0[0]), O1 = __dmul_rn(co, o1[0]), O2 = __dmul_rn(co, o2[0]);
+#pragma unroll
+        for (int m = 1; m < 4; ++m) {
+          const double ae = c_Ae[i][m], ao = c_Ao[i][m];
+          E0 = __fma_rn(ae, e0[m], E0);
+          E1 = __fma_rn(ae, e1[m], E1);
+          E2 = __fma_rn(ae, e2[m], E2);
+          O0 = __fma_rn(ao, o0[m], O0);
+          O1 = __fma_rn(ao, o1[m], O1);
+          O2 = __fma_rn(ao, o2[m], O2);
         }
-        d0[off[i]] = a0;
-        d1[off[i]] = a1;
-        d2[off[i]] = a2;
+        d0[off[i]] = __dadd_rn(E0, O0);
+        d1[off[i]] = __dadd_rn(E1, O1);
+        d2[off[i]] = __dadd_rn(E2, O2);
+        d0[off[kNP - 1 - i]] = __dsub_rn(O0, E0);
+        d1[off[kNP - 1 - i]] = __dsub_rn(O1, E1);
+        d2[off[kNP - 1 - i]] = __dsub_rn(O2, E2);
       }
     }
     if (it == n_it) break;
@@ -368,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         J[7] = __fma_rn(xs, zr, -__dmul_rn(xr, zs));
         J[8] = __fma_rn(xr, ys, -__dmul_rn(xs, yr));
         const double det = __fma_rn(zr, J[2], __fma_rn(yr, J[1], __dmul_rn(xr, J[0])));
-        const double rdet = __ddiv_rn(1.0, det);
+        const double rdet = __drcp_rn(det);           // == 1.0/det, correctly rounded
 #pragma unroll
         for (int c = 0; c < 9; ++c) J[c] = __dmul_rn(J[c], rdet);
         double U[9];
@@ -387,9 +415,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         const double om0 = __dsub_rn(A[7], A[5]);
         const double om1 = __dsub_rn(A[2], A[6]);
         const double om2 = __dsub_rn(A[3], A[1]);
-        vw = mag3(om0, om1, om2);
         Sq[q] = vq;
-        Sq[kArr + q] = vw;
+        if (p.need_wmag) {
+          vw = mag3(om0, om1, om2);
+          Sq[kArr + q] = vw;
+        }
         if (p.q_out) p.q_out[g0 + n] = vq;
         if (p.wmag_out) p.wmag_out[g0 + n] = vw;
         if (p.vort_out) {
@@ -398,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
           p.vort_out[3 * (g0 + n) + 2] = om2;
         }
       }
-      if (p.need_vel) vu = mag3(S_in[3 * kArr + q], S_in[4 * kArr + q], S_in[5 * kArr + q]);
+      if (p.need_umag) vu = mag3(S_in[3 * kArr + q], S_in[4 * kArr + q], S_in[5 * kArr + q]);
       unsigned bits = 0;
       for (int s = 0; s < p.n_surf; ++s) {
         const int src = p.surf_src[s];

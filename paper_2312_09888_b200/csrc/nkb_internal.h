@@ -62,6 +62,8 @@ struct FusedParams {
   const double* in_ptr[8];          // filled by launch_fused: staged inputs in slot order
   int need_grad;                    // compute velocity gradient (Q / vorticity)
   int need_vel;                     // load velocity
+  int need_wmag;                    // |vorticity| used (surface, colour or export)
+  int need_umag;                    // |velocity| used (surface or colour)
   int n_scalars;
   int n_surf;
   int surf_src[NKB_MAX_SURFACES];
