@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <math.h>
 #include <nccl.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -144,6 +145,7 @@ struct nkb_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   cudaEvent_t ev[6] = {};
+  long long* prof = nullptr;                 // debug phase profile (NKB_PROFILE_PHASES=1)
 };
 
 static int ctx_check(nkb_ctx* ctx) {
@@ -201,6 +203,10 @@ int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
   NKB_CUDA(cudaMallocHost(&c->h_counters, (8 + kMaxRegions) * sizeof(unsigned long long)));
   NKB_CUDA(cudaMalloc(&c->region_count, kMaxRegions * sizeof(unsigned long long)));
   for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
+  if (getenv("NKB_PROFILE_PHASES")) {
+    NKB_CUDA(cudaMalloc(&c->prof, kMaxRegions * 16 * sizeof(long long)));
+    NKB_CUDA(cudaMemset(c->prof, 0, kMaxRegions * 16 * sizeof(long long)));
+  }
   *out = c;
   return NKB_OK;
 }
@@ -431,6 +437,7 @@ static int fused_params_base(nkb_ctx* ctx, FusedParams& fp) {
   fp.z = ctx->z;
   fp.mode = FUSED_FAST;
   fp.counters = ctx->counters;
+  fp.prof = ctx->prof;
   fp.color_src = -1;
   return NKB_OK;
 }
@@ -793,6 +800,15 @@ int nkb_triangles_device(nkb_ctx* ctx, const float** tri, const uint64_t** meta,
   if (tri) *tri = reinterpret_cast<const float*>(ctx->tri_export);
   if (meta) *meta = ctx->meta_alloc ? reinterpret_cast<const uint64_t*>(ctx->meta_export) : nullptr;
   if (n) *n = cnt;
+  return NKB_OK;
+}
+
+// debug: phase cycle counters of the last fused launch ([grid][2][6]); returns grid
+int nkb_debug_phase_profile(nkb_ctx* ctx, long long* out, int cap) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->prof) return fail(NKB_ESTATE, "set NKB_PROFILE_PHASES=1 before nkb_ctx_create");
+  const int n = std::min(ctx->n_regions, cap);
+  NKB_CUDA(cudaMemcpy(out, ctx->prof, sizeof(long long) * 16 * n, cudaMemcpyDeviceToHost));
   return NKB_OK;
 }
 

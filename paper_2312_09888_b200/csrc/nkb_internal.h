@@ -85,6 +85,7 @@ struct FusedParams {
   int* elem_count;                  // [n_elements] (COUNT mode)
   const long long* elem_offset;     // [n_elements] exclusive scan (ORDERED mode)
   unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
+  long long* prof;                  // optional phase cycles [grid][2][6] (debug)
 };
 enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
 

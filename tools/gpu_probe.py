@@ -56,6 +56,20 @@ def main():
         print(f"rep {r}: ntri={rp.n_triangles} fused {rp.ms_fused:.3f} ms ({gb / rp.ms_fused:.0f} GB/s of "
               f"{gb:.2f} GB) raster {rp.ms_raster:.3f} resolve {rp.ms_resolve:.3f} total {tot:.3f} ms "
               f"range {rp.range} reran={rp.reran}", flush=True)
+    if os.environ.get("NKB_PROFILE_PHASES"):
+        import ctypes as C
+        from paper_2312_09888_b200 import _native as N
+        L = N.lib()
+        fn = L.nkb_debug_phase_profile
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        buf = np.zeros((148, 2, 2, 4), np.int64)       # [cta][group][pencil-thread | aux-thread][phase]
+        N.check(fn(ctx.handle, buf.ctypes.data, 148))
+        names = ["wait+bar1", "pencils|emit", "bar2+prefetch / classify", "node"]
+        tot = buf.sum(axis=(0, 1))
+        for r, rname in enumerate(("pencil-thread", "aux-thread")):
+            t = tot[r].sum()
+            print(rname, " ".join(f"{n}={v / t * 100:.1f}%" for n, v in zip(names, tot[r])),
+                  f"cycles/elem/group={t / (case.n_elements / 2):.0f}")
     if a.oracle:
         from oracle import oracle as orc
         cf = orc.CaseFields(case.x, case.y, case.z, case.fields)
