@@ -13,12 +13,14 @@
 //   6 pencil warps : even-odd 8-point derivatives of x,y,z | u,v,w along
 //                    r,s,t (192 (dir, pencil) threads x 6 fields, smem
 //                    offsets computed once, each coefficient feeds 3 DFMAs)
-//   2 aux warps    : meanwhile scan, allocate and emit the triangles of the
-//                    group's previous element
+//   2 aux warps    : meanwhile node-local pre-pass of the element (plane /
+//                    scalar / |u| case bits, colour range; via L2) and scan,
+//                    allocate and emit the triangles of the group's previous
+//                    element
 //   -- group barrier --
 //   aux warps      : cp.async prefetch of the group's next element
 //   8 warps        : node phase (2 nodes / thread): Jacobian inverse, grad u,
-//                    Q, |w|, |u|, plane distances, case bits, colour range
+//                    Q, |w|, Q / |w| case bits
 //   -- group barrier --
 //   8 warps        : classification (one sub-hex per thread)
 //
@@ -180,6 +182,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   const long long n_it = (E > blockIdx.x) ? (E - blockIdx.x + G - 1) / G : 0;
   const long long n_k = (n_it > g) ? (n_it - g + 1) / 2 : 0;   // elements of this group
   auto elem_of = [&](long long k) { return (long long)blockIdx.x + (2 * k + g) * G; };
+  bool need_xyz = false, grad_surf = false;         // any slice plane / any Q or |w| surface
+  for (int s = 0; s < p.n_surf; ++s) {
+    need_xyz |= p.surf_src[s] >= SRC_PLANE;
+    grad_surf |= src_is_grad(p.surf_src[s]);
+  }
+  const bool color_grad = src_is_grad(p.color_src);
   double cmin = INFINITY, cmax = -INFINITY;
 
   // aux warps: coalesced 8-byte cp.async of element e's staged arrays
@@ -206,6 +214,52 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     if (src == SRC_UMAG)
       return mag3(__ldg(p.vel[0] + g0 + n), __ldg(p.vel[1] + g0 + n), __ldg(p.vel[2] + g0 + n));
     return __ldg(p.scalar[src - SRC_SCALAR0] + g0 + n);
+  };
+
+  // aux warps: node-local classification bits (planes, scalars, |u|) and the
+  // colour range of non-derived colour fields for element e, through L2
+  auto prepass = [&](long long e) {
+    const long long g0 = e * (long long)kNN;
+#pragma unroll 1
+    for (int hb = 0; hb < kArr / kAuxThreads; hb += 4) {
+      double lx[4], ly[4], lz[4], ls0[4], ls1[4], lu[4], lv[4], lw[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {      // issue every load of the batch first
+        const int n = at + kAuxThreads * (hb + h);
+        lx[h] = ly[h] = lz[h] = ls0[h] = ls1[h] = lu[h] = lv[h] = lw[h] = 0.0;
+        if (need_xyz) {
+          lx[h] = __ldg(p.x + g0 + n);
+          ly[h] = __ldg(p.y + g0 + n);
+          lz[h] = __ldg(p.z + g0 + n);
+        }
+        if (p.n_scalars > 0) ls0[h] = __ldg(p.scalar[0] + g0 + n);
+        if (p.n_scalars > 1) ls1[h] = __ldg(p.scalar[1] + g0 + n);
+        if (p.need_umag) {
+          lu[h] = __ldg(p.vel[0] + g0 + n);
+          lv[h] = __ldg(p.vel[1] + g0 + n);
+          lw[h] = __ldg(p.vel[2] + g0 + n);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int n = at + kAuxThreads * (hb + h);
+        const double vu = p.need_umag ? mag3(lu[h], lv[h], lw[h]) : 0.0;
+        auto local = [&](int src, int s) -> double {
+          if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], lx[h], ly[h], lz[h]);
+          if (src == SRC_UMAG) return vu;
+          return src == SRC_SCALAR0 ? ls0[h] : ls1[h];
+        };
+        unsigned bits = 0;
+        for (int s = 0; s < p.n_surf; ++s)
+          if (!src_is_grad(p.surf_src[s])) bits |= (local(p.surf_src[s], s) >= p.surf_iso[s] ? 1u : 0u) << s;
+        S_bits[n] = (unsigned char)bits;
+        if (p.color_src >= 0 && !color_grad) {
+          const double c = local(p.color_src, 0);
+          cmin = fmin(cmin, c);
+          cmax = fmax(cmax, c);
+        }
+      }
+    }
   };
 
   // aux warps: scan the per-cell counts of element e, allocate, emit
@@ -396,8 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
           }
         }
       }
-    } else if (k > 0 && p.n_surf > 0) {
-      scan_emit(elem_of(k - 1));                    // the group's previous element
+    } else {
+      if (k < n_k) prepass(e);                      // node-local bits + colour of element k
+      if (k > 0 && p.n_surf > 0) scan_emit(elem_of(k - 1));   // the group's previous element
     }
     pf(1);
     group_bar(g);                                   // derivatives of element k ready
@@ -464,16 +519,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
           p.vort_out[3 * (g0 + n) + 2] = om2;
         }
       }
-      unsigned bits = 0;
-      for (int s = 0; s < p.n_surf; ++s) {
-        const int src = p.surf_src[s];
-        const double val = (src == SRC_Q) ? vq : (src == SRC_WMAG) ? vw : gvalue(src, s, g0, n);
-        bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+      if (grad_surf) {                                // Q / |w| surfaces: OR into the pre-pass bits
+        unsigned bits = 0;
+        for (int s = 0; s < p.n_surf; ++s) {
+          const int src = p.surf_src[s];
+          if (src_is_grad(src)) bits |= ((src == SRC_Q ? vq : vw) >= p.surf_iso[s] ? 1u : 0u) << s;
+        }
+        S_bits[n] |= (unsigned char)bits;
       }
-      S_bits[n] = (unsigned char)bits;
-      if (p.color_src >= 0) {
-        const int src = p.color_src;
-        const double c = (src == SRC_Q) ? vq : (src == SRC_WMAG) ? vw : gvalue(src, 0, g0, n);
+      if (color_grad) {
+        const double c = (p.color_src == SRC_Q) ? vq : vw;
         cmin = fmin(cmin, c);
         cmax = fmax(cmax, c);
       }
