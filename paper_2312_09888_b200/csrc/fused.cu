@@ -1,42 +1,36 @@
 // K1: the fused in situ pass -- SEM->VTK adaptor gather, tensor-product
 // derivatives, Jacobian inverse, velocity gradient, vorticity, Q-criterion,
 // marching-cubes classification of every linear sub-hex and triangle
-// emission, in ONE read of the element's GLL fields from HBM.
+// emission, in ONE read of the element's GLL fields.
 //
-// Persistent, two ping-pong element pipelines per SM.  One CTA (512 threads)
-// per SM walks the elements e_j = blockIdx.x + j*gridDim.x; warp group
-// g = 0, 1 (8 warps each, own shared memory, own named barriers) takes the
-// elements with j % 2 == g.  The groups never wait for each other, so one
-// group's latency-bound node phase overlaps the other's FP64/shared-memory
-// bound derivative phase.  Per element of a group:
+// Persistent, warp-specialised: one CTA (512 threads, 16 warps) per SM walks
+// the elements e_it = blockIdx.x + it*gridDim.x.  Iteration `it`:
 //
-//   6 pencil warps : even-odd 8-point derivatives of x,y,z | u,v,w along
-//                    r,s,t (192 (dir, pencil) threads x 6 fields, smem
-//                    offsets computed once, each coefficient feeds 3 DFMAs)
-//   2 aux warps    : meanwhile node-local pre-pass of the element (plane /
-//                    scalar / |u| case bits, colour range; via L2) and scan,
-//                    allocate and emit the triangles of the group's previous
-//                    element
-//   -- group barrier --
-//   aux warps      : cp.async prefetch of the group's next element
-//   8 warps        : node phase (2 nodes / thread): Jacobian inverse, grad u,
-//                    Q, |w|, Q / |w| case bits
-//   -- group barrier --
-//   8 warps        : classification (one sub-hex per thread)
+//   warps 0-11  (pencils)  : 8-point derivatives of x,y,z | u,v,w along r,s,t
+//                            for element it (384 threads x 3 fields)
+//   warps 12-15 (MC + DMA) : cp.async prefetch of element it+1 (3-stage ring)
+//                            and allocate / emit the triangles of element it-1
+//                            (one triangle per thread)
+//   ---- barrier ----
+//   all 16 warps (nodes)   : one GLL node per thread: Jacobian inverse, grad u,
+//                            Q, |w|, |u|, plane distances, case bits, colour range
+//   ---- barrier ----
+//   all warps (classify)   : one sub-hex per thread: case byte per surface and
+//                            triangle count, kept for the MC warps of it+1
 //
-// Only x,y,z,u,v,w are staged in shared memory (XOR-swizzled, bank-conflict
-// free for node-parallel and r/s/t-pencil access).  Scalars, and the
-// coordinates the node phase and the emission need after the prefetch has
-// recycled the staging slot, are re-read through L2 (the element was streamed
-// a few microseconds earlier), so HBM sees each field byte once.
+// The latency-bound MC work runs in the shadow of the FP64-bound pencils;
+// the fields of every element are read from HBM exactly once.
 //
 // Output slots: FAST mode appends each element's triangles to a region of the
-// triangle buffer private to the CTA (shared-memory counter, no global
-// atomics); the raster walks the regions, an export compacts them.  The
-// triangle order in the buffer therefore depends on the schedule -- the image
-// does not (the raster is an order-independent min); inside an element the
-// order is (cell, surface, table) always.  Deterministic global order
-// (emit_meta) runs COUNT mode, an exclusive scan, then ORDERED mode.
+// triangle buffer private to the CTA (a shared counter, no global atomics);
+// the raster walks the regions, an export compacts them.  Triangle order in
+// the buffer therefore depends on the CTA schedule -- the image does not (the
+// raster is an order-independent min); inside an element the order is
+// (cell, surface, table) always.  Deterministic global order (emit_meta)
+// runs COUNT mode, an exclusive scan of the per-element counts, then ORDERED.
+//
+// Shared memory is XOR-swizzled so node-parallel and r/s/t-pencil accesses
+// are bank-conflict free (2 wavefronts per 64-bit warp access).
 //
 // Reference anchors: the adaptor copy `solver.snapshot_of` (solver.py:282-305)
 // and the AoS layout (data_model.py:8-14) for R11; `scalar_field(':mag')`
@@ -59,7 +53,7 @@ __constant__ double c_D[kNP * kNP];
 __constant__ double c_Ae[4][4];   // even half: 0.5*(D[i][m] + D[i][7-m])
 __constant__ double c_Ao[4][4];   // odd half:  0.5*(D[i][m] - D[i][7-m])
 
-// MC tables in global memory (copied to shared memory once per CTA)
+// MC tables in global memory (read-only path; divergent indices)
 __device__ const unsigned char g_mc_ntri[256] = {NKB_MC_NTRI_DATA};
 __device__ const signed char g_mc_tri[256][3 * NKB_MC_MAX_TRI] = {NKB_MC_TRI_DATA};
 __device__ const unsigned char g_mc_edge_v[12][2] = {NKB_MC_EDGE_V_DATA};
@@ -80,15 +74,12 @@ int set_dmat_constant(const double* dmat) {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kGroupThreads = 256;     // one ping-pong pipeline
-constexpr int kPencilThreads = 192;    // per group: 3 dirs x 64 pencils
-constexpr int kAuxThreads = kGroupThreads - kPencilThreads;   // 64
-constexpr int kArr = kNN;              // 512 doubles per staged array
-constexpr int kNumD = 18;              // derivative arrays: d(f)/d(r,s,t) for x,y,z,u,v,w
-constexpr int kStaged = 6;             // staged arrays: x,y,z,u,v,w
-// per-group dynamic shared memory (doubles): staged + derivatives + (Q, |w|)
-constexpr int kGroupDoubles = (kStaged + kNumD + 2) * kArr;
-constexpr int kCellsPerAux = (kNC + kAuxThreads - 1) / kAuxThreads;   // 6
+constexpr int kPencilThreads = 384;   // 2 groups x 3 dirs x 64 pencils
+constexpr int kMcThreads = kThreads - kPencilThreads;   // 128
+constexpr int kArr = kNN;             // 512 doubles per staged array
+constexpr int kNumD = 18;             // derivative arrays: d(f)/d(r,s,t) for x,y,z,u,v,w
+constexpr int kMaxIn = 8;
+constexpr int kRing = 3;              // input ring: compute it, emit it-1, prefetch it+1
 
 // node (i,j,k) -> shared-memory slot.  Within each 64 B line the 8 doubles
 // are XOR-permuted by (j>>1 | (k&1)<<2); lines are XOR-permuted by (k&1).
@@ -115,13 +106,8 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-// named barriers: group g -> id 1+g over 256 threads; its aux warps -> id 3+g over 64
-__device__ __forceinline__ void group_bar(int g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
-}
-__device__ __forceinline__ void aux_bar(int g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(3 + g), "n"(kAuxThreads) : "memory");
-}
+// barrier among the 4 MC warps only (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void mc_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kMcThreads) : "memory"); }
 
 __device__ __forceinline__ double mag3(double a, double b, double c) {
   // reference ':mag' = sqrt(sum(v**2)) summed left to right (sinks.py:240-241)
@@ -134,202 +120,135 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
 
 __device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
 
-struct GroupScratch {
-  unsigned cases[kNC];          // byte s = case of surface s
-  unsigned char ntri[kNC];      // triangles of each cell (all surfaces)
-  unsigned short coff[kNC];     // exclusive triangle offset of each cell
-  int wtot[kAuxThreads / 32];
-  unsigned long long base;      // output slot of the element's first triangle
-  int total;                    // triangles to emit
-};
-
-struct Shared {
-  GroupScratch grp[2];
-  unsigned char t_ntri[256];
-  signed char t_tri[256][3 * NKB_MC_MAX_TRI];
-  unsigned char t_edge[12][2];
-  unsigned long long cta_fill;  // FAST mode: triangles in this CTA's region
-  double mn[kThreads / 32], mx[kThreads / 32];
+struct McScratch {
+  unsigned cases[2][kNC];       // by element parity: byte s = case of surface s
+  unsigned char ntri[2][kNC];   // triangles of each cell (all surfaces)
+  unsigned coff[kNC + 1];       // exclusive triangle offset of each cell (+ total)
+  int wtot[kMcThreads / 32];
+  unsigned long long base;
 };
 
 }  // namespace
 
 // mode: FUSED_FAST / FUSED_COUNT / FUSED_ORDERED (nkb_internal.h)
-__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nst) {
+__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nin, int slot_sc) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ Shared sh;
+  double* S_ring = smem;                               // kRing * nin * 512
+  double* S_d = S_ring + kRing * nin * kArr;           // 18 * 512 derivatives
+  double* S_q = S_d + kNumD * kArr;                    // 2 x (Q, |w|) * 512, by element parity
+  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 4 * kArr);   // 512 case bits
+  __shared__ McScratch mc;
+  __shared__ double s_mn[kThreads / 32], s_mx[kThreads / 32];
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int g = tid >> 8;                          // ping-pong group
-  const int lt = tid & (kGroupThreads - 1);        // thread index within the group
-  const bool is_pencil = lt < kPencilThreads;
-  const int at = lt - kPencilThreads;              // aux thread index
-  double* S_in = smem + g * kGroupDoubles;         // staged x,y,z,u,v,w (swizzled)
-  double* S_d = S_in + kStaged * kArr;             // 18 derivative arrays
-  double* S_q = S_d + kNumD * kArr;                // Q, |w| of the group's last node phase
-  unsigned char* S_bits = reinterpret_cast<unsigned char*>(smem + 2 * kGroupDoubles) + g * kNN;
-  GroupScratch& gs = sh.grp[g];
-
-  for (int i = tid; i < 256; i += kThreads) sh.t_ntri[i] = g_mc_ntri[i];
-  for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kThreads) (&sh.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
-  if (tid < 24) (&sh.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
-  if (tid == 0) sh.cta_fill = 0;
-  __syncthreads();
-
+  const bool is_mc = tid >= kPencilThreads;
+  const int t = tid - kPencilThreads;                  // MC-warp thread index
   const long long E = p.n_elements;
   const long long G = gridDim.x;
   const long long n_it = (E > blockIdx.x) ? (E - blockIdx.x + G - 1) / G : 0;
-  const long long n_k = (n_it > g) ? (n_it - g + 1) / 2 : 0;   // elements of this group
-  auto elem_of = [&](long long k) { return (long long)blockIdx.x + (2 * k + g) * G; };
-  bool need_xyz = false, grad_surf = false;         // any slice plane / any Q or |w| surface
-  for (int s = 0; s < p.n_surf; ++s) {
-    need_xyz |= p.surf_src[s] >= SRC_PLANE;
-    grad_surf |= src_is_grad(p.surf_src[s]);
-  }
-  const bool color_grad = src_is_grad(p.color_src);
   double cmin = INFINITY, cmax = -INFINITY;
+  unsigned long long cta_fill = 0;     // FAST mode: triangles in this CTA's region (MC thread 0)
 
-  // aux warps: coalesced 8-byte cp.async of element e's staged arrays
-  int qn[kArr / kAuxThreads];
+  // MC warps: coalesced 8-byte cp.async of element `e` into ring slot `b`
+  int qn[4];                                          // swizzled slots of my 4 nodes
 #pragma unroll
-  for (int h = 0; h < kArr / kAuxThreads; ++h) qn[h] = sw_node((at & (kAuxThreads - 1)) + kAuxThreads * h);
-  auto prefetch = [&](long long e) {
-    const long long g0 = e * (long long)kNN + at;
+  for (int h = 0; h < 4; ++h) qn[h] = sw_node(t + kMcThreads * h);
+  auto prefetch = [&](long long e, int b) {
+    double* dst = S_ring + b * nin * kArr;
+    const long long g0 = e * (long long)kNN + t;
 #pragma unroll
-    for (int f = 0; f < kStaged; ++f) {
-      if (f < nst) {
+    for (int f = 0; f < kMaxIn; ++f) {
+      if (f < nin) {
         const double* src = p.in_ptr[f] + g0;
-        double* d = S_in + f * kArr;
+        double* d = dst + f * kArr;
 #pragma unroll
-        for (int h = 0; h < kArr / kAuxThreads; ++h) cp_async8(d + qn[h], src + kAuxThreads * h);
+        for (int h = 0; h < 4; ++h) cp_async8(d + qn[h], src + kMcThreads * h);
       }
     }
   };
 
-  // global (L2-resident) per-node value of a source, by element-local node n
-  auto gvalue = [&](int src, int s, long long g0, int n) -> double {
-    if (src >= SRC_PLANE)
-      return plane_dist(p.surf_n[s], __ldg(p.x + g0 + n), __ldg(p.y + g0 + n), __ldg(p.z + g0 + n));
-    if (src == SRC_UMAG)
-      return mag3(__ldg(p.vel[0] + g0 + n), __ldg(p.vel[1] + g0 + n), __ldg(p.vel[2] + g0 + n));
-    return __ldg(p.scalar[src - SRC_SCALAR0] + g0 + n);
-  };
-
-  // aux warps: node-local classification bits (planes, scalars, |u|) and the
-  // colour range of non-derived colour fields for element e, through L2
-  auto prepass = [&](long long e) {
-    const long long g0 = e * (long long)kNN;
-#pragma unroll 1
-    for (int hb = 0; hb < kArr / kAuxThreads; hb += 4) {
-      double lx[4], ly[4], lz[4], ls0[4], ls1[4], lu[4], lv[4], lw[4];
+  // MC warps: allocate and emit the triangles of element `e` (cases and
+  // per-cell counts were classified by all warps at the end of its iteration)
+  auto mc_element = [&](long long e, int par, const double* S_in, const double* Sq) {
+    int cnt = 0, cc3[3] = {0, 0, 0};
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {      // issue every load of the batch first
-        const int n = at + kAuxThreads * (hb + h);
-        lx[h] = ly[h] = lz[h] = ls0[h] = ls1[h] = lu[h] = lv[h] = lw[h] = 0.0;
-        if (need_xyz) {
-          lx[h] = __ldg(p.x + g0 + n);
-          ly[h] = __ldg(p.y + g0 + n);
-          lz[h] = __ldg(p.z + g0 + n);
-        }
-        if (p.n_scalars > 0) ls0[h] = __ldg(p.scalar[0] + g0 + n);
-        if (p.n_scalars > 1) ls1[h] = __ldg(p.scalar[1] + g0 + n);
-        if (p.need_umag) {
-          lu[h] = __ldg(p.vel[0] + g0 + n);
-          lv[h] = __ldg(p.vel[1] + g0 + n);
-          lw[h] = __ldg(p.vel[2] + g0 + n);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int n = at + kAuxThreads * (hb + h);
-        const double vu = p.need_umag ? mag3(lu[h], lv[h], lw[h]) : 0.0;
-        auto local = [&](int src, int s) -> double {
-          if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], lx[h], ly[h], lz[h]);
-          if (src == SRC_UMAG) return vu;
-          return src == SRC_SCALAR0 ? ls0[h] : ls1[h];
-        };
-        unsigned bits = 0;
-        for (int s = 0; s < p.n_surf; ++s)
-          if (!src_is_grad(p.surf_src[s])) bits |= (local(p.surf_src[s], s) >= p.surf_iso[s] ? 1u : 0u) << s;
-        S_bits[n] = (unsigned char)bits;
-        if (p.color_src >= 0 && !color_grad) {
-          const double c = local(p.color_src, 0);
-          cmin = fmin(cmin, c);
-          cmax = fmax(cmax, c);
-        }
+    for (int j = 0; j < 3; ++j) {
+      const int c = 3 * t + j;
+      if (c < kNC) {
+        cc3[j] = mc.ntri[par][c];
+        cnt += cc3[j];
       }
     }
-  };
-
-  // aux warps: scan the per-cell counts of element e, allocate, emit
-  auto scan_emit = [&](long long e) {
-    int cc[kCellsPerAux], cnt = 0;
-#pragma unroll
-    for (int j = 0; j < kCellsPerAux; ++j) {
-      const int c = kCellsPerAux * at + j;
-      cc[j] = (c < kNC) ? gs.ntri[c] : 0;
-      cnt += cc[j];
-    }
+    // exclusive scan over the 128 MC threads (cell-major order)
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int aw = at >> 5;
-    if (lane == 31) gs.wtot[aw] = incl;
-    aux_bar(g);
-    const int w0 = gs.wtot[0], w1 = gs.wtot[1];
-    const int total = w0 + w1;
-    int run = (aw ? w0 : 0) + incl - cnt;
+    const int mw = warp - kPencilThreads / 32;
+    if (lane == 31) mc.wtot[mw] = incl;
+    mc_bar();
+    int before = 0, total = 0;
 #pragma unroll
-    for (int j = 0; j < kCellsPerAux; ++j) {
-      const int c = kCellsPerAux * at + j;
-      if (c < kNC) gs.coff[c] = (unsigned short)run;
-      run += cc[j];
+    for (int w = 0; w < kMcThreads / 32; ++w) {
+      const int v = mc.wtot[w];
+      before += (w < mw) ? v : 0;
+      total += v;
     }
-    if (at == 0) {
+    int run = before + incl - cnt;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = 3 * t + j;
+      if (c < kNC) {
+        mc.coff[c] = run;
+        run += cc3[j];
+      }
+    }
+    if (t == 0) {
+      mc.coff[kNC] = total;
       unsigned long long base = 0;
-      int emit_total = total;
       if (p.mode == FUSED_FAST) {
-        // CTA-private region of the triangle buffer: shared counter only
-        base = (unsigned long long)blockIdx.x * (unsigned long long)p.region_cap +
-               (total ? atomicAdd(&sh.cta_fill, (unsigned long long)total) : 0ULL);
+        // CTA-private region of the triangle buffer: no global atomics
+        base = (unsigned long long)blockIdx.x * (unsigned long long)p.region_cap + cta_fill;
+        cta_fill += (unsigned long long)total;
       } else if (p.mode == FUSED_COUNT) {
         p.elem_count[e] = total;
-        emit_total = 0;
       } else {
         base = (unsigned long long)p.elem_offset[e];
       }
-      gs.base = base;
-      gs.total = emit_total;
+      mc.base = base;
     }
-    aux_bar(g);
-    const int emit_total = gs.total;
-    if (emit_total == 0) return;
-    const unsigned long long base = gs.base;
-    const long long g0 = e * (long long)kNN;
-    const double* Sq = S_q;
-    auto value_at = [&](int src, int s, int n) -> double {
-      if (src == SRC_Q) return Sq[sw_node(n)];
-      if (src == SRC_WMAG) return Sq[kArr + sw_node(n)];
-      return gvalue(src, s, g0, n);
+    mc_bar();
+    if (p.mode == FUSED_COUNT || total == 0) return;
+    const unsigned long long base = mc.base;
+    const double* Sx = S_in;
+    const double* Sy = S_in + kArr;
+    const double* Sz = S_in + 2 * kArr;
+    const double* Su = S_in + 3 * kArr;
+    auto value_at = [&](int src, int s, int q) -> double {
+      if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
+      if (src == SRC_Q) return Sq[q];
+      if (src == SRC_WMAG) return Sq[kArr + q];
+      if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
+      return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
     };
-    for (int tt = at; tt < emit_total; tt += kAuxThreads) {
-      int lo = 0, hi = kNC - 1;          // last cell with coff <= tt
+    for (int tt = t; tt < total; tt += kMcThreads) {
+      // cell owning triangle tt: last c with coff[c] <= tt
+      int lo = 0, hi = kNC - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if ((int)gs.coff[mid] <= tt) lo = mid;
+        if ((int)mc.coff[mid] <= tt) lo = mid;
         else hi = mid - 1;
       }
       const int c = lo;
-      int li = tt - (int)gs.coff[c];
-      const unsigned packed = gs.cases[c];
+      int li = tt - (int)mc.coff[c];
+      const unsigned packed = mc.cases[par][c];
       int s = 0;
       unsigned cs = packed & 0xffu;
       for (;;) {
-        const int nt = sh.t_ntri[cs];
+        const int nt = g_mc_ntri[cs];
         if (li < nt) break;
         li -= nt;
         ++s;
@@ -346,19 +265,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       float4 vtx[3];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        const int ed = sh.t_tri[cs][3 * k + r];
-        const int va = sh.t_edge[ed][0], vb = sh.t_edge[ed][1];
-        const int na = (ca + voff_i(va)) + kNP * (cb + voff_j(va)) + kNP * kNP * (ck + voff_k(va));
-        const int nb = (ca + voff_i(vb)) + kNP * (cb + voff_j(vb)) + kNP * kNP * (ck + voff_k(vb));
-        const double sa = value_at(src, s, na), sb = value_at(src, s, nb);
+        const int ed = g_mc_tri[cs][3 * k + r];
+        const int va = g_mc_edge_v[ed][0], vb = g_mc_edge_v[ed][1];
+        const int qa = sw(ca + voff_i(va), cb + voff_j(va), ck + voff_k(va));
+        const int qb = sw(ca + voff_i(vb), cb + voff_j(vb), ck + voff_k(vb));
+        const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
         const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
-        const double cla = value_at(p.color_src, 0, na), clb = value_at(p.color_src, 0, nb);
-        const double xa = __ldg(p.x + g0 + na), xb = __ldg(p.x + g0 + nb);
-        const double ya = __ldg(p.y + g0 + na), yb = __ldg(p.y + g0 + nb);
-        const double za = __ldg(p.z + g0 + na), zb = __ldg(p.z + g0 + nb);
-        vtx[r].x = __double2float_rn(__fma_rn(tv, __dsub_rn(xb, xa), xa));
-        vtx[r].y = __double2float_rn(__fma_rn(tv, __dsub_rn(yb, ya), ya));
-        vtx[r].z = __double2float_rn(__fma_rn(tv, __dsub_rn(zb, za), za));
+        const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
+        vtx[r].x = __double2float_rn(__fma_rn(tv, __dsub_rn(Sx[qb], Sx[qa]), Sx[qa]));
+        vtx[r].y = __double2float_rn(__fma_rn(tv, __dsub_rn(Sy[qb], Sy[qa]), Sy[qa]));
+        vtx[r].z = __double2float_rn(__fma_rn(tv, __dsub_rn(Sz[qb], Sz[qa]), Sz[qa]));
         vtx[r].w = __double2float_rn(__fma_rn(tv, __dsub_rn(clb, cla), cla));
       }
       float4* dst = p.tri + 3 * out;
@@ -371,104 +287,97 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   };
 
-  // optional phase profile (p.prof != nullptr): cycles per phase, lt == 0 and at == 0
-  long long pf_t = clock64(), pf_acc[4] = {0, 0, 0, 0};
-  auto pf = [&](int k) {
-    if (p.prof && (lt == 0 || at == 0)) {
-      const long long now = clock64();
-      pf_acc[k] += now - pf_t;
-      pf_t = now;
-    }
-  };
-
-  if (!is_pencil && n_k > 0) prefetch(elem_of(0));
+  if (is_mc && n_it > 0) prefetch(blockIdx.x, 0);
   cp_async_commit();
-  for (long long k = 0; k <= n_k; ++k) {
-    const long long e = elem_of(k);
-    if (!is_pencil) cp_async_wait_all();
-    group_bar(g);                                   // element k staged; classify k-1 done
-    pf(0);
-    if (is_pencil) {
-      if (k < n_k && p.need_grad) {
-        // ---- pencils: thread = (dir, pencil); 2 triples of fields share offsets ----
-        const int dir = lt >> 6;                    // warp-uniform
-        const int pa = lt & 7, pb = (lt >> 3) & 7;
-        int off[kNP];
-        if (dir == 0) {
-#pragma unroll
-          for (int m = 0; m < kNP; ++m) off[m] = sw(m, pa, pb);
-        } else if (dir == 1) {
-#pragma unroll
-          for (int m = 0; m < kNP; ++m) off[m] = sw(pa, m, pb);
-        } else {
-#pragma unroll
-          for (int m = 0; m < kNP; ++m) off[m] = sw(pa, pb, m);
-        }
-#pragma unroll 1
-        for (int tg = 0; tg < 2; ++tg) {
-          const double* s0 = S_in + (3 * tg + 0) * kArr;
-          const double* s1 = S_in + (3 * tg + 1) * kArr;
-          const double* s2 = S_in + (3 * tg + 2) * kArr;
-          double* d0 = S_d + (3 * (3 * tg + 0) + dir) * kArr;
-          double* d1 = S_d + (3 * (3 * tg + 1) + dir) * kArr;
-          double* d2 = S_d + (3 * (3 * tg + 2) + dir) * kArr;
-          double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const double a0 = s0[off[m]], b0 = s0[off[kNP - 1 - m]];
-            const double a1 = s1[off[m]], b1 = s1[off[kNP - 1 - m]];
-            const double a2 = s2[off[m]], b2 = s2[off[kNP - 1 - m]];
-            e0[m] = __dadd_rn(a0, b0);
-            o0[m] = __dsub_rn(a0, b0);
-            e1[m] = __dadd_rn(a1, b1);
-            o1[m] = __dsub_rn(a1, b1);
-            e2[m] = __dadd_rn(a2, b2);
-            o2[m] = __dsub_rn(a2, b2);
-          }
-          // even-odd form (oracle deriv8): out[i] = E_i + O_i, out[7-i] = O_i - E_i
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const double ce = c_Ae[i][0], co = c_Ao[i][0];
-            double E0 = __dmul_rn(ce, e0[0]), E1 = __dmul_rn(ce, e1[0]), E2 = __dmul_rn(ce, e2[0]);
-            double O0 = __dmul_rn(co, o0[0]), O1 = __dmul_rn(co, o1[0]), O2 = __dmul_rn(co, o2[0]);
-#pragma unroll
-            for (int m = 1; m < 4; ++m) {
-              const double ae = c_Ae[i][m], ao = c_Ao[i][m];
-              E0 = __fma_rn(ae, e0[m], E0);
-              E1 = __fma_rn(ae, e1[m], E1);
-              E2 = __fma_rn(ae, e2[m], E2);
-              O0 = __fma_rn(ao, o0[m], O0);
-              O1 = __fma_rn(ao, o1[m], O1);
-              O2 = __fma_rn(ao, o2[m], O2);
-            }
-            d0[off[i]] = __dadd_rn(E0, O0);
-            d1[off[i]] = __dadd_rn(E1, O1);
-            d2[off[i]] = __dadd_rn(E2, O2);
-            d0[off[kNP - 1 - i]] = __dsub_rn(O0, E0);
-            d1[off[kNP - 1 - i]] = __dsub_rn(O1, E1);
-            d2[off[kNP - 1 - i]] = __dsub_rn(O2, E2);
-          }
-        }
-      }
-    } else {
-      if (k < n_k) prepass(e);                      // node-local bits + colour of element k
-      if (k > 0 && p.n_surf > 0) scan_emit(elem_of(k - 1));   // the group's previous element
-    }
-    pf(1);
-    group_bar(g);                                   // derivatives of element k ready
-    if (k == n_k) break;
-    pf(2);
-    if (!is_pencil) {
-      if (k + 1 < n_k) prefetch(elem_of(k + 1));    // staging slot free: pencils are done
+  for (long long it = 0; it <= n_it; ++it) {
+    const long long e = blockIdx.x + it * G;
+    const int slot = (int)(it % kRing);
+    const int par = (int)(it & 1);
+    if (is_mc) cp_async_wait_all();
+    __syncthreads();                                   // element `it` staged; node phase it-1 done
+    const double* S_in = S_ring + slot * nin * kArr;
+    if (is_mc) {
+      if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
       cp_async_commit();
+      if (it > 0 && p.n_surf > 0) {
+        const int ps = (int)((it - 1) % kRing), pp = (int)((it - 1) & 1);
+        mc_element(e - G, pp, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr);
+      }
+    } else if (it < n_it && p.need_grad) {
+      // ---- pencils: thread = (group, dir, pencil); 3 fields share offsets ----
+      const int g = tid / 192;                      // 0: x,y,z   1: u,v,w  (warp-uniform)
+      const int dir = (tid % 192) >> 6;             // warp-uniform
+      const int pa = tid & 7, pb = (tid >> 3) & 7;
+      int off[kNP];
+      if (dir == 0) {
+#pragma unroll
+        for (int m = 0; m < kNP; ++m) off[m] = sw(m, pa, pb);
+      } else if (dir == 1) {
+#pragma unroll
+        for (int m = 0; m < kNP; ++m) off[m] = sw(pa, m, pb);
+      } else {
+#pragma unroll
+        for (int m = 0; m < kNP; ++m) off[m] = sw(pa, pb, m);
+      }
+      const double* s0 = S_in + (3 * g + 0) * kArr;   // staged slot == field index
+      const double* s1 = S_in + (3 * g + 1) * kArr;
+      const double* s2 = S_in + (3 * g + 2) * kArr;
+      double* d0 = S_d + (3 * (3 * g + 0) + dir) * kArr;
+      double* d1 = S_d + (3 * (3 * g + 1) + dir) * kArr;
+      double* d2 = S_d + (3 * (3 * g + 2) + dir) * kArr;
+      double v0[kNP], v1[kNP], v2[kNP];
+#pragma unroll
+      for (int m = 0; m < kNP; ++m) {
+        v0[m] = s0[off[m]];
+        v1[m] = s1[off[m]];
+        v2[m] = s2[off[m]];
+      }
+      // even-odd form (oracle deriv8): e_m = v_m + v_{7-m}, o_m = v_m - v_{7-m},
+      // out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 fields
+      double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        e0[m] = __dadd_rn(v0[m], v0[kNP - 1 - m]);
+        o0[m] = __dsub_rn(v0[m], v0[kNP - 1 - m]);
+        e1[m] = __dadd_rn(v1[m], v1[kNP - 1 - m]);
+        o1[m] = __dsub_rn(v1[m], v1[kNP - 1 - m]);
+        e2[m] = __dadd_rn(v2[m], v2[kNP - 1 - m]);
+        o2[m] = __dsub_rn(v2[m], v2[kNP - 1 - m]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double ce = c_Ae[i][0], co = c_Ao[i][0];
+        double E0 = __dmul_rn(ce, e0[0]), E1 = __dmul_rn(ce, e1[0]), E2 = __dmul_rn(ce, e2[0]);
+        double O0 = __dmul_rn(co, o0[0]), O1 = __dmul_rn(co, o1[0]), O2 = __dmul_rn(co, o2[0]);
+#pragma unroll
+        for (int m = 1; m < 4; ++m) {
+          const double ae = c_Ae[i][m], ao = c_Ao[i][m];
+          E0 = __fma_rn(ae, e0[m], E0);
+          E1 = __fma_rn(ae, e1[m], E1);
+          E2 = __fma_rn(ae, e2[m], E2);
+          O0 = __fma_rn(ao, o0[m], O0);
+          O1 = __fma_rn(ao, o1[m], O1);
+          O2 = __fma_rn(ao, o2[m], O2);
+        }
+        d0[off[i]] = __dadd_rn(E0, O0);
+        d1[off[i]] = __dadd_rn(E1, O1);
+        d2[off[i]] = __dadd_rn(E2, O2);
+        d0[off[kNP - 1 - i]] = __dsub_rn(O0, E0);
+        d1[off[kNP - 1 - i]] = __dsub_rn(O1, E1);
+        d2[off[kNP - 1 - i]] = __dsub_rn(O2, E2);
+      }
     }
+    if (it == n_it) break;
+    __syncthreads();                                   // derivatives of element `it` ready
 
-    // ---- node phase: nodes lt and lt + 256 ----
-    const long long g0 = e * (long long)kNN;
-#pragma unroll 1
-    for (int n = lt; n < kNN; n += kGroupThreads) {
+    // ---- node phase: one node per thread ----
+    {
+      const int n = tid;
       const int q = sw_node(n);
-      double vq = 0.0, vw = 0.0;
+      const long long g0 = e * (long long)kNN;
+      double* Sq = S_q + par * 2 * kArr;
+      unsigned char* bits_out = S_bits;
+      double vq = 0.0, vw = 0.0, vu = 0.0;
       if (p.need_grad) {
         double G9[9];
 #pragma unroll
@@ -506,10 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         const double om0 = __dsub_rn(A[7], A[5]);
         const double om1 = __dsub_rn(A[2], A[6]);
         const double om2 = __dsub_rn(A[3], A[1]);
-        S_q[q] = vq;
+        Sq[q] = vq;
         if (p.need_wmag) {
           vw = mag3(om0, om1, om2);
-          S_q[kArr + q] = vw;
+          Sq[kArr + q] = vw;
         }
         if (p.q_out) p.q_out[g0 + n] = vq;
         if (p.wmag_out) p.wmag_out[g0 + n] = vw;
@@ -519,28 +428,37 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
           p.vort_out[3 * (g0 + n) + 2] = om2;
         }
       }
-      if (grad_surf) {                                // Q / |w| surfaces: OR into the pre-pass bits
-        unsigned bits = 0;
-        for (int s = 0; s < p.n_surf; ++s) {
-          const int src = p.surf_src[s];
-          if (src_is_grad(src)) bits |= ((src == SRC_Q ? vq : vw) >= p.surf_iso[s] ? 1u : 0u) << s;
-        }
-        S_bits[n] |= (unsigned char)bits;
+      if (p.need_umag) vu = mag3(S_in[3 * kArr + q], S_in[4 * kArr + q], S_in[5 * kArr + q]);
+      unsigned bits = 0;
+      for (int s = 0; s < p.n_surf; ++s) {
+        const int src = p.surf_src[s];
+        double val;
+        if (src >= SRC_PLANE) val = plane_dist(p.surf_n[s], S_in[q], S_in[kArr + q], S_in[2 * kArr + q]);
+        else if (src == SRC_Q) val = vq;
+        else if (src == SRC_WMAG) val = vw;
+        else if (src == SRC_UMAG) val = vu;
+        else val = S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+        bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
       }
-      if (color_grad) {
-        const double c = (p.color_src == SRC_Q) ? vq : vw;
+      bits_out[n] = (unsigned char)bits;
+      if (p.color_src >= 0) {
+        const int src = p.color_src;
+        const double c = (src == SRC_Q)      ? vq
+                         : (src == SRC_WMAG) ? vw
+                         : (src == SRC_UMAG) ? vu
+                                             : S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
         cmin = fmin(cmin, c);
         cmax = fmax(cmax, c);
       }
     }
-    pf(3);
     if (p.n_surf == 0) continue;
-    group_bar(g);                                   // case bits of element k ready
+    __syncthreads();                                   // case bits of element `it` ready
 
-    // ---- classify: cells lt and lt + 256 ----
-    for (int c = lt; c < kNC; c += kGroupThreads) {
-      const int a = c % kN, b = (c / kN) % kN, kk = c / (kN * kN);
-      const int n0 = a + kNP * b + kNP * kNP * kk;
+    // ---- classify: one sub-hex per thread (all warps) ----
+    if (tid < kNC) {
+      const int c = tid;
+      const int a = c % kN, b = (c / kN) % kN, k = c / (kN * kN);
+      const int n0 = a + kNP * b + kNP * kNP * k;
       unsigned cb[8];
 #pragma unroll
       for (int v = 0; v < 8; ++v) cb[v] = S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
@@ -551,22 +469,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
 #pragma unroll
         for (int v = 0; v < 8; ++v) cs |= ((cb[v] >> s) & 1u) << v;
         packed |= cs << (8 * s);
-        nc += sh.t_ntri[cs];
+        nc += g_mc_ntri[cs];
       }
-      gs.cases[c] = packed;
-      gs.ntri[c] = (unsigned char)nc;
+      mc.cases[par][c] = packed;
+      mc.ntri[par][c] = (unsigned char)nc;
     }
-    pf(2);
   }
 
-  if (p.prof && (lt == 0 || at == 0)) {
-    long long* dst = p.prof + (long long)blockIdx.x * 16 + g * 8 + (lt == 0 ? 0 : 4);
-    for (int k = 0; k < 4; ++k) dst[k] = pf_acc[k];
-  }
-  __syncthreads();
-  if (p.mode == FUSED_FAST && p.region_count != nullptr && tid == 0) {
-    p.region_count[blockIdx.x] = sh.cta_fill;
-    if (sh.cta_fill) atomicAdd(&p.counters[0], sh.cta_fill);
+  if (p.mode == FUSED_FAST && p.region_count != nullptr && tid == kPencilThreads) {
+    p.region_count[blockIdx.x] = cta_fill;
+    if (cta_fill) atomicAdd(&p.counters[0], cta_fill);
   }
   // colour range of all elements this CTA processed: one ordered atomic pair
   if (p.color_src >= 0 && p.mode != FUSED_ORDERED) {
@@ -576,15 +488,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
     }
     if (lane == 0) {
-      sh.mn[warp] = cmin;
-      sh.mx[warp] = cmax;
+      s_mn[warp] = cmin;
+      s_mx[warp] = cmax;
     }
     __syncthreads();
     if (tid == 0) {
-      double mn = sh.mn[0], mx = sh.mx[0];
+      double mn = s_mn[0], mx = s_mx[0];
       for (int w = 1; w < kThreads / 32; ++w) {
-        mn = fmin(mn, sh.mn[w]);
-        mx = fmax(mx, sh.mx[w]);
+        mn = fmin(mn, s_mn[w]);
+        mx = fmax(mx, s_mx[w]);
       }
       if (mn <= mx) {
         atomicMin(&p.counters[1], enc_ordered(mn));
@@ -593,7 +505,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   }
 }
-
 
 // exclusive scan of per-element triangle counts (ordered mode); single CTA
 __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict__ cnt, long long n,
@@ -677,27 +588,34 @@ int launch_compact(const float4* tri, const unsigned long long* meta, const unsi
   return NKB_OK;
 }
 
-static size_t fused_smem_bytes() {
-  return (size_t)2 * kGroupDoubles * sizeof(double) + 2 * kNN;
+static size_t fused_smem_bytes(int nin) {
+  return (size_t)(kRing * nin + kNumD + 4) * kArr * sizeof(double) + 2 * kNN;
 }
 
 int launch_fused(const FusedParams& p, cudaStream_t s) {
   if (p.n_elements <= 0) return NKB_OK;
-  const int nst = p.need_vel ? 6 : 3;
-  const size_t shm = fused_smem_bytes();
+  const int nin = 3 + (p.need_vel ? 3 : 0) + p.n_scalars;
+  const int slot_sc = 3 + (p.need_vel ? 3 : 0);
+  const size_t shm = fused_smem_bytes(nin);
   static bool attr_set = false;
   if (!attr_set) {
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)fused_smem_bytes(kMaxIn)));
+    int dev = 0;
+    NKB_CUDA(cudaGetDevice(&dev));
+    NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     attr_set = true;
   }
-  FusedParams q = p;   // staged inputs in slot order: x, y, z, [u, v, w]
-  q.in_ptr[0] = p.x;
-  q.in_ptr[1] = p.y;
-  q.in_ptr[2] = p.z;
+  FusedParams q = p;   // staged inputs in slot order: x, y, z, [u, v, w], [scalars]
+  int k = 0;
+  q.in_ptr[k++] = p.x;
+  q.in_ptr[k++] = p.y;
+  q.in_ptr[k++] = p.z;
   if (p.need_vel)
-    for (int c = 0; c < 3; ++c) q.in_ptr[3 + c] = p.vel[c];
+    for (int c = 0; c < 3; ++c) q.in_ptr[k++] = p.vel[c];
+  for (int c = 0; c < p.n_scalars; ++c) q.in_ptr[k++] = p.scalar[c];
   const int grid = fused_grid(p.n_elements);
-  fused_kernel<<<(unsigned)grid, kThreads, shm, s>>>(q, nst);
+  fused_kernel<<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
