@@ -120,13 +120,26 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
 
 __device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
 
+constexpr int kMaxTriPerElem = kNC * NKB_MC_MAX_TRI * NKB_MAX_SURFACES;   // 6860
+
 struct McScratch {
   unsigned cases[2][kNC];       // by element parity: byte s = case of surface s
   unsigned char ntri[2][kNC];   // triangles of each cell (all surfaces)
-  unsigned coff[kNC + 1];       // exclusive triangle offset of each cell (+ total)
+  unsigned short coff[kNC];     // exclusive triangle offset of each cell
+  unsigned short tri_cell[kMaxTriPerElem];   // cell of each triangle of the element
   int wtot[kMcThreads / 32];
   unsigned long long base;
+  // marching-cubes tables, copied once per CTA
+  unsigned char t_ntri[256];
+  signed char t_tri[256][3 * NKB_MC_MAX_TRI];
+  unsigned char t_edge[12][2];
 };
+
+// case byte of surface s from the 8 corner bit-bytes packed in w (byte v =
+// bits of corner v): gather bit s of every byte into one byte (bit v)
+__device__ __forceinline__ unsigned case_of(unsigned long long w, int s) {
+  return (unsigned)((((w >> s) & 0x0101010101010101ULL) * 0x0102040810204080ULL) >> 56);
+}
 
 }  // namespace
 
@@ -202,12 +215,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     for (int j = 0; j < 3; ++j) {
       const int c = 3 * t + j;
       if (c < kNC) {
-        mc.coff[c] = run;
+        mc.coff[c] = (unsigned short)run;
+        for (int q = 0; q < cc3[j]; ++q) mc.tri_cell[run + q] = (unsigned short)c;
         run += cc3[j];
       }
     }
     if (t == 0) {
-      mc.coff[kNC] = total;
       unsigned long long base = 0;
       if (p.mode == FUSED_FAST) {
         // CTA-private region of the triangle buffer: no global atomics
@@ -235,20 +248,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
     };
     for (int tt = t; tt < total; tt += kMcThreads) {
-      // cell owning triangle tt: last c with coff[c] <= tt
-      int lo = 0, hi = kNC - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if ((int)mc.coff[mid] <= tt) lo = mid;
-        else hi = mid - 1;
-      }
-      const int c = lo;
+      const int c = mc.tri_cell[tt];
       int li = tt - (int)mc.coff[c];
       const unsigned packed = mc.cases[par][c];
       int s = 0;
       unsigned cs = packed & 0xffu;
       for (;;) {
-        const int nt = g_mc_ntri[cs];
+        const int nt = mc.t_ntri[cs];
         if (li < nt) break;
         li -= nt;
         ++s;
@@ -265,8 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       float4 vtx[3];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        const int ed = g_mc_tri[cs][3 * k + r];
-        const int va = g_mc_edge_v[ed][0], vb = g_mc_edge_v[ed][1];
+        const int ed = mc.t_tri[cs][3 * k + r];
+        const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
         const int qa = sw(ca + voff_i(va), cb + voff_j(va), ck + voff_k(va));
         const int qb = sw(ca + voff_i(vb), cb + voff_j(vb), ck + voff_k(vb));
         const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
@@ -287,6 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   };
 
+  for (int i = tid; i < 256; i += kThreads) mc.t_ntri[i] = g_mc_ntri[i];
+  for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kThreads) (&mc.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
+  if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
   if (is_mc && n_it > 0) prefetch(blockIdx.x, 0);
   cp_async_commit();
   for (long long it = 0; it <= n_it; ++it) {
@@ -459,17 +468,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       const int c = tid;
       const int a = c % kN, b = (c / kN) % kN, k = c / (kN * kN);
       const int n0 = a + kNP * b + kNP * kNP * k;
-      unsigned cb[8];
+      unsigned long long w = 0;
 #pragma unroll
-      for (int v = 0; v < 8; ++v) cb[v] = S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)];
+      for (int v = 0; v < 8; ++v)
+        w |= (unsigned long long)S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)] << (8 * v);
       unsigned packed = 0;
       int nc = 0;
       for (int s = 0; s < p.n_surf; ++s) {
-        unsigned cs = 0;
-#pragma unroll
-        for (int v = 0; v < 8; ++v) cs |= ((cb[v] >> s) & 1u) << v;
+        const unsigned cs = case_of(w, s);
         packed |= cs << (8 * s);
-        nc += g_mc_ntri[cs];
+        nc += mc.t_ntri[cs];
       }
       mc.cases[par][c] = packed;
       mc.ntri[par][c] = (unsigned char)nc;
