@@ -31,6 +31,23 @@ METRIC = "GLL points/sec per in situ step (adaptor+Q-crit+iso+render) at 1/2/4/8
 UNIT = "GLL points/s"
 
 
+class _StdoutToStderr:
+    """Native libraries (NCCL's version banner) write to fd 1; the driver
+    expects exactly one JSON line there.  Route fd 1 to fd 2 meanwhile."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+        return False
+
+
 def _env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -151,8 +168,9 @@ def run_ours(a):
 
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
-    ctx = Context(local)
-    comm = Communicator.from_torch(ctx) if world > 1 else None
+    with _StdoutToStderr():
+        ctx = Context(local)
+        comm = Communicator.from_torch(ctx) if world > 1 else None
 
     # the workload lives in HBM before timing starts (device-side generator)
     from paper_2312_09888_b200 import synth_device
