@@ -214,12 +214,14 @@ def run_ours(a):
     barrier()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fused_ms, ntri = [], 0
+    fused_ms, ntri, stages = [], 0, []
     e0.record(stream)
     for _ in range(a.steps):
         res = an.execute(da, fetch_image=False)
         fused_ms.append(res.report.ms_fused)
         ntri = res.report.n_triangles
+        r = res.report
+        stages.append((r.ms_fused, r.ms_raster, r.ms_composite, r.ms_resolve))
     e1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -298,6 +300,8 @@ def run_ours(a):
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": "fused_kernel",
                      "kernel_ms": fused, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
                      "bytes_per_point": _bytes_read_per_point(case), "triangles": ntri},
+        "stages_ms": dict(zip(("fused", "raster", "composite", "resolve"),
+                              (round(statistics.mean(x), 4) for x in zip(*stages)))),
         "gpu_launches": 5 * a.steps,
         "clocks": clk,
     }
