@@ -228,6 +228,15 @@ def run_ours(a):
     ms = max_over_ranks(e0.elapsed_time(e1)) / a.steps
     value = world * npts / (ms / 1e3)      # every rank holds npts (weak scaling)
 
+    per_rank = [statistics.mean(fused_ms), float(ntri)]
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank)
+        per_rank_fused = [round(g[0], 4) for g in gathered]
+        per_rank_tri = [int(g[1]) for g in gathered]
+    else:
+        per_rank_fused, per_rank_tri = [round(per_rank[0], 4)], [ntri]
+
     # roofline of the dominant kernel (fused adaptor+grad+Q+MC pass)
     peaks, peak_kind = _peaks()
     fused = statistics.mean(fused_ms)
@@ -302,6 +311,8 @@ def run_ours(a):
                      "bytes_per_point": _bytes_read_per_point(case), "triangles": ntri},
         "stages_ms": dict(zip(("fused", "raster", "composite", "resolve"),
                               (round(statistics.mean(x), 4) for x in zip(*stages)))),
+        "fused_ms_per_rank": per_rank_fused,
+        "triangles_per_rank": per_rank_tri,
         "gpu_launches": 5 * a.steps,
         "clocks": clk,
     }
