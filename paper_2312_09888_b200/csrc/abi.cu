@@ -40,6 +40,7 @@ struct NcclApi {
                          cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -62,6 +63,7 @@ static int load_nccl() {
   NKB_SYM(CommDestroy, "ncclCommDestroy");
   NKB_SYM(Reduce, "ncclReduce");
   NKB_SYM(AllReduce, "ncclAllReduce");
+  NKB_SYM(AllGather, "ncclAllGather");
   NKB_SYM(GroupStart, "ncclGroupStart");
   NKB_SYM(GroupEnd, "ncclGroupEnd");
   NKB_SYM(GetErrorString, "ncclGetErrorString");
@@ -146,7 +148,97 @@ struct nkb_ctx {
   int rank = 0, nranks = 1;
   cudaEvent_t ev[6] = {};
   long long* prof = nullptr;                 // debug phase profile (NKB_PROFILE_PHASES=1)
+  // P2P composite state (composite.cu)
+  struct {
+    bool ready = false, unavailable = false;
+    int W = 0, H = 0;
+    unsigned long long* keys[2] = {nullptr, nullptr};
+    unsigned long long* flags = nullptr;
+    int* err = nullptr;
+    std::vector<void*> opened;
+    const unsigned long long* peer_keys[2][kMaxRanks] = {};
+    unsigned long long* peer_flags[kMaxRanks] = {};
+    unsigned char* root_rgba = nullptr;
+    float* root_depth = nullptr;
+    unsigned long long epoch = 0;
+  } p2p;
 };
+
+static void p2p_release(nkb_ctx* ctx) {
+  for (void* q : ctx->p2p.opened) cudaIpcCloseMemHandle(q);
+  ctx->p2p.opened.clear();
+  cudaFree(ctx->p2p.keys[0]);
+  cudaFree(ctx->p2p.keys[1]);
+  cudaFree(ctx->p2p.flags);
+  cudaFree(ctx->p2p.err);
+  ctx->p2p.keys[0] = ctx->p2p.keys[1] = nullptr;
+  ctx->p2p.flags = nullptr;
+  ctx->p2p.err = nullptr;
+  ctx->p2p.ready = false;
+}
+
+// collective: every rank calls it with the same image size.  Allocates the two
+// key buffers and the flag array, then exchanges CUDA IPC handles (keys x2,
+// flags, and the image of every rank) with one ncclAllGather.
+static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
+  auto& P = ctx->p2p;
+  if (P.ready && P.W == W && P.H == H) return NKB_OK;
+  if (P.ready) {
+    NKB_CUDA(cudaStreamSynchronize(s));
+    p2p_release(ctx);
+  }
+  const size_t npx = (size_t)W * H;
+  NKB_CUDA(cudaMalloc(&P.keys[0], (npx + 2) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&P.keys[1], (npx + 2) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&P.flags, 3 * kMaxRanks * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMemset(P.flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&P.err, sizeof(int)));
+  NKB_CUDA(cudaMemset(P.err, 0, sizeof(int)));
+  constexpr int kH = 5;
+  cudaIpcMemHandle_t mine[kH];
+  void* ptrs[kH] = {P.keys[0], P.keys[1], P.flags, ctx->rgba, ctx->depth};
+  for (int i = 0; i < kH; ++i) NKB_CUDA(cudaIpcGetMemHandle(&mine[i], ptrs[i]));
+  const size_t hb = sizeof(mine);
+  char *d_send = nullptr, *d_recv = nullptr;
+  NKB_CUDA(cudaMalloc(&d_send, hb));
+  NKB_CUDA(cudaMalloc(&d_recv, hb * ctx->nranks));
+  NKB_CUDA(cudaMemcpy(d_send, mine, hb, cudaMemcpyHostToDevice));
+  NKB_NCCL(g_nccl.AllGather(d_send, d_recv, hb, ncclChar, ctx->comm, s));
+  std::vector<cudaIpcMemHandle_t> all((size_t)kH * ctx->nranks);
+  NKB_CUDA(cudaMemcpyAsync(all.data(), d_recv, hb * ctx->nranks, cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_send);
+  cudaFree(d_recv);
+  for (int q = 0; q < ctx->nranks; ++q) {
+    void* mapped[kH];
+    for (int i = 0; i < kH; ++i) {
+      if (q == ctx->rank) {
+        mapped[i] = ptrs[i];
+        continue;
+      }
+      cudaError_t e = cudaIpcOpenMemHandle(&mapped[i], all[(size_t)q * kH + i], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        p2p_release(ctx);
+        P.unavailable = true;   // no peer mapping: the NCCL composite is used instead
+        return NKB_OK;
+      }
+      P.opened.push_back(mapped[i]);
+    }
+    P.peer_keys[0][q] = (const unsigned long long*)mapped[0];
+    P.peer_keys[1][q] = (const unsigned long long*)mapped[1];
+    P.peer_flags[q] = (unsigned long long*)mapped[2];
+    if (q == 0) {
+      P.root_rgba = (unsigned char*)mapped[3];
+      P.root_depth = (float*)mapped[4];
+    }
+  }
+  P.W = W;
+  P.H = H;
+  P.epoch = 0;
+  P.ready = true;
+  return NKB_OK;
+}
 
 static int ctx_check(nkb_ctx* ctx) {
   if (!ctx) return fail(NKB_EINVAL, "null context");
@@ -215,6 +307,7 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   if (!ctx) return NKB_OK;
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  p2p_release(ctx);
   if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
   cudaFree(ctx->elem_count);
   cudaFree(ctx->elem_offset);
@@ -601,7 +694,37 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
     NKB_TRY(launch_fused(fp, s));
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[1], s));
-  NKB_TRY(launch_zbuf_clear(ctx->zbuf, npx, s));
+  const bool p2p = composite && ctx->p2p.ready;
+  unsigned long long* zbuf = ctx->zbuf;
+  P2PParams pp;
+  unsigned long long ep = 0;
+  if (p2p) {
+    auto& P = ctx->p2p;
+    ep = ++P.epoch;
+    memset(&pp, 0, sizeof(pp));
+    pp.rank = ctx->rank;
+    pp.nranks = ctx->nranks;
+    pp.flags = P.flags;
+    for (int q = 0; q < ctx->nranks; ++q) {
+      pp.peer_flags[q] = P.peer_flags[q];
+      pp.peer_keys[q] = P.peer_keys[ep & 1][q];
+    }
+    pp.npx = npx;
+    pp.width = p->width;
+    pp.height = p->height;
+    pp.vmin = p->vmin;
+    pp.vmax = p->vmax;
+    pp.cmap = cm;
+    memcpy(pp.bg, p->background, 4);
+    pp.root_rgba = P.root_rgba;
+    pp.root_depth = P.root_depth;
+    pp.range_out = ctx->range_dev;
+    pp.err = P.err;
+    zbuf = P.keys[ep & 1];
+    // every peer has finished reading this key buffer (epoch ep-2) before it is cleared
+    if (ep > 2) NKB_TRY(launch_p2p_wait(pp, 1, ep - 2, s));
+  }
+  NKB_TRY(launch_zbuf_clear(zbuf, npx, s));
   RasterParams rp;
   rp.tri = ctx->tri;
   if (ordered) {          // one contiguous region; its count is the scan total
@@ -616,18 +739,24 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   memcpy(rp.view, p->view, sizeof(rp.view));
   rp.width = p->width;
   rp.height = p->height;
-  rp.zbuf = ctx->zbuf;
+  rp.zbuf = zbuf;
   NKB_TRY(launch_raster(rp, s));
-  NKB_TRY(launch_range_words(ctx->counters, ctx->zbuf + npx, s));
+  NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[2], s));
-  if (composite) {
+  if (p2p) {
+    // fused sort-last composite + resolve over NVLink peer memory
+    NKB_TRY(launch_p2p_signal(pp, 0, ep, nullptr, s));
+    NKB_TRY(launch_p2p_composite(pp, ep, s));
+    NKB_TRY(launch_p2p_signal(pp, 1, ep, ctx->counters, s));
+    if (ctx->rank == 0) NKB_TRY(launch_p2p_wait(pp, 1, ep, s));
+  } else if (composite) {
     NKB_NCCL(g_nccl.GroupStart());
     NKB_NCCL(g_nccl.Reduce(ctx->zbuf, ctx->zbuf, (size_t)npx + 2, ncclUint64, ncclMin, 0, ctx->comm, s));
     NKB_NCCL(g_nccl.AllReduce(ctx->counters, ctx->counters + 3, 1, ncclUint64, ncclSum, ctx->comm, s));
     NKB_NCCL(g_nccl.GroupEnd());
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[3], s));
-  if (!composite || ctx->rank == 0) {
+  if (!p2p && (!composite || ctx->rank == 0)) {
     ResolveParams rs;
     rs.zbuf = ctx->zbuf;
     rs.width = p->width;
@@ -651,7 +780,20 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   if (!ordered)
     NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 8, ctx->region_count,
                              sizeof(unsigned long long) * ctx->n_regions, cudaMemcpyDeviceToHost, s));
+  int p2p_err = 0;
+  unsigned long long tri_by_rank[kMaxRanks] = {};
+  if (p2p) {
+    NKB_CUDA(cudaMemcpyAsync(&p2p_err, ctx->p2p.err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NKB_CUDA(cudaMemcpyAsync(tri_by_rank, ctx->p2p.flags + 2 * kMaxRanks, sizeof(tri_by_rank),
+                             cudaMemcpyDeviceToHost, s));
+  }
   NKB_CUDA(cudaStreamSynchronize(s));
+  if (p2p) {
+    if (p2p_err) return fail(NKB_ENCCL, "P2P composite: timed out waiting for a peer rank");
+    unsigned long long tot = 0;
+    for (int q = 0; q < ctx->nranks; ++q) tot += tri_by_rank[q];
+    ctx->h_counters[3] = tot;   // meaningful on rank 0 (every rank reports to every rank)
+  }
   ctx->last_fast = !ordered;
   return NKB_OK;
 }
@@ -719,6 +861,10 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   else NKB_TRY(ensure_tri(ctx, ctx->tri_cap, p->emit_meta));
 
   const bool ordered = p->emit_meta && ctx->E > 0 && p->n_surfaces > 0;
+  if (composite && !ctx->p2p.unavailable) {
+    const char* mode = getenv("NKB_COMPOSITE");
+    if (!(mode && strcmp(mode, "nccl") == 0)) NKB_TRY(p2p_setup(ctx, p->width, p->height, s));
+  }
   NKB_TRY(run_step(ctx, p, fp, cm, s, composite, ordered));
   int reran = 0;
   int64_t ntri = (int64_t)ctx->h_counters[0];
@@ -842,6 +988,8 @@ int nkb_comm_init(nkb_ctx* ctx, const unsigned char id[128], int nranks, int ran
 
 int nkb_comm_destroy(nkb_ctx* ctx) {
   NKB_TRY(ctx_check(ctx));
+  cudaDeviceSynchronize();
+  p2p_release(ctx);
   if (ctx->comm && g_nccl.ok) g_nccl.CommDestroy(ctx->comm);
   ctx->comm = nullptr;
   ctx->rank = 0;

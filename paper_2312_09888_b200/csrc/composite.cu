@@ -1,0 +1,179 @@
+// Sort-last depth composite fused with the colormap resolve, over NVLink peer
+// memory (R16 of SURVEY.md §8a).
+//
+// Every rank rasterises its element partition into a packed-key buffer
+// (depth bits << 32 | scalar bits, + 2 colour-range words).  Instead of an
+// ncclReduce to rank 0 followed by a resolve on rank 0, each rank owns a band
+// of image rows and, in ONE kernel,
+//   - min-reduces that band straight out of every peer's key buffer (P2P
+//     loads through CUDA IPC mappings over NVLink/NVSwitch),
+//   - resolves the colormap (global range = min/max of all peers' range words),
+//   - stores RGBA8 + depth directly into rank 0's image (P2P stores).
+// Bytes crossing NVLink per rank: (N-1)/N of the key buffer in, (N-1)/N of
+// the RGBA+depth band out -- the same as a reduce-scatter + gather, with no
+// separate resolve pass and no host round trip.
+//
+// Ordering uses per-rank epoch flags in peer memory with system-scope
+// release / acquire; every spin has a globaltimer timeout so a lost peer
+// cannot hang the GPU (the host reports NKB_ENCCL instead).  Key buffers are
+// double-buffered by epoch parity; before a rank clears a buffer it waits
+// until every peer has finished reading it (epoch - 2).
+//
+// The result is identical to the NCCL path and to one GPU: min over packed
+// keys is associative and commutative (tests/test_gpu_multi.py).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "nkb_internal.h"
+
+namespace nkb {
+
+namespace {
+
+constexpr unsigned long long kTimeoutNs = 2000000000ULL;   // 2 s
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ double dec_ordered(unsigned long long u) {
+  unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
+  return __longlong_as_double((long long)b);
+}
+
+// same np.interp + floor(v + 0.5) rule as raster.cu resolve (sinks.py:201-209)
+__device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double t, int ch) {
+  if (t != t) return 0;
+  const int n = cm.n;
+  double v;
+  if (t >= cm.t[n - 1]) {
+    v = cm.rgb[n - 1][ch];
+  } else {
+    int j = 0;
+    for (int k = 1; k < n - 1; ++k)
+      if (t >= cm.t[k]) j = k;
+    if (t == cm.t[j]) {
+      v = cm.rgb[j][ch];
+    } else {
+      const double slope = __ddiv_rn(__dsub_rn(cm.rgb[j + 1][ch], cm.rgb[j][ch]),
+                                     __dsub_rn(cm.t[j + 1], cm.t[j]));
+      v = __dadd_rn(__dmul_rn(slope, __dsub_rn(t, cm.t[j])), cm.rgb[j][ch]);
+    }
+  }
+  return (unsigned char)floor(__dadd_rn(v, 0.5));
+}
+
+// wait until flags[first .. first+n) >= target (all peers); 0 = ok, 1 = timeout
+__device__ int wait_flags(const unsigned long long* flags, int first, int n, unsigned long long target,
+                          int* err) {
+  const unsigned long long t0 = gtimer();
+  for (int p = 0; p < n; ++p) {
+    while (ld_acquire_sys(flags + first + p) < target) {
+      if (gtimer() - t0 > kTimeoutNs) {
+        atomicExch(err, 1);
+        return 1;
+      }
+    }
+  }
+  return 0;
+}
+
+__global__ void signal_kernel(P2PParams p, int which, unsigned long long epoch, const unsigned long long* count) {
+  // which 0: "keys ready", 1: "done reading peers' keys" (+ this rank's triangle count)
+  const int q = threadIdx.x;
+  if (q < p.nranks) {
+    if (count) p.peer_flags[q][2 * kMaxRanks + p.rank] = *count;
+    __threadfence_system();
+    st_release_sys(p.peer_flags[q] + which * kMaxRanks + p.rank, epoch);
+  }
+}
+
+__global__ void wait_kernel(P2PParams p, int which, unsigned long long target) {
+  if (threadIdx.x == 0) wait_flags(p.flags, which * kMaxRanks, p.nranks, target, p.err);
+}
+
+__global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p, unsigned long long epoch) {
+  __shared__ int s_ok;
+  __shared__ double s_lo, s_hi;
+  if (threadIdx.x == 0) {
+    s_ok = !wait_flags(p.flags, 0, p.nranks, epoch, p.err);
+    // global colour range from every rank's range words
+    unsigned long long wmin = ~0ULL, wmax = ~0ULL;
+    for (int q = 0; q < p.nranks; ++q) {
+      const unsigned long long* z = p.peer_keys[q];
+      wmin = min(wmin, z[p.npx]);
+      wmax = min(wmax, z[p.npx + 1]);
+    }
+    double lo = p.vmin, hi = p.vmax;
+    if (!(lo == lo)) lo = (wmin == ~0ULL) ? 0.0 : dec_ordered(wmin);
+    if (!(hi == hi)) hi = (~wmax == 0ULL) ? 0.0 : dec_ordered(~wmax);
+    s_lo = lo;
+    s_hi = hi;
+    if (blockIdx.x == 0 && p.range_out) {
+      p.range_out[0] = lo;
+      p.range_out[1] = hi;
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const double lo = s_lo, hi = s_hi, span = __dsub_rn(hi, lo);
+  const long long r0 = (long long)p.height * p.rank / p.nranks, r1 = (long long)p.height * (p.rank + 1) / p.nranks;
+  const long long i0 = r0 * p.width, i1 = r1 * p.width;
+  for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < i1;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long key = ~0ULL;
+#pragma unroll 4
+    for (int q = 0; q < p.nranks; ++q) key = min(key, p.peer_keys[q][i]);
+    uchar4 o;
+    float dep;
+    if (key == ~0ULL) {
+      o = make_uchar4(p.bg[0], p.bg[1], p.bg[2], p.bg[3]);
+      dep = INFINITY;
+    } else {
+      const double s = (double)__uint_as_float((unsigned)(key & 0xffffffffULL));
+      dep = __uint_as_float((unsigned)(key >> 32));
+      double t = hi > lo ? __ddiv_rn(__dsub_rn(s, lo), span) : 0.0;
+      t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+      o = make_uchar4(cmap_channel(p.cmap, t, 0), cmap_channel(p.cmap, t, 1), cmap_channel(p.cmap, t, 2), 255);
+    }
+    reinterpret_cast<uchar4*>(p.root_rgba)[i] = o;
+    p.root_depth[i] = dep;
+  }
+}
+
+}  // namespace
+
+int launch_p2p_signal(const P2PParams& p, int which, unsigned long long epoch, const unsigned long long* count,
+                      cudaStream_t s) {
+  signal_kernel<<<1, 32, 0, s>>>(p, which, epoch, count);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_p2p_wait(const P2PParams& p, int which, unsigned long long target, cudaStream_t s) {
+  wait_kernel<<<1, 32, 0, s>>>(p, which, target);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_p2p_composite(const P2PParams& p, unsigned long long epoch, cudaStream_t s) {
+  const long long band = (long long)p.width * ((long long)p.height / p.nranks + 1);
+  long long blocks = (band + 255) / 256;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks < 1) blocks = 1;
+  p2p_composite_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, epoch);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+}  // namespace nkb

@@ -105,6 +105,28 @@ struct Colormap {
   double rgb[NKB_MAX_ANCHORS][3];
 };
 
+// ---- P2P sort-last composite (composite.cu) ----------------------------------
+constexpr int kMaxRanks = 8;
+struct P2PParams {
+  int rank, nranks;
+  unsigned long long* flags;                          // local [3*kMaxRanks]: ready | done | tri count
+  unsigned long long* peer_flags[kMaxRanks];          // every rank's flags (IPC-mapped)
+  const unsigned long long* peer_keys[kMaxRanks];     // every rank's key buffer of this epoch
+  long long npx;
+  int width, height;
+  double vmin, vmax;                                  // NaN => global data range
+  Colormap cmap;
+  unsigned char bg[4];
+  unsigned char* root_rgba;                           // rank 0's image (IPC-mapped)
+  float* root_depth;
+  double* range_out;                                  // local [2]
+  int* err;                                           // local: 1 = peer timeout
+};
+int launch_p2p_signal(const P2PParams& p, int which, unsigned long long epoch, const unsigned long long* count,
+                      cudaStream_t s);
+int launch_p2p_wait(const P2PParams& p, int which, unsigned long long target, cudaStream_t s);
+int launch_p2p_composite(const P2PParams& p, unsigned long long epoch, cudaStream_t s);
+
 struct ResolveParams {
   const unsigned long long* zbuf;
   int width, height;

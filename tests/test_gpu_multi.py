@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _image(rank, size, out_dir):
+def _image(rank, size, out_dir, steps=3):
     import torch.distributed as dist
 
     from paper_2312_09888_b200 import synth
@@ -43,7 +43,9 @@ def _image(rank, size, out_dir):
     da.initialize(Snapshot(0.0, 0, 0, (SemBlock(c.n_elements, c.x, c.y, c.z, fields=fields,
                                                 element_offset=e0, n_elements_global=E),)))
     params = {**c.params, "width": str(W), "height": str(H)}
-    res = InsituAnalysis(pipeline_from_params(params)).execute(da, depth=True)
+    an = InsituAnalysis(pipeline_from_params(params))
+    for _ in range(steps):            # several epochs: exercises the double-buffered key exchange
+        res = an.execute(da, depth=True)
     if rank == 0:
         np.savez(os.path.join(out_dir, f"g{size}.npz"), rgba=res.rgba, dep=res.depth,
                  n=res.report.n_triangles_global, rng=np.array(res.report.range))
@@ -51,10 +53,10 @@ def _image(rank, size, out_dir):
     comm.close()
 
 
-def _worker(rank, size, port, out_dir):
+def _worker(rank, size, port, out_dir, mode="p2p"):
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank), NKB_COMPOSITE=mode)
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
         _image(rank, size, out_dir)
@@ -68,14 +70,17 @@ def _ngpus():
     return device_count()
 
 
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
 @pytest.mark.parametrize("size", [2, 4])
-def test_nccl_composite_equals_single_gpu(tmp_path, size):
+def test_composite_equals_single_gpu(tmp_path, size, mode):
+    """P2P fused composite (default) and the NCCL reduce path both reproduce
+    the one-GPU image bit for bit."""
     if _ngpus() < size:
         pytest.skip(f"needs {size} GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
-    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
+    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), mode), nprocs=size, join=True)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / f"g{size}.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
