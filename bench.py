@@ -137,8 +137,17 @@ def _pipeline(case, width):
     return replace(p, composite=True)
 
 
-def _bytes_read_per_point(case) -> int:
-    return 8 * (3 + sum(v.shape[0] for v in case.fields.values()))
+def _bytes_read_per_point(case, cached: bool = False, plane: bool = True) -> int:
+    """Algorithmic HBM bytes the fused kernel reads per GLL point: every field
+    component once (f64), the coordinates unless the geometry cache replaces
+    them (still staged when a slice plane needs x,y,z), and the 9 cached
+    Jacobian-inverse entries (72 B) when the cache is used."""
+    b = 8 * sum(v.shape[0] for v in case.fields.values())
+    if not cached or plane:
+        b += 24
+    if cached:
+        b += 72
+    return b
 
 
 WORKLOADS = {
@@ -194,8 +203,13 @@ def run_ours(a):
     from dataclasses import replace
 
     an = InsituAnalysis(replace(pipe, timing=True))
+    geo_build_ms = 0.0
     for _ in range(a.warmup):
-        an.execute(da, fetch_image=False)
+        r = an.execute(da, fetch_image=False).report
+        geo_build_ms = max(geo_build_ms, r.ms_geometry)
+    cached = bool(r.geometry_cached)
+    plane = any(s.kind == "slice" for s in pipe.surfaces)
+    bpp = _bytes_read_per_point(case, cached, plane)
 
     def barrier():
         torch.cuda.synchronize()
@@ -240,7 +254,7 @@ def run_ours(a):
     # roofline of the dominant kernel (fused adaptor+grad+Q+MC pass)
     peaks, peak_kind = _peaks()
     fused = statistics.mean(fused_ms)
-    alg_bytes = npts * _bytes_read_per_point(case) + 48 * ntri
+    alg_bytes = npts * bpp + 48 * ntri
     achieved = alg_bytes / (fused / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{a.config}.json")
@@ -248,8 +262,21 @@ def run_ours(a):
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
 
+    # the same step without the geometry cache (x,y,z derivative pencils and
+    # the cofactor/reciprocal chain recomputed every step), for comparison
+    uncached = None
+    if cached:
+        ctx.set_geometry_cache(False)
+        for _ in range(2):
+            an.execute(da, fetch_image=False)
+        um = [an.execute(da, fetch_image=False).report.ms_fused for _ in range(max(3, min(a.steps, 10)))]
+        ctx.set_geometry_cache(True)
+        an.execute(da, fetch_image=False)
+        uncached = {"fused_ms": round(statistics.mean(um), 4),
+                    "bytes_per_point": _bytes_read_per_point(case, False, plane)}
+
     # ---- end-to-end through the reference-facing sink with host buffers ----
-    host_bytes = npts * _bytes_read_per_point(case)
+    host_bytes = npts * _bytes_read_per_point(case, False, True)
     e2e = None
     hcase = None
     if host_bytes <= a.e2e_max_gb * 1e9:
@@ -301,14 +328,17 @@ def run_ours(a):
             "gll_points_total": npts * world,
             "surfaces": case.params.get("iso", "") + (";slice " + case.params["slice"] if "slice" in case.params else ""),
             "color": case.params.get("field"), "image": f"{a.width}x{a.width}",
-            "l2": f"inputs {npts * _bytes_read_per_point(case) / 1e9:.2f} GB/GPU >> 126 MB L2 (no flush needed)",
+            "l2": f"inputs {npts * bpp / 1e9:.2f} GB/GPU >> 126 MB L2 (no flush needed)",
+            "geometry_cache": ("on: d(r,s,t)/d(x,y,z) cached per mesh (static mesh), "
+                               f"built once in {geo_build_ms:.3f} ms during warm-up") if cached else "off/not needed",
             "parallelism": f"element partition x{world}, sort-last composite (NCCL min-reduce)",
         },
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": "fused_kernel",
                      "kernel_ms": fused, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
-                     "bytes_per_point": _bytes_read_per_point(case), "triangles": ntri},
+                     "bytes_per_point": bpp, "triangles": ntri},
+        "fused_uncached": uncached,
         "stages_ms": dict(zip(("fused", "raster", "composite", "resolve"),
                               (round(statistics.mean(x), 4) for x in zip(*stages)))),
         "fused_ms_per_rank": per_rank_fused,

@@ -106,6 +106,8 @@ typedef struct {
     double  data_range[2];        /* colour-field min/max over this rank's points */
     float   ms_fused, ms_raster, ms_composite, ms_resolve;   /* when timing */
     int     reran;                /* 1 if the triangle buffer grew and the step re-ran */
+    int     geometry_cached;      /* 1 if the step used the geometry cache */
+    float   ms_geometry;          /* time spent (re)building the cache this step (when timing) */
 } nkb_report;
 
 typedef struct {
@@ -136,6 +138,15 @@ int nkb_gll(int order, double* nodes, double* dmat);
 int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order,
                  const double* x, const double* y, const double* z,
                  int64_t element_offset, int64_t n_elements_global);
+/* Geometry cache.  The first step that needs velocity gradients computes the
+ * Jacobian inverse d(r,s,t)/d(x,y,z) at every GLL node (72 B/point, the SEM
+ * "geometric factors" NekRS keeps in mesh->vgeo) and later steps reuse it;
+ * values are bit-identical to recomputing them.  Calling nkb_mesh_set again
+ * with the same pointers, sizes and offsets keeps the cache (static mesh);
+ * after editing coordinates in place (moving mesh) call nkb_mesh_modified.
+ * nkb_set_geometry_cache(ctx, 0) disables it (default on; env NKB_GEOM_CACHE=0). */
+int nkb_mesh_modified(nkb_ctx* ctx);
+int nkb_set_geometry_cache(nkb_ctx* ctx, int enable);
 /* register (or re-point) a device-resident point field, borrowed.
  * replaces: FieldArray(name, POINT, comps, values) (data_model.py:27-55) */
 int nkb_field_set(nkb_ctx* ctx, const char* name, int ncomp,

@@ -69,6 +69,8 @@ class NkbReport(C.Structure):
         ("ms_composite", C.c_float),
         ("ms_resolve", C.c_float),
         ("reran", C.c_int),
+        ("geometry_cached", C.c_int),
+        ("ms_geometry", C.c_float),
     ]
 
 
@@ -104,6 +106,8 @@ _SIGS = {
     "nkb_add_array": ([_vp, C.c_char_p, C.c_int, _vp, C.POINTER(C.c_int), _vp], C.c_int),
     "nkb_array_components": ([_vp, C.c_char_p, C.POINTER(C.c_int)], C.c_int),
     "nkb_set_velocity_name": ([_vp, C.c_char_p], C.c_int),
+    "nkb_mesh_modified": ([_vp], C.c_int),
+    "nkb_set_geometry_cache": ([_vp, C.c_int], C.c_int),
     "nkb_execute": ([_vp, C.POINTER(NkbPipeline), C.POINTER(NkbReport), _vp], C.c_int),
     "nkb_image_device": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
     "nkb_image_copy": ([_vp, _vp, _vp, _vp], C.c_int),

@@ -37,6 +37,10 @@ class UnstructuredGrid:
     n_cells: int
 
 
+def _read_only(a) -> bool:
+    return isinstance(a, np.ndarray) and not a.flags.writeable
+
+
 class SemDataAdaptor:
     """DataAdaptor over one SemBlock per rank (NekRS partition)."""
 
@@ -49,6 +53,7 @@ class SemDataAdaptor:
         self._block: SemBlock | None = None
         self._staging: dict[str, DeviceArray] = {}
         self._fields: dict[str, FieldArray] = {}
+        self._coords = None
         self.time = 0.0
         self.step = 0
         self.h2d_bytes = 0
@@ -65,11 +70,24 @@ class SemDataAdaptor:
         self.time, self.step = float(snapshot.time), int(snapshot.step)
         self.h2d_bytes = 0
         npts = b.point_count
-        x = self._dev("__x", b.x, npts)
-        y = self._dev("__y", b.y, npts)
-        z = self._dev("__z", b.z, npts)
+        # Static mesh (NekRS without a moving mesh): when the block carries the
+        # very same read-only host coordinate arrays as last step, they are
+        # already resident and the library keeps its geometry cache.  Any
+        # other host coordinates are re-uploaded and the cache is dropped.
+        coords = (b.x, b.y, b.z)
+        static = (self._coords is not None and all(a is p for a, p in zip(coords, self._coords))
+                  and all(_read_only(a) for a in coords) and "__x" in self._staging)
+        if static:
+            x, y, z = (self._staging[k] for k in ("__x", "__y", "__z"))
+        else:
+            x = self._dev("__x", b.x, npts)
+            y = self._dev("__y", b.y, npts)
+            z = self._dev("__z", b.z, npts)
         self.ctx.mesh_set(b.n_elements, x, y, z, order=b.order, element_offset=b.element_offset,
                           n_elements_global=b.n_elements_global)
+        if not static and not all(is_device_array(a) for a in coords):
+            self.ctx.mesh_modified()
+        self._coords = coords
         self.ctx.field_clear()
         self._fields = {}
         for f in b.fields:
@@ -177,6 +195,11 @@ class SemDataAdaptor:
         self.ctx.add_array(array_name, out)
         N.call("nkb_stream_sync", None)
         return FieldArray(array_name, POINT, nc, out)
+
+    def mesh_modified(self) -> None:
+        """The bound coordinates were edited in place (moving mesh): the
+        geometry cache is rebuilt on the next gradient step."""
+        self.ctx.mesh_modified()
 
     def release_data(self) -> None:
         self._block = None

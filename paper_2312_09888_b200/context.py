@@ -25,6 +25,8 @@ class Report:
     ms_composite: float
     ms_resolve: float
     reran: bool
+    geometry_cached: bool = False
+    ms_geometry: float = 0.0
 
     @classmethod
     def from_native(cls, r: N.NkbReport) -> "Report":
@@ -33,7 +35,7 @@ class Report:
             (float(r.range[0]), float(r.range[1])),
             (float(r.data_range[0]), float(r.data_range[1])),
             float(r.ms_fused), float(r.ms_raster), float(r.ms_composite), float(r.ms_resolve),
-            bool(r.reran),
+            bool(r.reran), bool(r.geometry_cached), float(r.ms_geometry),
         )
 
 
@@ -77,6 +79,13 @@ class Context:
                  n_elements_global: int = 0) -> None:
         N.call("nkb_mesh_set", self.handle, int(n_elements), int(order), device_ptr(x), device_ptr(y),
                device_ptr(z), int(element_offset), int(n_elements_global))
+
+    def mesh_modified(self) -> None:
+        """Coordinates were edited in place (moving mesh): drop the geometry cache."""
+        N.call("nkb_mesh_modified", self.handle)
+
+    def set_geometry_cache(self, enable: bool) -> None:
+        N.call("nkb_set_geometry_cache", self.handle, int(bool(enable)))
 
     def field_set(self, name: str, base, ncomp: int = 1, comp_stride: int = 0) -> None:
         N.call("nkb_field_set", self.handle, name.encode(), int(ncomp), device_ptr(base), int(comp_stride))

@@ -147,7 +147,13 @@ struct nkb_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   cudaEvent_t ev[6] = {};
-  long long* prof = nullptr;                 // debug phase profile (NKB_PROFILE_PHASES=1)
+  // geometry cache: 9 SoA arrays of d(r,s,t)/d(x,y,z) (fused.cu geometry_kernel)
+  bool geo_enabled = true;
+  bool geo_valid = false;
+  double* geo = nullptr;
+  int64_t geo_cap = 0;                       // points
+  bool geo_used = false;                     // last step used it
+  bool geo_built = false;                    // last step (re)built it
   // P2P composite state (composite.cu)
   struct {
     bool ready = false, unavailable = false;
@@ -295,10 +301,7 @@ int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
   NKB_CUDA(cudaMallocHost(&c->h_counters, (8 + kMaxRegions) * sizeof(unsigned long long)));
   NKB_CUDA(cudaMalloc(&c->region_count, kMaxRegions * sizeof(unsigned long long)));
   for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
-  if (getenv("NKB_PROFILE_PHASES")) {
-    NKB_CUDA(cudaMalloc(&c->prof, kMaxRegions * 16 * sizeof(long long)));
-    NKB_CUDA(cudaMemset(c->prof, 0, kMaxRegions * 16 * sizeof(long long)));
-  }
+  if (const char* g = getenv("NKB_GEOM_CACHE")) c->geo_enabled = strcmp(g, "0") != 0;
   *out = c;
   return NKB_OK;
 }
@@ -321,6 +324,7 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->rgba);
   cudaFree(ctx->depth);
   cudaFree(ctx->range_dev);
+  cudaFree(ctx->geo);
   cudaFree(ctx->s_ptrs);
   cudaFree(ctx->s_col0);
   cudaFree(ctx->s_minmax);
@@ -342,6 +346,8 @@ int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order, const double* x, c
   if (n_elements < 0) return fail(NKB_EINVAL, "negative element count");
   if (n_elements > 0 && (!x || !y || !z)) return fail(NKB_EINVAL, "null coordinate pointer");
   if (n_elements > (int64_t)0x7fffffff) return fail(NKB_EINVAL, "too many elements for one rank");
+  const bool same = ctx->E == n_elements && ctx->N == order && ctx->x == x && ctx->y == y && ctx->z == z;
+  if (!same) ctx->geo_valid = false;       // a different mesh: rebuild the geometry cache on demand
   ctx->E = n_elements;
   ctx->N = order;
   ctx->x = x;
@@ -382,6 +388,53 @@ int nkb_field_set(nkb_ctx* ctx, const char* name, int ncomp, const double* base,
 int nkb_field_clear(nkb_ctx* ctx) {
   NKB_TRY(ctx_check(ctx));
   ctx->fields.clear();
+  return NKB_OK;
+}
+
+int nkb_mesh_modified(nkb_ctx* ctx) {
+  NKB_TRY(ctx_check(ctx));
+  ctx->geo_valid = false;
+  return NKB_OK;
+}
+
+int nkb_set_geometry_cache(nkb_ctx* ctx, int enable) {
+  NKB_TRY(ctx_check(ctx));
+  ctx->geo_enabled = enable != 0;
+  if (!ctx->geo_enabled) {
+    cudaFree(ctx->geo);                    // give the 72 B/point back
+    ctx->geo = nullptr;
+    ctx->geo_cap = 0;
+    ctx->geo_valid = false;
+  }
+  return NKB_OK;
+}
+
+// Attach the geometry cache to a gradient step, building it first when the
+// mesh changed.  On allocation failure the step runs uncached (the other
+// GPU kernel variant -- same results), never on the CPU.
+static int geo_attach(nkb_ctx* ctx, FusedParams& fp, cudaStream_t s) {
+  fp.geo = nullptr;
+  if (!fp.need_grad || !ctx->geo_enabled || ctx->E <= 0) return NKB_OK;
+  const int64_t npts = ctx->E * kNN;
+  if (ctx->geo_cap < npts) {
+    cudaFree(ctx->geo);
+    ctx->geo = nullptr;
+    ctx->geo_cap = 0;
+    ctx->geo_valid = false;
+    if (cudaMalloc(&ctx->geo, (size_t)npts * 9 * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->geo = nullptr;
+      return NKB_OK;
+    }
+    ctx->geo_cap = npts;
+  }
+  if (!ctx->geo_valid) {
+    NKB_TRY(launch_geometry(ctx->x, ctx->y, ctx->z, ctx->E, ctx->geo, s));
+    ctx->geo_valid = true;
+    ctx->geo_built = true;
+  }
+  fp.geo = ctx->geo;
+  ctx->geo_used = true;
   return NKB_OK;
 }
 
@@ -511,6 +564,7 @@ int nkb_add_array(nkb_ctx* ctx, const char* name, int association, double* out, 
       fp.need_wmag = 1;
     }
     NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
+    NKB_TRY(geo_attach(ctx, fp, s));
     NKB_TRY(launch_fused(fp, s));
     return NKB_OK;
   }
@@ -530,7 +584,6 @@ static int fused_params_base(nkb_ctx* ctx, FusedParams& fp) {
   fp.z = ctx->z;
   fp.mode = FUSED_FAST;
   fp.counters = ctx->counters;
-  fp.prof = ctx->prof;
   fp.color_src = -1;
   return NKB_OK;
 }
@@ -865,6 +918,9 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     const char* mode = getenv("NKB_COMPOSITE");
     if (!(mode && strcmp(mode, "nccl") == 0)) NKB_TRY(p2p_setup(ctx, p->width, p->height, s));
   }
+  ctx->geo_used = ctx->geo_built = false;
+  if (p->timing) NKB_CUDA(cudaEventRecord(ctx->ev[5], s));
+  NKB_TRY(geo_attach(ctx, fp, s));
   NKB_TRY(run_step(ctx, p, fp, cm, s, composite, ordered));
   int reran = 0;
   int64_t ntri = (int64_t)ctx->h_counters[0];
@@ -889,7 +945,9 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     out->data_range[0] = ctx->h_counters[1] == ~0ULL ? NAN : dec_ordered_h(ctx->h_counters[1]);
     out->data_range[1] = ctx->h_counters[2] == 0ULL ? NAN : dec_ordered_h(ctx->h_counters[2]);
     out->reran = reran;
+    out->geometry_cached = ctx->geo_used ? 1 : 0;
     if (p->timing) {
+      if (ctx->geo_built) cudaEventElapsedTime(&out->ms_geometry, ctx->ev[5], ctx->ev[0]);
       cudaEventElapsedTime(&out->ms_fused, ctx->ev[0], ctx->ev[1]);
       cudaEventElapsedTime(&out->ms_raster, ctx->ev[1], ctx->ev[2]);
       cudaEventElapsedTime(&out->ms_composite, ctx->ev[2], ctx->ev[3]);
@@ -946,15 +1004,6 @@ int nkb_triangles_device(nkb_ctx* ctx, const float** tri, const uint64_t** meta,
   if (tri) *tri = reinterpret_cast<const float*>(ctx->tri_export);
   if (meta) *meta = ctx->meta_alloc ? reinterpret_cast<const uint64_t*>(ctx->meta_export) : nullptr;
   if (n) *n = cnt;
-  return NKB_OK;
-}
-
-// debug: phase cycle counters of the last fused launch ([grid][2][6]); returns grid
-int nkb_debug_phase_profile(nkb_ctx* ctx, long long* out, int cap) {
-  NKB_TRY(ctx_check(ctx));
-  if (!ctx->prof) return fail(NKB_ESTATE, "set NKB_PROFILE_PHASES=1 before nkb_ctx_create");
-  const int n = std::min(ctx->n_regions, cap);
-  NKB_CUDA(cudaMemcpy(out, ctx->prof, sizeof(long long) * 16 * n, cudaMemcpyDeviceToHost));
   return NKB_OK;
 }
 

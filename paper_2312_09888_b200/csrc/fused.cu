@@ -106,6 +106,30 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// mbarrier + bulk (TMA) copy helpers: one elected thread moves a contiguous block
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, unsigned bytes, unsigned long long* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(gsrc), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(b), "r"(parity) : "memory");
+}
 // barrier among the 4 MC warps only (id 1; id 0 is __syncthreads)
 __device__ __forceinline__ void mc_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kMcThreads) : "memory"); }
 
@@ -118,9 +142,87 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
   return __fma_rn(n[2], z, __fma_rn(n[1], y, __dmul_rn(n[0], x)));
 }
 
-__device__ __forceinline__ bool src_is_grad(int s) { return s == SRC_Q || s == SRC_WMAG; }
 
 constexpr int kMaxTriPerElem = kNC * NKB_MC_MAX_TRI * NKB_MAX_SURFACES;   // 6860
+
+// even-odd 8-point derivatives of three staged fields along one pencil
+// (oracle deriv8): e_m = v_m + v_{7-m}, o_m = v_m - v_{7-m},
+// out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 DFMAs
+// I0/NI: compute only rows i in [I0, I0+NI) (and their mirrors 7-i), so two
+// threads can share one pencil (the geometry-cached variant)
+template <int I0 = 0, int NI = 4>
+__device__ __forceinline__ void pencil3(const double* s0, const double* s1, const double* s2, double* d0,
+                                        double* d1, double* d2, const int* off) {
+  double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const double a0 = s0[off[m]], b0 = s0[off[kNP - 1 - m]];
+    const double a1 = s1[off[m]], b1 = s1[off[kNP - 1 - m]];
+    const double a2 = s2[off[m]], b2 = s2[off[kNP - 1 - m]];
+    e0[m] = __dadd_rn(a0, b0);
+    o0[m] = __dsub_rn(a0, b0);
+    e1[m] = __dadd_rn(a1, b1);
+    o1[m] = __dsub_rn(a1, b1);
+    e2[m] = __dadd_rn(a2, b2);
+    o2[m] = __dsub_rn(a2, b2);
+  }
+#pragma unroll
+  for (int i = I0; i < I0 + NI; ++i) {
+    const double ce = c_Ae[i][0], co = c_Ao[i][0];
+    double E0 = __dmul_rn(ce, e0[0]), E1 = __dmul_rn(ce, e1[0]), E2 = __dmul_rn(ce, e2[0]);
+    double O0 = __dmul_rn(co, o0[0]), O1 = __dmul_rn(co, o1[0]), O2 = __dmul_rn(co, o2[0]);
+#pragma unroll
+    for (int m = 1; m < 4; ++m) {
+      const double ae = c_Ae[i][m], ao = c_Ao[i][m];
+      E0 = __fma_rn(ae, e0[m], E0);
+      E1 = __fma_rn(ae, e1[m], E1);
+      E2 = __fma_rn(ae, e2[m], E2);
+      O0 = __fma_rn(ao, o0[m], O0);
+      O1 = __fma_rn(ao, o1[m], O1);
+      O2 = __fma_rn(ao, o2[m], O2);
+    }
+    d0[off[i]] = __dadd_rn(E0, O0);
+    d1[off[i]] = __dadd_rn(E1, O1);
+    d2[off[i]] = __dadd_rn(E2, O2);
+    d0[off[kNP - 1 - i]] = __dsub_rn(O0, E0);
+    d1[off[kNP - 1 - i]] = __dsub_rn(O1, E1);
+    d2[off[kNP - 1 - i]] = __dsub_rn(O2, E2);
+  }
+}
+
+__device__ __forceinline__ void pencil_offsets(int dir, int pa, int pb, int* off) {
+  if (dir == 0) {
+#pragma unroll
+    for (int m = 0; m < kNP; ++m) off[m] = sw(m, pa, pb);
+  } else if (dir == 1) {
+#pragma unroll
+    for (int m = 0; m < kNP; ++m) off[m] = sw(pa, m, pb);
+  } else {
+#pragma unroll
+    for (int m = 0; m < kNP; ++m) off[m] = sw(pa, pb, m);
+  }
+}
+
+// Jacobian inverse d(r,s,t)/d(x,y,z) from the 9 reference derivatives
+// G = (xr,xs,xt, yr,ys,yt, zr,zs,zt): cofactors, det, 1/det (oracle order)
+__device__ __forceinline__ void jinv(const double* G, double* J) {
+  const double xr = G[0], xs = G[1], xt = G[2];
+  const double yr = G[3], ys = G[4], yt = G[5];
+  const double zr = G[6], zs = G[7], zt = G[8];
+  J[0] = __fma_rn(ys, zt, -__dmul_rn(yt, zs));
+  J[1] = __fma_rn(xt, zs, -__dmul_rn(xs, zt));
+  J[2] = __fma_rn(xs, yt, -__dmul_rn(xt, ys));
+  J[3] = __fma_rn(yt, zr, -__dmul_rn(yr, zt));
+  J[4] = __fma_rn(xr, zt, -__dmul_rn(xt, zr));
+  J[5] = __fma_rn(xt, yr, -__dmul_rn(xr, yt));
+  J[6] = __fma_rn(yr, zs, -__dmul_rn(ys, zr));
+  J[7] = __fma_rn(xs, zr, -__dmul_rn(xr, zs));
+  J[8] = __fma_rn(xr, ys, -__dmul_rn(xs, yr));
+  const double det = __fma_rn(zr, J[2], __fma_rn(yr, J[1], __dmul_rn(xr, J[0])));
+  const double rdet = __drcp_rn(det);           // == 1.0/det, correctly rounded
+#pragma unroll
+  for (int c = 0; c < 9; ++c) J[c] = __dmul_rn(J[c], rdet);
+}
 
 struct McScratch {
   unsigned cases[2][kNC];       // by element parity: byte s = case of surface s
@@ -144,11 +246,23 @@ __device__ __forceinline__ unsigned case_of(unsigned long long w, int s) {
 }  // namespace
 
 // mode: FUSED_FAST / FUSED_COUNT / FUSED_ORDERED (nkb_internal.h)
-__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nin, int slot_sc) {
+// kCached: the Jacobian inverse comes from the per-mesh geometry cache
+// (p.geo: per element 9 arrays of 512 doubles, 36 KB contiguous) instead of
+// x,y,z derivative pencils.  One thread moves element it+1's block into S_geo
+// with a single bulk (TMA) copy as soon as the node phase of element it has
+// consumed it; the node phase of it+1 waits on the mbarrier.  The 384 pencil
+// threads split the u,v,w pencils in two halves of output rows.
+// slot_xyz < 0: x,y,z are not staged (no slice plane; emission reads them via L2).
+template <bool kCached>
+__global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nin, int slot_sc,
+                                                            int slot_vel, int slot_xyz) {
+  constexpr int kD = kCached ? 9 : kNumD;              // derivative arrays held
   extern __shared__ __align__(16) double smem[];
   double* S_ring = smem;                               // kRing * nin * 512
-  double* S_d = S_ring + kRing * nin * kArr;           // 18 * 512 derivatives
-  double* S_q = S_d + kNumD * kArr;                    // 2 x (Q, |w|) * 512, by element parity
+  double* S_d = S_ring + kRing * nin * kArr;           // kD * 512 derivatives
+  double* S_dv = S_d + (kD - 9) * kArr;                // u,v,w derivatives (9 arrays)
+  double* S_geo = S_d + kD * kArr;                     // kCached: 9 * 512 d(r,s,t)/d(x,y,z), node order
+  double* S_q = S_geo + (kCached ? 9 : 0) * kArr;      // 2 x (Q, |w|) * 512, by element parity
   unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 4 * kArr);   // 512 case bits
   __shared__ McScratch mc;
   __shared__ double s_mn[kThreads / 32], s_mx[kThreads / 32];
@@ -236,10 +350,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     mc_bar();
     if (p.mode == FUSED_COUNT || total == 0) return;
     const unsigned long long base = mc.base;
-    const double* Sx = S_in;
-    const double* Sy = S_in + kArr;
-    const double* Sz = S_in + 2 * kArr;
-    const double* Su = S_in + 3 * kArr;
+    // slot_xyz < 0 (no slice plane): coordinates are not staged; the few
+    // active-cell corners are read through L2 from the global SoA arrays
+    const bool xyz_staged = slot_xyz >= 0;
+    const double* Sx = xyz_staged ? S_in + slot_xyz * kArr : p.x + e * (long long)kNN;
+    const double* Sy = xyz_staged ? S_in + (slot_xyz + 1) * kArr : p.y + e * (long long)kNN;
+    const double* Sz = xyz_staged ? S_in + (slot_xyz + 2) * kArr : p.z + e * (long long)kNN;
+    const double* Su = S_in + slot_vel * kArr;
     auto value_at = [&](int src, int s, int q) -> double {
       if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
       if (src == SRC_Q) return Sq[q];
@@ -273,14 +390,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       for (int r = 0; r < 3; ++r) {
         const int ed = mc.t_tri[cs][3 * k + r];
         const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
-        const int qa = sw(ca + voff_i(va), cb + voff_j(va), ck + voff_k(va));
-        const int qb = sw(ca + voff_i(vb), cb + voff_j(vb), ck + voff_k(vb));
+        const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
+        const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
+        const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
         const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
         const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
         const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
-        vtx[r].x = __double2float_rn(__fma_rn(tv, __dsub_rn(Sx[qb], Sx[qa]), Sx[qa]));
-        vtx[r].y = __double2float_rn(__fma_rn(tv, __dsub_rn(Sy[qb], Sy[qa]), Sy[qa]));
-        vtx[r].z = __double2float_rn(__fma_rn(tv, __dsub_rn(Sz[qb], Sz[qa]), Sz[qa]));
+        const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
+        const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
+        const double xa = Sx[pa], ya = Sy[pa], za = Sz[pa];
+        const double xb = Sx[pb], yb = Sy[pb], zb = Sz[pb];
+        vtx[r].x = __double2float_rn(__fma_rn(tv, __dsub_rn(xb, xa), xa));
+        vtx[r].y = __double2float_rn(__fma_rn(tv, __dsub_rn(yb, ya), ya));
+        vtx[r].z = __double2float_rn(__fma_rn(tv, __dsub_rn(zb, za), za));
         vtx[r].w = __double2float_rn(__fma_rn(tv, __dsub_rn(clb, cla), cla));
       }
       float4* dst = p.tri + 3 * out;
@@ -297,6 +419,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kThreads) (&mc.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
   if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
   if (is_mc && n_it > 0) prefetch(blockIdx.x, 0);
+  __shared__ unsigned long long s_geo_bar;
+  constexpr unsigned kGeoBytes = 9u * kNN * sizeof(double);
+  if (kCached && tid == 0) {
+    mbar_init(&s_geo_bar, 1);
+    if (n_it > 0) bulk_load(S_geo, p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes, &s_geo_bar);
+  }
   cp_async_commit();
   for (long long it = 0; it <= n_it; ++it) {
     const long long e = blockIdx.x + it * G;
@@ -314,69 +442,26 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
     } else if (it < n_it && p.need_grad) {
       // ---- pencils: thread = (group, dir, pencil); 3 fields share offsets ----
-      const int g = tid / 192;                      // 0: x,y,z   1: u,v,w  (warp-uniform)
+      const int g = tid / 192;                      // warp-uniform
       const int dir = (tid % 192) >> 6;             // warp-uniform
-      const int pa = tid & 7, pb = (tid >> 3) & 7;
       int off[kNP];
-      if (dir == 0) {
-#pragma unroll
-        for (int m = 0; m < kNP; ++m) off[m] = sw(m, pa, pb);
-      } else if (dir == 1) {
-#pragma unroll
-        for (int m = 0; m < kNP; ++m) off[m] = sw(pa, m, pb);
+      pencil_offsets(dir, tid & 7, (tid >> 3) & 7, off);
+      if (kCached) {
+        // u,v,w only; g selects output rows {0,1,6,7} or {2,3,4,5}
+        const double* su = S_in + slot_vel * kArr;
+        double* d0 = S_dv + dir * kArr;
+        if (g == 0) pencil3<0, 2>(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
+        else pencil3<2, 2>(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
       } else {
-#pragma unroll
-        for (int m = 0; m < kNP; ++m) off[m] = sw(pa, pb, m);
-      }
-      const double* s0 = S_in + (3 * g + 0) * kArr;   // staged slot == field index
-      const double* s1 = S_in + (3 * g + 1) * kArr;
-      const double* s2 = S_in + (3 * g + 2) * kArr;
-      double* d0 = S_d + (3 * (3 * g + 0) + dir) * kArr;
-      double* d1 = S_d + (3 * (3 * g + 1) + dir) * kArr;
-      double* d2 = S_d + (3 * (3 * g + 2) + dir) * kArr;
-      double v0[kNP], v1[kNP], v2[kNP];
-#pragma unroll
-      for (int m = 0; m < kNP; ++m) {
-        v0[m] = s0[off[m]];
-        v1[m] = s1[off[m]];
-        v2[m] = s2[off[m]];
-      }
-      // even-odd form (oracle deriv8): e_m = v_m + v_{7-m}, o_m = v_m - v_{7-m},
-      // out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 fields
-      double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        e0[m] = __dadd_rn(v0[m], v0[kNP - 1 - m]);
-        o0[m] = __dsub_rn(v0[m], v0[kNP - 1 - m]);
-        e1[m] = __dadd_rn(v1[m], v1[kNP - 1 - m]);
-        o1[m] = __dsub_rn(v1[m], v1[kNP - 1 - m]);
-        e2[m] = __dadd_rn(v2[m], v2[kNP - 1 - m]);
-        o2[m] = __dsub_rn(v2[m], v2[kNP - 1 - m]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double ce = c_Ae[i][0], co = c_Ao[i][0];
-        double E0 = __dmul_rn(ce, e0[0]), E1 = __dmul_rn(ce, e1[0]), E2 = __dmul_rn(ce, e2[0]);
-        double O0 = __dmul_rn(co, o0[0]), O1 = __dmul_rn(co, o1[0]), O2 = __dmul_rn(co, o2[0]);
-#pragma unroll
-        for (int m = 1; m < 4; ++m) {
-          const double ae = c_Ae[i][m], ao = c_Ao[i][m];
-          E0 = __fma_rn(ae, e0[m], E0);
-          E1 = __fma_rn(ae, e1[m], E1);
-          E2 = __fma_rn(ae, e2[m], E2);
-          O0 = __fma_rn(ao, o0[m], O0);
-          O1 = __fma_rn(ao, o1[m], O1);
-          O2 = __fma_rn(ao, o2[m], O2);
-        }
-        d0[off[i]] = __dadd_rn(E0, O0);
-        d1[off[i]] = __dadd_rn(E1, O1);
-        d2[off[i]] = __dadd_rn(E2, O2);
-        d0[off[kNP - 1 - i]] = __dsub_rn(O0, E0);
-        d1[off[kNP - 1 - i]] = __dsub_rn(O1, E1);
-        d2[off[kNP - 1 - i]] = __dsub_rn(O2, E2);
+        // g = 0: x,y,z   1: u,v,w
+        const int sf = (g == 0) ? slot_xyz : slot_vel;
+        pencil3(S_in + (sf + 0) * kArr, S_in + (sf + 1) * kArr, S_in + (sf + 2) * kArr,
+                S_d + (3 * (3 * g + 0) + dir) * kArr, S_d + (3 * (3 * g + 1) + dir) * kArr,
+                S_d + (3 * (3 * g + 2) + dir) * kArr, off);
       }
     }
     if (it == n_it) break;
+    if (kCached) mbar_wait(&s_geo_bar, (unsigned)(it & 1));   // geometry of element `it` landed
     __syncthreads();                                   // derivatives of element `it` ready
 
     // ---- node phase: one node per thread ----
@@ -388,29 +473,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       unsigned char* bits_out = S_bits;
       double vq = 0.0, vw = 0.0, vu = 0.0;
       if (p.need_grad) {
-        double G9[9];
-#pragma unroll
-        for (int c = 0; c < 9; ++c) G9[c] = S_d[c * kArr + q];
-        const double xr = G9[0], xs = G9[1], xt = G9[2];
-        const double yr = G9[3], ys = G9[4], yt = G9[5];
-        const double zr = G9[6], zs = G9[7], zt = G9[8];
         double J[9];
-        J[0] = __fma_rn(ys, zt, -__dmul_rn(yt, zs));
-        J[1] = __fma_rn(xt, zs, -__dmul_rn(xs, zt));
-        J[2] = __fma_rn(xs, yt, -__dmul_rn(xt, ys));
-        J[3] = __fma_rn(yt, zr, -__dmul_rn(yr, zt));
-        J[4] = __fma_rn(xr, zt, -__dmul_rn(xt, zr));
-        J[5] = __fma_rn(xt, yr, -__dmul_rn(xr, yt));
-        J[6] = __fma_rn(yr, zs, -__dmul_rn(ys, zr));
-        J[7] = __fma_rn(xs, zr, -__dmul_rn(xr, zs));
-        J[8] = __fma_rn(xr, ys, -__dmul_rn(xs, yr));
-        const double det = __fma_rn(zr, J[2], __fma_rn(yr, J[1], __dmul_rn(xr, J[0])));
-        const double rdet = __drcp_rn(det);           // == 1.0/det, correctly rounded
+        if (kCached) {
 #pragma unroll
-        for (int c = 0; c < 9; ++c) J[c] = __dmul_rn(J[c], rdet);
+          for (int c = 0; c < 9; ++c) J[c] = S_geo[c * kArr + n];
+        } else {
+          double G9[9];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) G9[c] = S_d[c * kArr + q];
+          jinv(G9, J);
+        }
         double U[9];
 #pragma unroll
-        for (int c = 0; c < 9; ++c) U[c] = S_d[(9 + c) * kArr + q];
+        for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
         double A[9];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
@@ -437,12 +512,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
           p.vort_out[3 * (g0 + n) + 2] = om2;
         }
       }
-      if (p.need_umag) vu = mag3(S_in[3 * kArr + q], S_in[4 * kArr + q], S_in[5 * kArr + q]);
+      if (p.need_umag) vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
       unsigned bits = 0;
       for (int s = 0; s < p.n_surf; ++s) {
         const int src = p.surf_src[s];
         double val;
-        if (src >= SRC_PLANE) val = plane_dist(p.surf_n[s], S_in[q], S_in[kArr + q], S_in[2 * kArr + q]);
+        if (src >= SRC_PLANE)
+          val = plane_dist(p.surf_n[s], S_in[slot_xyz * kArr + q], S_in[(slot_xyz + 1) * kArr + q],
+                           S_in[(slot_xyz + 2) * kArr + q]);
         else if (src == SRC_Q) val = vq;
         else if (src == SRC_WMAG) val = vw;
         else if (src == SRC_UMAG) val = vu;
@@ -460,8 +537,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         cmax = fmax(cmax, c);
       }
     }
-    if (p.n_surf == 0) continue;
+    if (p.n_surf == 0 && !kCached) continue;
     __syncthreads();                                   // case bits of element `it` ready
+    if (kCached && tid == 0 && it + 1 < n_it)          // S_geo consumed: fetch element it+1
+      bulk_load(S_geo, p.geo + (e + G) * 9 * kNN, kGeoBytes, &s_geo_bar);
+    if (p.n_surf == 0) continue;
 
     // ---- classify: one sub-hex per thread (all warps) ----
     if (tid < kNC) {
@@ -596,34 +676,93 @@ int launch_compact(const float4* tri, const unsigned long long* meta, const unsi
   return NKB_OK;
 }
 
+// ---- per-mesh geometry cache: d(r,s,t)/d(x,y,z) at every GLL node ----
+// Same pencil3/jinv code as the uncached fused kernel, so the cached values
+// are bit-identical to what the fused kernel would recompute each step.
+// Layout: per element 9 arrays of 512 doubles (component c of node n of
+// element e at geo[(9e + c) * 512 + n]) so one element is one 36 KB block.
+__global__ void __launch_bounds__(kNN) geometry_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                                       const double* __restrict__ z, long long E, double* geo) {
+  __shared__ double S[12 * kArr];                  // x,y,z + 9 derivatives (48 KB)
+  const int tid = threadIdx.x;
+  const int q = sw_node(tid);
+  for (long long e = blockIdx.x; e < E; e += gridDim.x) {
+    const long long g = e * (long long)kNN + tid;
+    S[q] = x[g];
+    S[kArr + q] = y[g];
+    S[2 * kArr + q] = z[g];
+    __syncthreads();
+    if (tid < 192) {
+      const int dir = tid >> 6;
+      int off[kNP];
+      pencil_offsets(dir, tid & 7, (tid >> 3) & 7, off);
+      double* D = S + 3 * kArr;
+      pencil3(S, S + kArr, S + 2 * kArr, D + dir * kArr, D + (3 + dir) * kArr, D + (6 + dir) * kArr, off);
+    }
+    __syncthreads();
+    double G9[9], J[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) G9[c] = S[(3 + c) * kArr + q];
+    jinv(G9, J);
+#pragma unroll
+    for (int c = 0; c < 9; ++c) geo[(e * 9 + c) * kNN + tid] = J[c];
+    __syncthreads();
+  }
+}
+
+int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* geo, cudaStream_t s) {
+  if (E <= 0) return NKB_OK;
+  const long long grid = E < 148LL * 64 ? E : 148LL * 64;
+  geometry_kernel<<<(unsigned)grid, kNN, 0, s>>>(x, y, z, (long long)E, geo);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
 static size_t fused_smem_bytes(int nin) {
   return (size_t)(kRing * nin + kNumD + 4) * kArr * sizeof(double) + 2 * kNN;
 }
 
 int launch_fused(const FusedParams& p, cudaStream_t s) {
   if (p.n_elements <= 0) return NKB_OK;
-  const int nin = 3 + (p.need_vel ? 3 : 0) + p.n_scalars;
-  const int slot_sc = 3 + (p.need_vel ? 3 : 0);
+  const bool cached = p.geo != nullptr && p.need_grad;
+  bool has_plane = false;
+  for (int i = 0; i < p.n_surf; ++i) has_plane |= p.surf_src[i] >= SRC_PLANE;
+  // staged inputs in slot order: [x, y, z], [u, v, w], [scalars]; with the
+  // geometry cache x,y,z are staged only when a slice plane needs them
+  const bool stage_xyz = !cached || has_plane;
+  FusedParams q = p;
+  int k = 0;
+  int slot_xyz = -1, slot_vel = 0;
+  if (stage_xyz) {
+    slot_xyz = k;
+    q.in_ptr[k++] = p.x;
+    q.in_ptr[k++] = p.y;
+    q.in_ptr[k++] = p.z;
+  }
+  if (p.need_vel) {
+    slot_vel = k;
+    for (int c = 0; c < 3; ++c) q.in_ptr[k++] = p.vel[c];
+  }
+  const int slot_sc = k;
+  for (int c = 0; c < p.n_scalars; ++c) q.in_ptr[k++] = p.scalar[c];
+  const int nin = k;
   const size_t shm = fused_smem_bytes(nin);
   static bool attr_set = false;
   if (!attr_set) {
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)fused_smem_bytes(kMaxIn)));
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)fused_smem_bytes(kMaxIn)));
     int dev = 0;
     NKB_CUDA(cudaGetDevice(&dev));
     NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     attr_set = true;
   }
-  FusedParams q = p;   // staged inputs in slot order: x, y, z, [u, v, w], [scalars]
-  int k = 0;
-  q.in_ptr[k++] = p.x;
-  q.in_ptr[k++] = p.y;
-  q.in_ptr[k++] = p.z;
-  if (p.need_vel)
-    for (int c = 0; c < 3; ++c) q.in_ptr[k++] = p.vel[c];
-  for (int c = 0; c < p.n_scalars; ++c) q.in_ptr[k++] = p.scalar[c];
   const int grid = fused_grid(p.n_elements);
-  fused_kernel<<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc);
+  if (cached)
+    fused_kernel<true><<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
+  else
+    fused_kernel<false><<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

@@ -85,7 +85,7 @@ struct FusedParams {
   int* elem_count;                  // [n_elements] (COUNT mode)
   const long long* elem_offset;     // [n_elements] exclusive scan (ORDERED mode)
   unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
-  long long* prof;                  // optional phase cycles [grid][2][6] (debug)
+  const double* geo;                // optional geometry cache d(r,s,t)/d(x,y,z): [E][9][512]
 };
 enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
 
@@ -144,6 +144,7 @@ struct ResolveParams {
 int set_dmat_constant(const double* dmat);
 int fused_grid(int64_t n_elements);       // CTAs (= triangle regions) of launch_fused
 int launch_fused(const FusedParams& p, cudaStream_t s);
+int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* geo, cudaStream_t s);
 int launch_compact(const float4* tri, const unsigned long long* meta, const unsigned long long* region_count,
                    int n_regions, int64_t region_cap, float4* out_tri, unsigned long long* out_meta,
                    int64_t n_total, cudaStream_t s);

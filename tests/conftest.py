@@ -30,3 +30,13 @@ def ctx():
     c = Context(0)
     yield c
     c.close()
+
+
+@pytest.fixture(params=["geo_cached", "geo_uncached"])
+def ctx_geo(request, ctx):
+    """The session context with the per-mesh geometry cache on or off: both
+    fused-kernel variants must give bit-identical results."""
+    on = request.param == "geo_cached"
+    ctx.set_geometry_cache(on)
+    yield ctx
+    ctx.set_geometry_cache(True)

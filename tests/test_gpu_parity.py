@@ -83,11 +83,11 @@ BOX_PIPES = {
 
 
 @pytest.mark.parametrize("name", list(BOX_PIPES))
-def test_box_pipelines_bit_exact(ctx, name):
+def test_box_pipelines_bit_exact(ctx_geo, name):
     case = synth.box(nel=(4, 3, 3))
     pipe = Pipeline(**{**BOX_PIPES[name].__dict__, "emit_meta": True})
-    _, res = _run(ctx, case, pipe)
-    _check_against_oracle(ctx, case, pipe, res)
+    _, res = _run(ctx_geo, case, pipe)
+    _check_against_oracle(ctx_geo, case, pipe, res)
 
 
 def _rows(t):
@@ -110,12 +110,12 @@ def test_fast_path_triangle_set_and_image(ctx, name):
     assert np.array_equal(res.rgba, rgba)
 
 
-def test_taylor_green_c1_bit_exact(ctx):
+def test_taylor_green_c1_bit_exact(ctx_geo):
     case = synth.taylor_green()
     pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.1),), color_field="velocity:mag", width=256, height=256,
                     view_dir=(35.0, 30.0), emit_meta=True)
-    _, res = _run(ctx, case, pipe)
-    _check_against_oracle(ctx, case, pipe, res)
+    _, res = _run(ctx_geo, case, pipe)
+    _check_against_oracle(ctx_geo, case, pipe, res)
 
 
 def test_aos_host_velocity_layout(ctx):
@@ -209,6 +209,66 @@ def test_repeat_is_deterministic(ctx):
     assert np.array_equal(r1.rgba, r2.rgba) and np.array_equal(r1.depth, r2.depth)
 
 
+# ------------------------------------------------------------- geometry cache
+
+
+def _ro(a):
+    a = np.array(a)
+    a.flags.writeable = False
+    return a
+
+
+def test_static_mesh_reuses_geometry_cache(ctx):
+    """Same read-only coordinate arrays step after step (static NekRS mesh):
+    the cache is built once and reused; every step stays bit-exact."""
+    case = synth.box(nel=(3, 3, 2))
+    case.x, case.y, case.z = _ro(case.x), _ro(case.y), _ro(case.z)
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="vorticity:mag", emit_meta=True,
+                    timing=True)
+    da = SemDataAdaptor(ctx)
+    an = InsituAnalysis(pipe)
+    da.initialize(_snapshot(case))
+    r1 = an.execute(da, depth=True)
+    assert r1.report.geometry_cached
+    h2d_first = da.h2d_bytes
+    rng = np.random.default_rng(3)
+    case.fields["velocity"] = case.fields["velocity"] + 0.1 * rng.standard_normal(case.fields["velocity"].shape)
+    da.initialize(_snapshot(case, step=1))
+    r2 = an.execute(da, depth=True)
+    assert r2.report.geometry_cached and r2.report.ms_geometry == 0.0
+    assert da.h2d_bytes == h2d_first - 3 * 8 * case.n_points         # coordinates not re-sent
+    _check_against_oracle(ctx, case, pipe, r2)
+
+
+def test_moving_mesh_rebuilds_geometry_cache(ctx):
+    """New coordinates (host arrays) or in-place edits of device coordinates
+    followed by mesh_modified() give the new mesh's exact results."""
+    import torch
+
+    case = synth.box(nel=(3, 2, 2))
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="temperature", emit_meta=True)
+    da = SemDataAdaptor(ctx)
+    an = InsituAnalysis(pipe)
+    da.initialize(_snapshot(case))
+    an.execute(da, depth=True)
+    # host: deform the mesh, new arrays
+    case.x = case.x + 0.05 * np.sin(3.0 * case.y)
+    da.initialize(_snapshot(case, step=1))
+    _check_against_oracle(ctx, case, pipe, an.execute(da, depth=True))
+    # device arrays edited in place
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (case.x, case.y, case.z)]
+    flds = tuple(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=case.n_points)
+                 for k, v in case.fields.items())
+    blk = lambda: Snapshot(0.0, 2, 0, (SemBlock(case.n_elements, *dev, fields=flds),))
+    da.initialize(blk())
+    an.execute(da, depth=True)
+    case.z = case.z + 0.03 * np.cos(2.0 * case.x)
+    dev[2].copy_(torch.from_numpy(case.z))
+    da.initialize(blk())
+    da.mesh_modified()
+    _check_against_oracle(ctx, case, pipe, an.execute(da, depth=True))
+
+
 # ---------------------------------------------------------------- DataAdaptor
 
 
@@ -232,7 +292,8 @@ def test_get_mesh_connectivity_and_points(ctx):
     assert np.array_equal(pts, np.stack([case.x, case.y, case.z], axis=1))
 
 
-def test_add_array_exports_bit_exact(ctx):
+def test_add_array_exports_bit_exact(ctx_geo):
+    ctx = ctx_geo
     case = synth.box(nel=(3, 2, 2))
     da = SemDataAdaptor(ctx)
     da.initialize(_snapshot(case))

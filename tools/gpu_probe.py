@@ -28,13 +28,19 @@ def main():
     ap.add_argument("--width", type=int, default=1024)
     ap.add_argument("--no-surfaces", action="store_true")
     ap.add_argument("--color", default=None)
+    ap.add_argument("--geo", choices=("on", "off", "both"), default="both")
+    ap.add_argument("--device-gen", action="store_true", help="generate the case on the GPU (fast; no --oracle)")
     a = ap.parse_args()
     t0 = time.time()
-    case = synth.make_case(a.config) if a.config != "box" else synth.box()
+    if a.device_gen:
+        from paper_2312_09888_b200 import synth_device
+        case = synth_device.make_case(a.config, 0, 1, device="cuda:0")
+    else:
+        case = synth.make_case(a.config) if a.config != "box" else synth.box()
     print(f"[{a.config}] E={case.n_elements} pts={case.n_points} gen {time.time()-t0:.1f}s", flush=True)
     ctx = Context(0)
     da = SemDataAdaptor(ctx)
-    fields = tuple(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=case.n_points)
+    fields = tuple(FieldArray(k, POINT, v.shape[0], v.reshape(-1), comp_stride=case.n_points)
                    for k, v in case.fields.items())
     blk = SemBlock(case.n_elements, case.x, case.y, case.z, fields=fields)
     da.initialize(Snapshot(0.0, 0, 0, (blk,)))
@@ -48,28 +54,24 @@ def main():
     if a.color:
         pipe = replace(pipe, color_field=a.color)
     an = InsituAnalysis(pipe)
-    for r in range(a.reps):
-        res = an.execute(da)
-        rp = res.report
-        tot = rp.ms_fused + rp.ms_raster + rp.ms_composite + rp.ms_resolve
-        gb = case.n_points * 8 * (3 + sum(v.shape[0] for v in case.fields.values())) / 1e9
-        print(f"rep {r}: ntri={rp.n_triangles} fused {rp.ms_fused:.3f} ms ({gb / rp.ms_fused:.0f} GB/s of "
-              f"{gb:.2f} GB) raster {rp.ms_raster:.3f} resolve {rp.ms_resolve:.3f} total {tot:.3f} ms "
-              f"range {rp.range} reran={rp.reran}", flush=True)
-    if os.environ.get("NKB_PROFILE_PHASES"):
-        import ctypes as C
-        from paper_2312_09888_b200 import _native as N
-        L = N.lib()
-        fn = L.nkb_debug_phase_profile
-        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
-        buf = np.zeros((148, 2, 2, 4), np.int64)       # [cta][group][pencil-thread | aux-thread][phase]
-        N.check(fn(ctx.handle, buf.ctypes.data, 148))
-        names = ["wait+bar1", "pencils|emit", "bar2+prefetch / classify", "node"]
-        tot = buf.sum(axis=(0, 1))
-        for r, rname in enumerate(("pencil-thread", "aux-thread")):
-            t = tot[r].sum()
-            print(rname, " ".join(f"{n}={v / t * 100:.1f}%" for n, v in zip(names, tot[r])),
-                  f"cycles/elem/group={t / (case.n_elements / 2):.0f}")
+    plane = any(s.kind == "slice" for s in pipe.surfaces)
+    images = {}
+    for geo in (("on", "off") if a.geo == "both" else (a.geo,)):
+        ctx.set_geometry_cache(geo == "on")
+        for r in range(a.reps):
+            res = an.execute(da)
+            rp = res.report
+            tot = rp.ms_fused + rp.ms_raster + rp.ms_composite + rp.ms_resolve
+            bpp = 8 * sum(v.shape[0] for v in case.fields.values())
+            bpp += (24 if (not rp.geometry_cached or plane) else 0) + (72 if rp.geometry_cached else 0)
+            gb = case.n_points * bpp / 1e9
+            print(f"geo={geo} rep {r}: ntri={rp.n_triangles} fused {rp.ms_fused:.3f} ms ({gb / rp.ms_fused * 1e3:.0f} GB/s"
+                  f" of {gb:.2f} GB) raster {rp.ms_raster:.3f} resolve {rp.ms_resolve:.3f} total {tot:.3f} ms "
+                  f"range {rp.range} reran={rp.reran} cached={rp.geometry_cached} build={rp.ms_geometry:.3f}",
+                  flush=True)
+        images[geo] = res.rgba.copy()
+    if len(images) == 2:
+        print("cached == uncached image:", np.array_equal(images["on"], images["off"]))
     if a.oracle:
         from oracle import oracle as orc
         cf = orc.CaseFields(case.x, case.y, case.z, case.fields)
