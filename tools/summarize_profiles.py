@@ -27,6 +27,12 @@ def launches(tag):
              f"{'kernel':60s} {'launches':>8s} {'mean_us':>10s} {'share':>7s}"]
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"{k[:60]:60s} {len(v):8d} {sum(v) / len(v) / 1e3:10.2f} {sum(v) / tot * 100:6.1f}%")
+    ours = {k: v for k, v in per.items() if "nkb::" in k}
+    t2 = sum(sum(v) for v in ours.values()) or 1.0
+    lines += ["", "# libnekb200 kernels only (the rest is the synthetic-data generator and torch glue)",
+              f"{'kernel':60s} {'launches':>8s} {'mean_us':>10s} {'share':>7s}"]
+    for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"{k[:60]:60s} {len(v):8d} {sum(v) / len(v) / 1e3:10.2f} {sum(v) / t2 * 100:6.1f}%")
     return "\n".join(lines) + "\n"
 
 
@@ -67,6 +73,21 @@ def main(tag):
         f = float(v.replace(",", ""))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         return f * scale
+    # per-source-line stall samples of the same capture (where the warps wait)
+    rep = os.path.join(ROOT, "gpurun_out", f"{tag}_fused.ncu-rep")
+    page = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                          capture_output=True, text=True).stdout
+    tmp = os.path.join(ROOT, "gpurun_out", f"{tag}_source.csv")
+    open(tmp, "w").write(page)
+    top = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), tmp, "40"],
+                         capture_output=True, text=True).stdout
+    open(os.path.join(ROOT, "profiles", f"{tag}_fused_lines.txt"), "w").write(
+        f"# fused_kernel stall samples / instructions by CUDA source line (ncu source page), tag {tag}\n" + top)
+    bj = os.path.join(ROOT, "gpurun_out", f"{tag}_bench.json")
+    if os.path.exists(bj):
+        js = [ln for ln in open(bj).read().splitlines() if ln.startswith("{")]
+        if js:
+            open(os.path.join(ROOT, "profiles", f"{tag}_bench.json"), "w").write(js[-1] + "\n")
     if "dram__bytes_read.sum" in m:
         traffic = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
         json.dump({"dram_bytes_per_launch": traffic, "source": f"profiles/{tag}_fused_full.txt"},
