@@ -182,6 +182,12 @@ int nkb_image_device(nkb_ctx* ctx, const unsigned char** rgba, const float** dep
                      const uint64_t** zbuf);
 /* copy the last image to host memory (rgba: W*H*4, depth: W*H floats, either may be NULL) */
 int nkb_image_copy(nkb_ctx* ctx, unsigned char* rgba, float* depth, void* stream);
+/* The image as a complete binary PPM (P6 header + RGB rows, top row first),
+ * byte-identical to write_ppm(ImageRGB(...)) (sinks.py:298-303), in
+ * library-owned PINNED host memory valid until the next call on this ctx:
+ * the RGBA->RGB pack runs on the GPU and only 3 B/pixel cross PCIe.
+ * replaces: ImageRGB(w, h, rgba[..., :3].tobytes()) + write_ppm's encode */
+int nkb_image_ppm(nkb_ctx* ctx, const unsigned char** ppm, int64_t* nbytes, void* stream);
 /* triangles of the last execute, in deterministic (element, cell, surface, table) order:
  *   tri  [n*12] float: per vertex (x, y, z, colour scalar), 3 vertices
  *   meta [n]    uint64: element<<32 | cell<<16 | surface<<12 | tri_in_case<<8 | case

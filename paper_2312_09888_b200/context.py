@@ -134,6 +134,13 @@ class Context:
                stream or None)
         return (rgba, dep) if depth else rgba
 
+    def image_ppm(self, stream: int = 0) -> memoryview:
+        """The last image as complete PPM bytes (header + RGB), packed on the
+        GPU into library-owned pinned memory; valid until the next call."""
+        ptr, n = C.c_void_p(), C.c_int64()
+        N.call("nkb_image_ppm", self.handle, C.byref(ptr), C.byref(n), stream or None)
+        return memoryview((C.c_ubyte * n.value).from_address(ptr.value)).cast("B")
+
     def image_device(self) -> tuple[int, int, int]:
         a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
         N.call("nkb_image_device", self.handle, C.byref(a), C.byref(b), C.byref(c))

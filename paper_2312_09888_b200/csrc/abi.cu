@@ -132,6 +132,9 @@ struct nkb_ctx {
   unsigned long long* zbuf = nullptr;       // W*H + 2 range words
   unsigned char* rgba = nullptr;
   float* depth = nullptr;
+  unsigned char* rgb_dev = nullptr;         // packed RGB for the PPM payload
+  unsigned char* h_ppm = nullptr;           // pinned: PPM header + RGB
+  int64_t ppm_cap = 0;
   double* range_dev = nullptr;
   int W = 0, H = 0;
   bool image_valid = false;
@@ -325,6 +328,8 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->depth);
   cudaFree(ctx->range_dev);
   cudaFree(ctx->geo);
+  cudaFree(ctx->rgb_dev);
+  cudaFreeHost(ctx->h_ppm);
   cudaFree(ctx->s_ptrs);
   cudaFree(ctx->s_col0);
   cudaFree(ctx->s_minmax);
@@ -975,6 +980,34 @@ int nkb_image_copy(nkb_ctx* ctx, unsigned char* rgba, float* depth, void* stream
   if (rgba) NKB_CUDA(cudaMemcpyAsync(rgba, ctx->rgba, npx * 4, cudaMemcpyDeviceToHost, s));
   if (depth) NKB_CUDA(cudaMemcpyAsync(depth, ctx->depth, npx * sizeof(float), cudaMemcpyDeviceToHost, s));
   NKB_CUDA(cudaStreamSynchronize(s));
+  return NKB_OK;
+}
+
+int nkb_image_ppm(nkb_ctx* ctx, const unsigned char** ppm, int64_t* nbytes, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ppm || !nbytes) return fail(NKB_EINVAL, "null out");
+  if (!ctx->image_valid) return fail(NKB_ESTATE, "no image (execute not run, or not the composite root)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npx = (int64_t)ctx->W * ctx->H;
+  char hdr[64];
+  const int hn = snprintf(hdr, sizeof(hdr), "P6\n%d %d\n255\n", ctx->W, ctx->H);
+  const int64_t total = hn + 3 * npx;
+  if (ctx->ppm_cap < total) {
+    cudaFree(ctx->rgb_dev);
+    cudaFreeHost(ctx->h_ppm);
+    ctx->rgb_dev = nullptr;
+    ctx->h_ppm = nullptr;
+    ctx->ppm_cap = 0;
+    NKB_CUDA(cudaMalloc(&ctx->rgb_dev, (size_t)std::max<int64_t>(3 * npx, 16)));
+    NKB_CUDA(cudaMallocHost(&ctx->h_ppm, (size_t)total));
+    ctx->ppm_cap = total;
+  }
+  memcpy(ctx->h_ppm, hdr, hn);
+  NKB_TRY(launch_pack_rgb(ctx->rgba, ctx->rgb_dev, npx, s));
+  NKB_CUDA(cudaMemcpyAsync(ctx->h_ppm + hn, ctx->rgb_dev, (size_t)(3 * npx), cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  *ppm = ctx->h_ppm;
+  *nbytes = total;
   return NKB_OK;
 }
 

@@ -153,6 +153,7 @@ int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
 int launch_raster(const RasterParams& p, cudaStream_t s);
 int launch_range_words(const unsigned long long* counters, unsigned long long* words, cudaStream_t s);
 int launch_resolve(const ResolveParams& p, cudaStream_t s);
+int launch_pack_rgb(const unsigned char* rgba, unsigned char* rgb, int64_t npx, cudaStream_t s);
 int launch_points_aos(const double* x, const double* y, const double* z, int64_t npts,
                       double* out, cudaStream_t s);
 int launch_connectivity(int64_t ncells, int64_t* conn, int64_t* offsets, unsigned char* types,

@@ -261,6 +261,26 @@ __global__ void __launch_bounds__(256) structured_render_kernel(const Structured
   }
 }
 
+// RGBA8 -> packed RGB8 (the PPM payload): 4 pixels per thread, 16 B in, 12 B out
+__global__ void pack_rgb_kernel(const uchar4* __restrict__ rgba, unsigned char* __restrict__ rgb, long long npx) {
+  const long long n4 = npx / 4;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n4; q += (long long)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(rgba)[q];        // pixels 4q .. 4q+3, bytes r g b a
+    uint3 o;
+    o.x = __byte_perm(v.x, v.y, 0x4210);      // r0 g0 b0 r1
+    o.y = __byte_perm(v.y, v.z, 0x5421);      // g1 b1 r2 g2
+    o.z = __byte_perm(v.z, v.w, 0x6542);      // b2 r3 g3 b3
+    reinterpret_cast<uint3*>(rgb)[q] = o;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (npx & 3)) {
+    const long long i = n4 * 4 + threadIdx.x;
+    const uchar4 c = rgba[i];
+    rgb[3 * i] = c.x;
+    rgb[3 * i + 1] = c.y;
+    rgb[3 * i + 2] = c.z;
+  }
+}
+
 inline unsigned grid_for(long long n, int threads, int max_blocks) {
   long long b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -286,6 +306,14 @@ int launch_raster(const RasterParams& p, cudaStream_t s) {
 int launch_range_words(const unsigned long long* counters, unsigned long long* words,
                        cudaStream_t s) {
   range_words_kernel<<<1, 1, 0, s>>>(counters, words);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_pack_rgb(const unsigned char* rgba, unsigned char* rgb, int64_t npx, cudaStream_t s) {
+  if (npx <= 0) return NKB_OK;
+  pack_rgb_kernel<<<grid_for(npx / 4 + 1, 256, 148 * 8), 256, 0, s>>>(reinterpret_cast<const uchar4*>(rgba), rgb,
+                                                                     (long long)npx);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

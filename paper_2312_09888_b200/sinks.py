@@ -217,13 +217,18 @@ class InsituSink:
             ctx = self.comm.ctx if self.comm is not None else default_context()
             self.adaptor = SemDataAdaptor(ctx, velocity=self.velocity)
         self.adaptor.initialize(s)
-        res = self.analysis.execute(self.adaptor)
+        ctx = self.adaptor.ctx
+        res = self.analysis.execute(self.adaptor, fetch_image=False)
         self.last = res
-        if res.rgba is None:
+        if not ((ctx.nranks == 1) or (not self.pipeline.composite) or ctx.rank == 0):
             return 0
-        img = ImageRGB(self.pipeline.width, self.pipeline.height, res.rgba[..., :3].tobytes())
+        # header + RGB packed on the GPU into pinned memory: same bytes as
+        # write_ppm(ImageRGB(w, h, rgba[..., :3].tobytes())) (sinks.py:298-303)
+        ppm = ctx.image_ppm()
         fname = f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}.ppm"
-        return write_ppm(img, self.dir / fname)
+        with open(self.dir / fname, "wb") as f:
+            f.write(ppm)
+        return len(ppm)
 
     def finalize(self):
         pass

@@ -126,3 +126,27 @@ def test_failing_insitu_sink_is_isolated(tmp_path):
                    fields=(FieldArray("temperature", POINT, 1, case.fields["temperature"].ravel()),))
     reps = br.update(Snapshot(0.0, 0, 0, (blk,)))
     assert "ValueError" in reps[0].error and reps[1].error is None
+
+
+@pytest.mark.parametrize("wh", [(7, 5), (80, 60), (1, 1), (13, 3)])
+def test_image_ppm_equals_write_ppm_bytes(tmp_path, wh):
+    """GPU RGB pack + pinned PPM buffer == write_ppm(ImageRGB(rgba[..., :3]))
+    byte for byte, including pixel counts that are not a multiple of 4."""
+    from paper_2312_09888_b200.adaptor import SemDataAdaptor
+    from paper_2312_09888_b200.analysis import InsituAnalysis, Pipeline, Surface
+    from paper_2312_09888_b200.context import Context
+    from paper_2312_09888_b200.sinks import ImageRGB, write_ppm
+
+    w, h = wh
+    case = synth.box(nel=(2, 2, 2))
+    ctx = Context(0)
+    da = SemDataAdaptor(ctx)
+    fields = tuple(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=case.n_points)
+                   for k, v in case.fields.items())
+    da.initialize(Snapshot(0.0, 0, 0, (SemBlock(case.n_elements, case.x, case.y, case.z, fields=fields),)))
+    res = InsituAnalysis(Pipeline(surfaces=(Surface("iso", "temperature", 0.6),), color_field="temperature",
+                                  width=w, height=h)).execute(da)
+    n = write_ppm(ImageRGB(w, h, res.rgba[..., :3].tobytes()), tmp_path / "a.ppm")
+    ppm = bytes(ctx.image_ppm())
+    assert len(ppm) == n and ppm == (tmp_path / "a.ppm").read_bytes()
+    ctx.close()
