@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   int qn[4];                                          // swizzled slots of my 4 nodes
 #pragma unroll
   for (int h = 0; h < 4; ++h) qn[h] = sw_node(t + kMcThreads * h);
-  auto prefetch = [&](long long e, int b) {
+  auto prefetch_mc = [&](long long e, int b) {
     double* dst = S_ring + b * nin * kArr;
     const long long g0 = e * (long long)kNN + t;
 #pragma unroll
@@ -292,6 +292,31 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
 #pragma unroll
         for (int h = 0; h < 4; ++h) cp_async8(d + qn[h], src + kMcThreads * h);
       }
+    }
+  };
+  // When the pencil warps have slack (cached geometry, or no gradients at
+  // all) warps 0-7 stage the next element instead, taking the cp.async issue
+  // work off the MC warps, which are on the critical path.
+  const bool pw_prefetch = kCached || !p.need_grad;
+  const int qp0 = sw_node(tid & 255), qp1 = sw_node((tid & 255) + 256);
+  auto prefetch_pw = [&](long long e, int b) {
+    double* dst = S_ring + b * nin * kArr;
+    const long long g0 = e * (long long)kNN + tid;
+#pragma unroll
+    for (int f = 0; f < kMaxIn; ++f) {
+      if (f < nin) {
+        const double* src = p.in_ptr[f] + g0;
+        double* d = dst + f * kArr;
+        cp_async8(d + qp0, src);
+        cp_async8(d + qp1, src + 256);
+      }
+    }
+  };
+  auto prefetch = [&](long long e, int b) {
+    if (pw_prefetch) {
+      if (tid < 256) prefetch_pw(e, b);
+    } else if (is_mc) {
+      prefetch_mc(e, b);
     }
   };
 
@@ -418,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   for (int i = tid; i < 256; i += kThreads) mc.t_ntri[i] = g_mc_ntri[i];
   for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kThreads) (&mc.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
   if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
-  if (is_mc && n_it > 0) prefetch(blockIdx.x, 0);
+  if (n_it > 0) prefetch(blockIdx.x, 0);
   __shared__ unsigned long long s_geo_bar;
   constexpr unsigned kGeoBytes = 9u * kNN * sizeof(double);
   if (kCached && tid == 0) {
@@ -430,12 +455,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     const long long e = blockIdx.x + it * G;
     const int slot = (int)(it % kRing);
     const int par = (int)(it & 1);
-    if (is_mc) cp_async_wait_all();
+    cp_async_wait_all();                               // my share of element `it` landed
     __syncthreads();                                   // element `it` staged; node phase it-1 done
     const double* S_in = S_ring + slot * nin * kArr;
+    if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
+    cp_async_commit();
     if (is_mc) {
-      if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
-      cp_async_commit();
       if (it > 0 && p.n_surf > 0) {
         const int ps = (int)((it - 1) % kRing), pp = (int)((it - 1) & 1);
         mc_element(e - G, pp, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr);
@@ -514,7 +539,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
       if (p.need_umag) vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
       unsigned bits = 0;
-      for (int s = 0; s < p.n_surf; ++s) {
+#pragma unroll
+      for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
+        if (s >= p.n_surf) break;
         const int src = p.surf_src[s];
         double val;
         if (src >= SRC_PLANE)
@@ -554,7 +581,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         w |= (unsigned long long)S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)] << (8 * v);
       unsigned packed = 0;
       int nc = 0;
-      for (int s = 0; s < p.n_surf; ++s) {
+#pragma unroll
+      for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
+        if (s >= p.n_surf) break;
         const unsigned cs = case_of(w, s);
         packed |= cs << (8 * s);
         nc += mc.t_ntri[cs];
