@@ -250,8 +250,8 @@ __device__ __forceinline__ unsigned case_of(unsigned long long w, int s) {
 // (p.geo: per element 9 arrays of 512 doubles, 36 KB contiguous) instead of
 // x,y,z derivative pencils.  One thread moves element it+1's block into S_geo
 // with a single bulk (TMA) copy as soon as the node phase of element it has
-// consumed it; the node phase of it+1 waits on the mbarrier.  The 384 pencil
-// threads split the u,v,w pencils in two halves of output rows.
+// consumed it; the node phase of it+1 waits on the mbarrier.  Warps 0-5 do
+// the u,v,w pencils; warps 8-11 stage the next element.
 // slot_xyz < 0: x,y,z are not staged (no slice plane; emission reads them via L2).
 template <bool kCached>
 __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nin, int slot_sc,
@@ -295,8 +295,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     }
   };
   // When the pencil warps have slack (cached geometry, or no gradients at
-  // all) warps 0-7 stage the next element instead, taking the cp.async issue
-  // work off the MC warps, which are on the critical path.
+  // all) they stage the next element instead of the MC warps, which are on
+  // the critical path: warps 8-11 with cached geometry, warps 0-7 without
+  // gradients.
   const bool pw_prefetch = kCached || !p.need_grad;
   const int qp0 = sw_node(tid & 255), qp1 = sw_node((tid & 255) + 256);
   auto prefetch_pw = [&](long long e, int b) {
@@ -312,8 +313,26 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
     }
   };
+  int qx[4];
+#pragma unroll
+  for (int h = 0; h < 4; ++h) qx[h] = sw_node((tid & 127) + kMcThreads * h);
+  auto prefetch_w811 = [&](long long e, int b) {
+    double* dst = S_ring + b * nin * kArr;
+    const long long g0 = e * (long long)kNN + (tid & 127);
+#pragma unroll
+    for (int f = 0; f < kMaxIn; ++f) {
+      if (f < nin) {
+        const double* src = p.in_ptr[f] + g0;
+        double* d = dst + f * kArr;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) cp_async8(d + qx[h], src + kMcThreads * h);
+      }
+    }
+  };
   auto prefetch = [&](long long e, int b) {
-    if (pw_prefetch) {
+    if (kCached) {
+      if (tid >= 256 && tid < 384) prefetch_w811(e, b);     // warps 8-11; 0-5 do the pencils
+    } else if (pw_prefetch) {
       if (tid < 256) prefetch_pw(e, b);
     } else if (is_mc) {
       prefetch_mc(e, b);
@@ -472,11 +491,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       int off[kNP];
       pencil_offsets(dir, tid & 7, (tid >> 3) & 7, off);
       if (kCached) {
-        // u,v,w only; g selects output rows {0,1,6,7} or {2,3,4,5}
-        const double* su = S_in + slot_vel * kArr;
-        double* d0 = S_dv + dir * kArr;
-        if (g == 0) pencil3<0, 2>(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
-        else pencil3<2, 2>(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
+        // u,v,w only, on warps 0-5 (warps 8-11 stage the next element)
+        if (g == 0) {
+          const double* su = S_in + slot_vel * kArr;
+          double* d0 = S_dv + dir * kArr;
+          pencil3(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
+        }
       } else {
         // g = 0: x,y,z   1: u,v,w
         const int sf = (g == 0) ? slot_xyz : slot_vel;
