@@ -470,17 +470,22 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     if (n_it > 0) bulk_load(S_geo, p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes, &s_geo_bar);
   }
   cp_async_commit();
+  int cls_any = 0;                                     // my sub-hex of the last element emits triangles
   for (long long it = 0; it <= n_it; ++it) {
     const long long e = blockIdx.x + it * G;
     const int slot = (int)(it % kRing);
     const int par = (int)(it & 1);
     cp_async_wait_all();                               // my share of element `it` landed
-    __syncthreads();                                   // element `it` staged; node phase it-1 done
+    // element `it` staged; node phase it-1 done; does element it-1 emit anything?
+    const int prev_emits = __syncthreads_or(cls_any);
+    cls_any = 0;
     const double* S_in = S_ring + slot * nin * kArr;
     if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
     cp_async_commit();
     if (is_mc) {
-      if (it > 0 && p.n_surf > 0) {
+      if (it > 0 && p.n_surf > 0 && !prev_emits) {
+        if (p.mode == FUSED_COUNT && t == 0) p.elem_count[e - G] = 0;   // empty element: skip the scan
+      } else if (it > 0 && p.n_surf > 0) {
         const int ps = (int)((it - 1) % kRing), pp = (int)((it - 1) & 1);
         mc_element(e - G, pp, S_ring + ps * nin * kArr, S_q + pp * 2 * kArr);
       }
@@ -594,11 +599,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     if (tid < kNC) {
       const int c = tid;
       const int a = c % kN, b = (c / kN) % kN, k = c / (kN * kN);
-      const int n0 = a + kNP * b + kNP * kNP * k;
-      unsigned long long w = 0;
-#pragma unroll
-      for (int v = 0; v < 8; ++v)
-        w |= (unsigned long long)S_bits[n0 + voff_i(v) + kNP * voff_j(v) + kNP * kNP * voff_k(v)] << (8 * v);
+      // the 8 corner bytes in VTK order from 4 node rows (8 bytes each):
+      // row(b,k) -> v0 v1, row(b+1,k) -> v3 v2, row(b,k+1) -> v4 v5, row(b+1,k+1) -> v7 v6
+      const unsigned long long* rows = reinterpret_cast<const unsigned long long*>(S_bits);
+      const int sh = 8 * a;
+      const unsigned r00 = (unsigned)(rows[b + kNP * k] >> sh), r10 = (unsigned)(rows[b + 1 + kNP * k] >> sh);
+      const unsigned r01 = (unsigned)(rows[b + kNP * (k + 1)] >> sh);
+      const unsigned r11 = (unsigned)(rows[b + 1 + kNP * (k + 1)] >> sh);
+      const unsigned long long w = (unsigned long long)__byte_perm(r00, r10, 0x4510) |
+                                   ((unsigned long long)__byte_perm(r01, r11, 0x4510) << 32);
       unsigned packed = 0;
       int nc = 0;
 #pragma unroll
@@ -610,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
       mc.cases[par][c] = packed;
       mc.ntri[par][c] = (unsigned char)nc;
+      cls_any = nc;
     }
   }
 
