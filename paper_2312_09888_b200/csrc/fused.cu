@@ -408,12 +408,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
       return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
     };
-    for (int tt = t; tt < total; tt += kMcThreads) {
-      const int c = mc.tri_cell[tt];
+    // triangle slot tt -> (cell, surface, case, table row)
+    auto locate = [&](int tt, int& c, int& s, unsigned& cs, int& k) {
+      c = mc.tri_cell[tt];
       int li = tt - (int)mc.coff[c];
       const unsigned packed = mc.cases[par][c];
-      int s = 0;
-      unsigned cs = packed & 0xffu;
+      s = 0;
+      cs = packed & 0xffu;
       for (;;) {
         const int nt = mc.t_ntri[cs];
         if (li < nt) break;
@@ -421,41 +422,70 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         ++s;
         cs = (packed >> (8 * s)) & 0xffu;
       }
-      const int k = li;
-      const long long out = (long long)base + tt;
-      if (p.mode == FUSED_FAST ? (out - (long long)blockIdx.x * p.region_cap >= p.region_cap)
-                               : (out >= p.tri_cap))
-        continue;   // overflow: counted, not written; the host grows the buffer and re-runs
+      k = li;
+    };
+    auto overflow = [&](long long out) {   // counted, not written; the host grows the buffer and re-runs
+      return p.mode == FUSED_FAST ? (out - (long long)blockIdx.x * p.region_cap >= p.region_cap)
+                                  : (out >= p.tri_cap);
+    };
+    auto vertex = [&](int c, int s, unsigned cs, int k, int r) -> float4 {
       const int ca = c % kN, cb = (c / kN) % kN, ck = c / (kN * kN);
       const int src = p.surf_src[s];
       const double iso = p.surf_iso[s];
-      float4 vtx[3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int ed = mc.t_tri[cs][3 * k + r];
-        const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
-        const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
-        const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
-        const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
-        const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
-        const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
-        const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
-        const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
-        const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
-        const double xa = Sx[pa], ya = Sy[pa], za = Sz[pa];
-        const double xb = Sx[pb], yb = Sy[pb], zb = Sz[pb];
-        vtx[r].x = __double2float_rn(__fma_rn(tv, __dsub_rn(xb, xa), xa));
-        vtx[r].y = __double2float_rn(__fma_rn(tv, __dsub_rn(yb, ya), ya));
-        vtx[r].z = __double2float_rn(__fma_rn(tv, __dsub_rn(zb, za), za));
-        vtx[r].w = __double2float_rn(__fma_rn(tv, __dsub_rn(clb, cla), cla));
-      }
-      float4* dst = p.tri + 3 * out;
-      dst[0] = vtx[0];
-      dst[1] = vtx[1];
-      dst[2] = vtx[2];
+      const int ed = mc.t_tri[cs][3 * k + r];
+      const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
+      const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
+      const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
+      const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
+      const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
+      const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
+      const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
+      const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
+      const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
+      const double xa = Sx[pa], ya = Sy[pa], za = Sz[pa];
+      const double xb = Sx[pb], yb = Sy[pb], zb = Sz[pb];
+      float4 v;
+      v.x = __double2float_rn(__fma_rn(tv, __dsub_rn(xb, xa), xa));
+      v.y = __double2float_rn(__fma_rn(tv, __dsub_rn(yb, ya), ya));
+      v.z = __double2float_rn(__fma_rn(tv, __dsub_rn(zb, za), za));
+      v.w = __double2float_rn(__fma_rn(tv, __dsub_rn(clb, cla), cla));
+      return v;
+    };
+    auto put_meta = [&](long long out, int c, int s, int k, unsigned cs) {
       if (p.meta)
         p.meta[out] = ((unsigned long long)e << 32) | ((unsigned long long)c << 16) |
                       ((unsigned long long)s << 12) | ((unsigned long long)k << 8) | cs;
+    };
+    if (3 * total <= kMcThreads) {
+      // small element (the common case): one task per triangle VERTEX -- one
+      // pass with a third of the dependent chain, consecutive float4 stores
+      if (t < 3 * total) {
+        const int tt = t / 3, r = t - 3 * tt;
+        int c, s, k;
+        unsigned cs;
+        locate(tt, c, s, cs, k);
+        const long long out = (long long)base + tt;
+        if (!overflow(out)) {
+          p.tri[3 * out + r] = vertex(c, s, cs, k, r);
+          if (r == 0) put_meta(out, c, s, k, cs);
+        }
+      }
+    } else {
+      for (int tt = t; tt < total; tt += kMcThreads) {
+        int c, s, k;
+        unsigned cs;
+        locate(tt, c, s, cs, k);
+        const long long out = (long long)base + tt;
+        if (overflow(out)) continue;
+        float4 v[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) v[r] = vertex(c, s, cs, k, r);
+        float4* dst = p.tri + 3 * out;
+        dst[0] = v[0];
+        dst[1] = v[1];
+        dst[2] = v[2];
+        put_meta(out, c, s, k, cs);
+      }
     }
   };
 
