@@ -7,6 +7,7 @@
 // The step is stream-ordered; nkb_execute synchronises once at the end to fill
 // the report (SENSEI's Execute returns after the analysis ran).
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <dlfcn.h>
 #include <math.h>
 #include <nccl.h>
@@ -157,6 +158,7 @@ struct nkb_ctx {
   int64_t geo_cap = 0;                       // points
   bool geo_used = false;                     // last step used it
   bool geo_built = false;                    // last step (re)built it
+  unsigned long long* prof = nullptr;        // debug phase profile (NKB_PROFILE_PHASES=1)
   // P2P composite state (composite.cu)
   struct {
     bool ready = false, unavailable = false;
@@ -328,6 +330,7 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->depth);
   cudaFree(ctx->range_dev);
   cudaFree(ctx->geo);
+  cudaFree(ctx->prof);
   cudaFree(ctx->rgb_dev);
   cudaFreeHost(ctx->h_ppm);
   cudaFree(ctx->s_ptrs);
@@ -926,7 +929,26 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   ctx->geo_used = ctx->geo_built = false;
   if (p->timing) NKB_CUDA(cudaEventRecord(ctx->ev[5], s));
   NKB_TRY(geo_attach(ctx, fp, s));
+  const bool prof = getenv("NKB_PROFILE_PHASES") != nullptr && !ordered;
+  if (prof) {
+    if (!ctx->prof) NKB_CUDA(cudaMalloc(&ctx->prof, 18 * sizeof(unsigned long long)));
+    NKB_CUDA(cudaMemsetAsync(ctx->prof, 0, 18 * sizeof(unsigned long long), s));
+    fp.prof = ctx->prof;
+  }
   NKB_TRY(run_step(ctx, p, fp, cm, s, composite, ordered));
+  if (prof) {
+    unsigned long long h[18];
+    NKB_CUDA(cudaMemcpy(h, ctx->prof, sizeof(h), cudaMemcpyDeviceToHost));
+    static const char* ph[6] = {"top-barrier", "role-work", "pre-node-wait", "node", "post-node-wait", "classify"};
+    static const char* role[3] = {"pencil(w0)", "stage(w8)", "mc(w12)"};
+    for (int r = 0; r < 3; ++r) {
+      fprintf(stderr, "[nkb phases] %-11s", role[r]);
+      for (int k = 0; k < 6; ++k)
+        fprintf(stderr, " %s=%.0f", ph[k], ctx->E ? (double)h[6 * r + k] / (double)ctx->E : 0.0);
+      fprintf(stderr, " (cycles/element)\n");
+    }
+    fp.prof = nullptr;
+  }
   int reran = 0;
   int64_t ntri = (int64_t)ctx->h_counters[0];
   const int64_t need = needed_capacity(ctx, ordered);

@@ -253,7 +253,9 @@ __device__ __forceinline__ unsigned case_of(unsigned long long w, int s) {
 // consumed it; the node phase of it+1 waits on the mbarrier.  Warps 0-5 do
 // the u,v,w pencils; warps 8-11 stage the next element.
 // slot_xyz < 0: x,y,z are not staged (no slice plane; emission reads them via L2).
-template <bool kCached>
+// kProf (debug, NKB_PROFILE_PHASES=1): lane 0 of warps 0 (pencils), 8
+// (staging) and 12 (MC) accumulate clock64 cycles per loop phase.
+template <bool kCached, bool kProf>
 __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p, int nin, int slot_sc,
                                                             int slot_vel, int slot_xyz) {
   constexpr int kD = kCached ? 9 : kNumD;              // derivative arrays held
@@ -501,6 +503,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   }
   cp_async_commit();
   int cls_any = 0;                                     // my sub-hex of the last element emits triangles
+  long long pacc[6] = {0, 0, 0, 0, 0, 0}, pt = kProf ? clock64() : 0;
+  auto tick = [&](int ph) {
+    if (kProf) {
+      const long long now = clock64();
+      pacc[ph] += now - pt;
+      pt = now;
+    }
+  };
   for (long long it = 0; it <= n_it; ++it) {
     const long long e = blockIdx.x + it * G;
     const int slot = (int)(it % kRing);
@@ -508,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     cp_async_wait_all();                               // my share of element `it` landed
     // element `it` staged; node phase it-1 done; does element it-1 emit anything?
     const int prev_emits = __syncthreads_or(cls_any);
+    tick(0);
     cls_any = 0;
     const double* S_in = S_ring + slot * nin * kArr;
     if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
@@ -541,8 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       }
     }
     if (it == n_it) break;
+    tick(1);
     if (kCached) mbar_wait(&s_geo_bar, (unsigned)(it & 1));   // geometry of element `it` landed
     __syncthreads();                                   // derivatives of element `it` ready
+    tick(2);
 
     // ---- node phase: one node per thread ----
     {
@@ -619,8 +632,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         cmax = fmax(cmax, c);
       }
     }
+    tick(3);
     if (p.n_surf == 0 && !kCached) continue;
     __syncthreads();                                   // case bits of element `it` ready
+    tick(4);
     if (kCached && tid == 0 && it + 1 < n_it)          // S_geo consumed: fetch element it+1
       bulk_load(S_geo, p.geo + (e + G) * 9 * kNN, kGeoBytes, &s_geo_bar);
     if (p.n_surf == 0) continue;
@@ -651,6 +666,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       mc.ntri[par][c] = (unsigned char)nc;
       cls_any = nc;
     }
+    tick(5);
+  }
+  if (kProf && lane == 0 && (warp == 0 || warp == 8 || warp == 12)) {
+    const int role = warp == 0 ? 0 : (warp == 8 ? 1 : 2);
+#pragma unroll
+    for (int ph = 0; ph < 6; ++ph) atomicAdd(p.prof + 6 * role + ph, (unsigned long long)pacc[ph]);
   }
 
   if (p.mode == FUSED_FAST && p.region_count != nullptr && tid == kPencilThreads) {
@@ -838,20 +859,25 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   const size_t shm = fused_smem_bytes(nin);
   static bool attr_set = false;
   if (!attr_set) {
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)fused_smem_bytes(kMaxIn)));
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)fused_smem_bytes(kMaxIn)));
+    const int mx = (int)fused_smem_bytes(kMaxIn);
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     int dev = 0;
     NKB_CUDA(cudaGetDevice(&dev));
     NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     attr_set = true;
   }
   const int grid = fused_grid(p.n_elements);
-  if (cached)
-    fused_kernel<true><<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
-  else
-    fused_kernel<false><<<(unsigned)grid, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
+  const unsigned gx = (unsigned)grid;
+  if (p.prof) {
+    if (cached) fused_kernel<true, true><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
+    else fused_kernel<false, true><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
+  } else {
+    if (cached) fused_kernel<true, false><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
+    else fused_kernel<false, false><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
+  }
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

@@ -86,6 +86,7 @@ struct FusedParams {
   const long long* elem_offset;     // [n_elements] exclusive scan (ORDERED mode)
   unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
   const double* geo;                // optional geometry cache d(r,s,t)/d(x,y,z): [E][9][512]
+  unsigned long long* prof;         // debug: [role 3][phase 6] cycle sums (NKB_PROFILE_PHASES=1)
 };
 enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
 
