@@ -188,6 +188,24 @@ int nkb_image_copy(nkb_ctx* ctx, unsigned char* rgba, float* depth, void* stream
  * the RGBA->RGB pack runs on the GPU and only 3 B/pixel cross PCIe.
  * replaces: ImageRGB(w, h, rgba[..., :3].tobytes()) + write_ppm's encode */
 int nkb_image_ppm(nkb_ctx* ctx, const unsigned char** ppm, int64_t* nbytes, void* stream);
+
+/* ---- field statistics (StatsSink, sinks.py:366-393) ------------------------ */
+/* One borrowed DEVICE array run: n_tuples tuples of ncomp components, the
+ * components comp_stride values apart (SoA), read in the reference's AoS
+ * order (component fastest, data_model.py:8-14). */
+typedef struct nkb_segment {
+    const double* base;
+    int64_t       n_tuples;
+    int           ncomp;
+    int64_t       comp_stride;   /* ignored when ncomp == 1 */
+} nkb_segment;
+/* min, max and mean of the concatenated segments -- and, with collective != 0
+ * and a communicator, of all ranks' concatenations in rank order -- with
+ * numpy's arithmetic: out = {vals.min(), vals.max(), vals.mean()}, the mean
+ * being np.add.reduce's pairwise summation divided by the count, bit for bit.
+ * NaN anywhere gives NaN min/max/mean.  Zero values: NKB_EINVAL (numpy raises).
+ * replaces: np.concatenate(...) + min/max/mean in StatsSink.consume (sinks.py:381-386) */
+int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, double out[3], void* stream);
 /* triangles of the last execute, in deterministic (element, cell, surface, table) order:
  *   tri  [n*12] float: per vertex (x, y, z, colour scalar), 3 vertices
  *   meta [n]    uint64: element<<32 | cell<<16 | surface<<12 | tri_in_case<<8 | case

@@ -54,6 +54,7 @@ class SemDataAdaptor:
         self._staging: dict[str, DeviceArray] = {}
         self._fields: dict[str, FieldArray] = {}
         self._coords = None
+        self._segments: dict[str, tuple[int, int, int]] = {}   # name -> (ptr, ncomp, comp_stride)
         self.time = 0.0
         self.step = 0
         self.h2d_bytes = 0
@@ -90,6 +91,7 @@ class SemDataAdaptor:
         self._coords = coords
         self.ctx.field_clear()
         self._fields = {}
+        self._segments = {}
         for f in b.fields:
             if f.association != POINT:
                 raise ValueError(f"field {f.name!r}: only point fields exist on the SEM mesh")
@@ -111,17 +113,28 @@ class SemDataAdaptor:
         self.h2d_bytes += a.nbytes
         return d
 
+    def _set(self, name: str, base, ncomp: int, stride: int) -> None:
+        self.ctx.field_set(name, base, ncomp, stride)
+        self._segments[name] = (device_ptr(base), ncomp, stride)
+
+    def field_segment(self, name: str) -> tuple[int, int, int, int]:
+        """(device ptr, n_points, ncomp, comp_stride) of a bound point field."""
+        if name not in self._segments:
+            raise ValueError(f"no field named {name!r}")
+        ptr, nc, st = self._segments[name]
+        return ptr, self._require().point_count, nc, st
+
     def _bind_field(self, f: FieldArray, npts: int) -> None:
         if isinstance(f.values, tuple):  # one device (or host) array per component
             comps = [self._dev(f"{f.name}#{c}", f.values[c], npts) for c in range(f.components)]
             if f.components == 1:
-                self.ctx.field_set(f.name, comps[0], 1, npts)
+                self._set(f.name, comps[0], 1, npts)
                 return
             # components must be evenly spaced for the ABI's (base, stride) form
             ptrs = [device_ptr(c) for c in comps]
             stride = (ptrs[1] - ptrs[0]) // 8 if len(ptrs) > 1 else npts
             if all(ptrs[c] == ptrs[0] + 8 * stride * c for c in range(len(ptrs))) and stride >= npts:
-                self.ctx.field_set(f.name, ptrs[0], f.components, stride)
+                self._set(f.name, ptrs[0], f.components, stride)
                 return
             # not evenly spaced: gather into one staging array (D2D)
             d = self._staging.get(f.name)
@@ -130,23 +143,23 @@ class SemDataAdaptor:
                 self._staging[f.name] = d
             for c, p in enumerate(ptrs):
                 N.call("nkb_memcpy", d.ptr + 8 * c * npts, p, 8 * npts, 3, None)
-            self.ctx.field_set(f.name, d, f.components, npts)
+            self._set(f.name, d, f.components, npts)
             return
         if is_device_array(f.values):
             stride = f.comp_stride or npts
-            self.ctx.field_set(f.name, f.values, f.components, stride)
+            self._set(f.name, f.values, f.components, stride)
             return
         # host values: component-fastest AoS (reference layout) or SoA with comp_stride
         a = np.asarray(f.values, dtype=np.float64)
         if f.components > 1 and not f.comp_stride:
             a = np.ascontiguousarray(a.reshape(npts, f.components).T)   # AoS -> SoA
             d = self._dev(f.name, a, npts, f.components)
-            self.ctx.field_set(f.name, d, f.components, npts)
+            self._set(f.name, d, f.components, npts)
         else:
             stride = f.comp_stride or npts
             n = (f.components - 1) * stride + npts
             d = self._dev(f.name, a[:n], n)
-            self.ctx.field_set(f.name, d, f.components, stride)
+            self._set(f.name, d, f.components, stride)
 
     # ---- GetNumberOfMeshes / GetMeshMetadata ------------------------------------------
     def get_number_of_meshes(self) -> int:

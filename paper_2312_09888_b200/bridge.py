@@ -35,6 +35,7 @@ _ATTRS_BY_KIND: dict[str, frozenset[str]] = {
     "render": frozenset({"dir", "width", "height", "field", "vmin", "vmax"}),
     "insitu": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
                          "velocity", "composite"}),
+    "stats": frozenset({"path"}),
     "null": frozenset(),
 }
 _ALIASES = {"catalyst": "render"}
@@ -86,6 +87,8 @@ def _spec_from_element(el: ET.Element) -> AnalysisSpec:
             log.warning("ignoring unknown attribute %r on analysis type %r", key, kind)
             continue
         params[key] = val
+    if kind == "stats" and "path" not in params:
+        raise ConfigError("stats analysis requires a 'path' attribute")
     return AnalysisSpec(kind, freq, params)
 
 

@@ -141,6 +141,17 @@ class Context:
         N.call("nkb_image_ppm", self.handle, C.byref(ptr), C.byref(n), stream or None)
         return memoryview((C.c_ubyte * n.value).from_address(ptr.value)).cast("B")
 
+    def stats(self, segments, collective: bool = False, stream: int = 0) -> tuple[float, float, float]:
+        """(min, max, mean) of the concatenated device segments
+        [(ptr, n_tuples, ncomp, comp_stride), ...] in AoS order, with numpy's
+        arithmetic (nkb_stats); collective: over all ranks in rank order."""
+        arr = (N.NkbSegment * max(1, len(segments)))()
+        for i, (ptr, n, nc, st) in enumerate(segments):
+            arr[i] = N.NkbSegment(C.c_void_p(int(ptr)), int(n), int(nc), int(st))
+        out = (C.c_double * 3)()
+        N.call("nkb_stats", self.handle, arr, len(segments), int(bool(collective)), out, stream or None)
+        return float(out[0]), float(out[1]), float(out[2])
+
     def image_device(self) -> tuple[int, int, int]:
         a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
         N.call("nkb_image_device", self.handle, C.byref(a), C.byref(b), C.byref(c))

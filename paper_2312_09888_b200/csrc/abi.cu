@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -501,6 +502,273 @@ int nkb_mesh_bounds(nkb_ctx* ctx, double* out6, void* stream) {
     out6[2 * a] = dec_ordered_h(h6[a]);
     out6[2 * a + 1] = dec_ordered_h(~h6[3 + a]);
   }
+  return NKB_OK;
+}
+
+// ---- field statistics (stats sink) --------------------------------------------
+
+// device copies of one pairwise plan (tables for the chunks this rank owns)
+struct StatsTables {
+  std::vector<PlanChunk> plan;
+  std::vector<StatChunk> mine;                 // owned chunks, local offsets
+  std::vector<int> mine_idx;                   // their plan indices
+  std::vector<int> owned_count;                // per rank
+  std::vector<StatShapeHost> shapes;
+  std::map<long long, int> shape_of_len;
+  StatChunk* d_chunks = nullptr;
+  StatShape* d_shapes = nullptr;
+  int2* d_leaves = nullptr;
+  int2* d_nodes = nullptr;
+  int* d_levels = nullptr;
+  double* d_out = nullptr;                     // sums [n] + mm [3n]
+  int n_dev = 0;
+};
+
+static int shape_id(StatsTables& T, long long len) {
+  auto it = T.shape_of_len.find(len);
+  if (it != T.shape_of_len.end()) return it->second;
+  StatShapeHost sh;
+  pairwise_shape(len, sh);
+  if ((int)sh.leaves.size() > kMaxChunkLeaves) return -1;
+  T.shapes.push_back(std::move(sh));
+  const int id = (int)T.shapes.size() - 1;
+  T.shape_of_len[len] = id;
+  return id;
+}
+
+static void stats_tables_free(StatsTables& T) {
+  cudaFree(T.d_chunks);
+  cudaFree(T.d_shapes);
+  cudaFree(T.d_leaves);
+  cudaFree(T.d_nodes);
+  cudaFree(T.d_levels);
+  cudaFree(T.d_out);
+  T.d_chunks = nullptr;
+  T.d_shapes = nullptr;
+  T.d_leaves = nullptr;
+  T.d_nodes = nullptr;
+  T.d_levels = nullptr;
+  T.d_out = nullptr;
+}
+
+// upload chunk list + shape tables; returns the kernel parameters
+static int stats_upload(StatsTables& T, const std::vector<StatChunk>& chunks, StatsParams& P) {
+  std::vector<StatShape> shp;
+  std::vector<int2> lv, nd;
+  std::vector<int> ls;
+  for (auto& sh : T.shapes) {
+    StatShape d;
+    d.leaf0 = (int)lv.size();
+    d.n_leaves = (int)sh.leaves.size();
+    d.node0 = (int)nd.size();
+    d.n_nodes = (int)sh.nodes.size();
+    d.level0 = (int)ls.size();
+    d.n_levels = sh.n_levels;
+    lv.insert(lv.end(), sh.leaves.begin(), sh.leaves.end());
+    nd.insert(nd.end(), sh.nodes.begin(), sh.nodes.end());
+    ls.insert(ls.end(), sh.level_start.begin(), sh.level_start.end());
+    shp.push_back(d);
+  }
+  if (nd.empty()) nd.push_back(make_int2(0, 0));
+  if (ls.empty()) ls.push_back(0);
+  stats_tables_free(T);
+  const int n = (int)chunks.size();
+  NKB_CUDA(cudaMalloc(&T.d_chunks, sizeof(StatChunk) * std::max(n, 1)));
+  NKB_CUDA(cudaMalloc(&T.d_shapes, sizeof(StatShape) * std::max<size_t>(shp.size(), 1)));
+  NKB_CUDA(cudaMalloc(&T.d_leaves, sizeof(int2) * std::max<size_t>(lv.size(), 1)));
+  NKB_CUDA(cudaMalloc(&T.d_nodes, sizeof(int2) * nd.size()));
+  NKB_CUDA(cudaMalloc(&T.d_levels, sizeof(int) * ls.size()));
+  NKB_CUDA(cudaMalloc(&T.d_out, sizeof(double) * 4 * std::max(n, 1)));
+  if (n) NKB_CUDA(cudaMemcpy(T.d_chunks, chunks.data(), sizeof(StatChunk) * n, cudaMemcpyHostToDevice));
+  if (!shp.empty()) NKB_CUDA(cudaMemcpy(T.d_shapes, shp.data(), sizeof(StatShape) * shp.size(), cudaMemcpyHostToDevice));
+  if (!lv.empty()) NKB_CUDA(cudaMemcpy(T.d_leaves, lv.data(), sizeof(int2) * lv.size(), cudaMemcpyHostToDevice));
+  NKB_CUDA(cudaMemcpy(T.d_nodes, nd.data(), sizeof(int2) * nd.size(), cudaMemcpyHostToDevice));
+  NKB_CUDA(cudaMemcpy(T.d_levels, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
+  T.n_dev = n;
+  P.chunks = T.d_chunks;
+  P.n_chunks = n;
+  P.shapes = T.d_shapes;
+  P.leaves = T.d_leaves;
+  P.nodes = T.d_nodes;
+  P.level_start = T.d_levels;
+  P.out_sum = T.d_out;
+  P.out_mm = T.d_out + std::max(n, 1);
+  return NKB_OK;
+}
+
+int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, double out[3], void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!out || (nseg > 0 && !segs)) return fail(NKB_EINVAL, "null argument");
+  if (nseg < 0 || nseg > kMaxSeg) return fail(NKB_EINVAL, "between 0 and 16 segments");
+  cudaStream_t s = (cudaStream_t)stream;
+  StatsParams P;
+  memset(&P, 0, sizeof(P));
+  long long n = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const nkb_segment& g = segs[i];
+    if (g.n_tuples < 0 || g.ncomp < 1) return fail(NKB_EINVAL, "bad segment shape");
+    if (g.n_tuples > 0 && !g.base) return fail(NKB_EINVAL, "null segment pointer");
+    if (g.ncomp > 1 && g.comp_stride < g.n_tuples) return fail(NKB_EINVAL, "comp_stride smaller than the tuple count");
+    if (g.n_tuples == 0) continue;
+    StatSeg& d = P.seg[P.nseg++];
+    d.base = g.base;
+    d.n_tuples = g.n_tuples;
+    d.ncomp = g.ncomp;
+    d.comp_stride = g.ncomp > 1 ? g.comp_stride : g.n_tuples;
+    d.start = n;
+    n += g.n_tuples * g.ncomp;
+  }
+  P.n = n;
+  // global layout: rank r holds values [lo[r], lo[r+1])
+  const bool coll = collective && ctx->comm && ctx->nranks > 1;
+  const int R = coll ? ctx->nranks : 1, me = coll ? ctx->rank : 0;
+  std::vector<long long> lo(R + 1, 0);
+  if (coll) {
+    unsigned long long* d = nullptr;
+    NKB_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long) * (R + 1), s));
+    const unsigned long long mine = (unsigned long long)n;
+    NKB_CUDA(cudaMemcpyAsync(d + R, &mine, sizeof(mine), cudaMemcpyHostToDevice, s));
+    NKB_NCCL(g_nccl.AllGather(d + R, d, 1, ncclUint64, ctx->comm, s));
+    std::vector<unsigned long long> cnt(R);
+    NKB_CUDA(cudaMemcpyAsync(cnt.data(), d, sizeof(unsigned long long) * R, cudaMemcpyDeviceToHost, s));
+    NKB_CUDA(cudaFreeAsync(d, s));
+    NKB_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < R; ++r) lo[r + 1] = lo[r] + (long long)cnt[r];
+  } else {
+    lo[1] = n;
+  }
+  const long long N = lo[R];
+  if (N == 0) return fail(NKB_EINVAL, "zero-size array to reduction operation minimum which has no identity");
+
+  StatsTables T;
+  pairwise_plan(N, lo, T.plan);
+  const int nc = (int)T.plan.size();
+  T.owned_count.assign(R, 0);
+  std::vector<int> boundary;
+  for (int i = 0; i < nc; ++i) {
+    const PlanChunk& c = T.plan[i];
+    if (c.owner < 0) {
+      boundary.push_back(i);
+      continue;
+    }
+    ++T.owned_count[c.owner];
+    if (c.owner == me) {
+      const int sid = shape_id(T, c.n);
+      if (sid < 0) return fail(NKB_EINVAL, "internal: chunk shape too large");
+      T.mine.push_back({c.off - lo[me], sid});
+      T.mine_idx.push_back(i);
+    }
+  }
+  std::vector<double> sums(nc, 0.0);
+  double mn = INFINITY, mx = -INFINITY;
+  bool nan = false;
+  auto run = [&](const std::vector<StatChunk>& chunks, StatsParams& Q, std::vector<double>& hs,
+                 std::vector<double>& hm) -> int {
+    NKB_TRY(stats_upload(T, chunks, Q));
+    NKB_TRY(launch_pairwise_chunks(Q, s));
+    const int m = (int)chunks.size();
+    hs.resize(m);
+    hm.resize(3 * (size_t)m);
+    if (m) {
+      NKB_CUDA(cudaMemcpyAsync(hs.data(), Q.out_sum, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+      NKB_CUDA(cudaMemcpyAsync(hm.data(), Q.out_mm, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+    }
+    NKB_CUDA(cudaStreamSynchronize(s));
+    return NKB_OK;
+  };
+  std::vector<double> hs, hm;
+  NKB_TRY(run(T.mine, P, hs, hm));
+  double lmn = INFINITY, lmx = -INFINITY, lnan = 0.0;
+  for (size_t k = 0; k < T.mine.size(); ++k) {
+    lmn = fmin(lmn, hm[3 * k]);
+    lmx = fmax(lmx, hm[3 * k + 1]);
+    if (hm[3 * k + 2] != 0.0) lnan = 1.0;
+  }
+  if (!coll) {
+    for (size_t k = 0; k < T.mine.size(); ++k) sums[T.mine_idx[k]] = hs[k];
+    mn = lmn;
+    mx = lmx;
+    nan = lnan != 0.0;
+  } else {
+    // every rank's owned chunk sums (contiguous in plan order) + min / max
+    int maxo = 0;
+    for (int r = 0; r < R; ++r) maxo = std::max(maxo, T.owned_count[r]);
+    const int w = maxo + 3;
+    std::vector<double> send(w, 0.0), all((size_t)w * R);
+    for (size_t k = 0; k < T.mine.size(); ++k) send[k] = hs[k];
+    send[maxo] = lmn;
+    send[maxo + 1] = lmx;
+    send[maxo + 2] = lnan;
+    double* d = nullptr;
+    NKB_CUDA(cudaMallocAsync(&d, sizeof(double) * (size_t)w * (R + 1), s));
+    NKB_CUDA(cudaMemcpyAsync(d + (size_t)w * R, send.data(), sizeof(double) * w, cudaMemcpyHostToDevice, s));
+    NKB_NCCL(g_nccl.AllGather(d + (size_t)w * R, d, w, ncclFloat64, ctx->comm, s));
+    NKB_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(double) * (size_t)w * R, cudaMemcpyDeviceToHost, s));
+    // boundary windows: first / last kWin values of every rank
+    std::vector<double> win((size_t)2 * kWin * R);
+    double* dw = nullptr;
+    if (!boundary.empty()) {
+      NKB_CUDA(cudaMallocAsync(&dw, sizeof(double) * 2 * kWin * (R + 1), s));
+      NKB_TRY(launch_stat_windows(P, dw + (size_t)2 * kWin * R, s));
+      NKB_NCCL(g_nccl.AllGather(dw + (size_t)2 * kWin * R, dw, 2 * kWin, ncclFloat64, ctx->comm, s));
+      NKB_CUDA(cudaMemcpyAsync(win.data(), dw, sizeof(double) * 2 * kWin * R, cudaMemcpyDeviceToHost, s));
+    }
+    NKB_CUDA(cudaStreamSynchronize(s));
+    NKB_CUDA(cudaFreeAsync(d, s));
+    if (dw) NKB_CUDA(cudaFreeAsync(dw, s));
+    std::vector<int> seen(R, 0);
+    for (int i = 0; i < nc; ++i) {
+      const int o = T.plan[i].owner;
+      if (o >= 0) sums[i] = all[(size_t)w * o + seen[o]++];
+    }
+    for (int r = 0; r < R; ++r) {
+      if (lo[r + 1] == lo[r]) continue;
+      mn = fmin(mn, all[(size_t)w * r + maxo]);
+      mx = fmax(mx, all[(size_t)w * r + maxo + 1]);
+      if (all[(size_t)w * r + maxo + 2] != 0.0) nan = true;
+    }
+    if (!boundary.empty()) {
+      // the leaves across rank boundaries, rebuilt from the windows and
+      // summed on the GPU like any other chunk (every rank, same result)
+      std::vector<double> vals;
+      std::vector<StatChunk> bch;
+      T.shapes.clear();
+      T.shape_of_len.clear();
+      for (int i : boundary) {
+        const PlanChunk& c = T.plan[i];
+        bch.push_back({(long long)vals.size(), shape_id(T, c.n)});
+        for (long long g = c.off; g < c.off + c.n; ++g) {
+          const int r = (int)(std::upper_bound(lo.begin(), lo.end(), g) - lo.begin()) - 1;
+          const long long l = g - lo[r], nr = lo[r + 1] - lo[r];
+          vals.push_back(l < kWin ? win[(size_t)2 * kWin * r + l]
+                                  : win[(size_t)2 * kWin * r + kWin + (l - (nr - kWin))]);
+        }
+      }
+      double* dv = nullptr;
+      NKB_CUDA(cudaMalloc(&dv, sizeof(double) * vals.size()));
+      NKB_CUDA(cudaMemcpy(dv, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice));
+      StatsParams B;
+      memset(&B, 0, sizeof(B));
+      B.nseg = 1;
+      B.seg[0] = {dv, (long long)vals.size(), 1, (long long)vals.size(), 0};
+      B.n = (long long)vals.size();
+      std::vector<double> bs, bm;
+      const int rc = run(bch, B, bs, bm);
+      cudaFree(dv);
+      NKB_TRY(rc);
+      for (size_t k = 0; k < boundary.size(); ++k) {
+        sums[boundary[k]] = bs[k];
+        mn = fmin(mn, bm[3 * k]);
+        mx = fmax(mx, bm[3 * k + 1]);
+        if (bm[3 * k + 2] != 0.0) nan = true;
+      }
+    }
+  }
+  stats_tables_free(T);
+  const double total = 0.0 + pairwise_combine(N, lo, sums);      // np.add.reduce: identity + pairwise
+  out[0] = nan ? NAN : mn;
+  out[1] = nan ? NAN : mx;
+  out[2] = total / (double)N;                                    // np.mean: sum / count
   return NKB_OK;
 }
 

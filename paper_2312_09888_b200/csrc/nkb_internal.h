@@ -154,6 +154,53 @@ int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
 int launch_raster(const RasterParams& p, cudaStream_t s);
 int launch_range_words(const unsigned long long* counters, unsigned long long* words, cudaStream_t s);
 int launch_resolve(const ResolveParams& p, cudaStream_t s);
+// ---- stats.cu: numpy-exact min / max / mean ----
+constexpr long long kChunk = 32768;      // values per CTA subtree (<= 640 leaves of 57..128)
+constexpr int kWin = 128;                // boundary window (one pairwise leaf)
+constexpr int kMaxChunkLeaves = 640;
+constexpr int kMaxSeg = 16;
+struct StatSeg {
+  const double* base;
+  long long n_tuples;
+  int ncomp;
+  long long comp_stride;
+  long long start;                       // first AoS index of this segment
+};
+struct StatChunk {
+  long long off;                         // first AoS index (in the segments' numbering)
+  int shape;
+};
+struct StatShape {
+  int leaf0, n_leaves, node0, n_nodes, level0, n_levels;
+};
+struct StatsParams {
+  StatSeg seg[kMaxSeg];
+  int nseg;
+  long long n;                           // values in the segments
+  const StatChunk* chunks;
+  int n_chunks;
+  const StatShape* shapes;
+  const int2* leaves;                    // (offset in chunk, length)
+  const int2* nodes;                     // children as slots of the value array
+  const int* level_start;
+  double* out_sum;                       // [n_chunks]
+  double* out_mm;                        // [n_chunks][3]: min, max, nan flag
+};
+struct PlanChunk {
+  long long off, n;
+  int owner;                             // rank, or -1 for a leaf across a rank boundary
+};
+struct StatShapeHost {
+  std::vector<int2> leaves, nodes;
+  std::vector<int> level_start;
+  int n_levels = 0;
+};
+void pairwise_plan(long long n, const std::vector<long long>& rank_lo, std::vector<PlanChunk>& out);
+double pairwise_combine(long long n, const std::vector<long long>& rank_lo, const std::vector<double>& chunk_sums);
+void pairwise_shape(long long n, StatShapeHost& sh);
+int launch_pairwise_chunks(const StatsParams& p, cudaStream_t s);
+int launch_stat_windows(const StatsParams& p, double* out, cudaStream_t s);
+
 int launch_pack_rgb(const unsigned char* rgba, unsigned char* rgb, int64_t npx, cudaStream_t s);
 int launch_points_aos(const double* x, const double* y, const double* z, int64_t npts,
                       double* out, cudaStream_t s);

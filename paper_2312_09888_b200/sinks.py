@@ -13,10 +13,13 @@ bytes written, ``finalize()`` flushes.  Registered kinds:
 * ``insitu`` -- the SEM hot path: adaptor -> Q -> iso/slice -> raster ->
   composite (analysis.InsituAnalysis); writes one PPM per trigger on the
   composite root.
+* ``stats`` -- drop-in for the reference's StatsSink (:366-393): appends
+  ``step,time,field,min,max,mean`` rows; the reductions run on the GPU
+  (nkb_stats) with numpy's exact arithmetic, so the rows are byte-identical.
 * ``null`` -- counts invocations (:354-363).
 
-The checkpoint and stats sinks of the reference are outside the hot path
- and are not provided.
+The reference's checkpoint sink is outside the hot path
+and is not provided.
 """
 from __future__ import annotations
 
@@ -29,8 +32,8 @@ from . import _native as N
 from .adaptor import SemDataAdaptor
 from .analysis import InsituAnalysis, pipeline_from_params
 from .context import Context
-from .data_model import CELL, check_assembly
-from .device import DeviceArray, is_device_array
+from .data_model import CELL, SemBlock, check_assembly
+from .device import DeviceArray, device_ptr, is_device_array
 
 
 @dataclass(frozen=True)
@@ -234,6 +237,87 @@ class InsituSink:
         pass
 
 
+def _device_len(d) -> int:
+    shape = d.__cuda_array_interface__["shape"]
+    return int(np.prod(shape)) if len(shape) else 1
+
+
+class StatsSink:
+    """Appends step,time,field,min,max,mean rows (sinks.py:366-393).
+
+    Structured snapshots (the reference's data model): every block, point and
+    component of each field, concatenated in block order, exactly as
+    ``np.concatenate([b.field_named(name).values for b in s.blocks])``.  SEM
+    snapshots: the rank's SemBlock; with a communicator the statistics are
+    global (all ranks' values in rank order) and rank 0 writes the file.
+    min / max / mean come from nkb_stats, bit-identical to numpy's."""
+
+    HEADER = "step,time,field,min,max,mean"
+
+    def __init__(self, params: dict[str, str], comm=None):
+        self.path = Path(params["path"])
+        self.comm = comm
+        self.root = comm is None or comm.rank == 0
+        if self.root:
+            if self.path.parent != Path(""):
+                self.path.parent.mkdir(parents=True, exist_ok=True)
+            if not self.path.exists():
+                self.path.write_text(self.HEADER + "\n")
+            _probe_writable(self.path.parent)
+        self._ctx: Context | None = None
+        self._adaptor: SemDataAdaptor | None = None
+        self._staging: dict[tuple[int, str], DeviceArray] = {}
+
+    @property
+    def ctx(self) -> Context:
+        if self._ctx is None:
+            self._ctx = self.comm.ctx if self.comm is not None else default_context()
+        return self._ctx
+
+    def _segments(self, s) -> tuple[list[str], dict[str, list], bool]:
+        blocks = list(s.blocks)
+        names = [f.name for f in blocks[0].fields]
+        if isinstance(blocks[0], SemBlock):
+            if self._adaptor is None:
+                self._adaptor = SemDataAdaptor(self.ctx)
+            self._adaptor.initialize(s)
+            return names, {n: [self._adaptor.field_segment(n)] for n in names}, self.comm is not None
+        segs: dict[str, list] = {}
+        for name in names:
+            lst = []
+            for bi, b in enumerate(blocks):
+                vals = b.field_named(name).values
+                if is_device_array(vals):
+                    d = vals
+                else:
+                    a = np.ascontiguousarray(vals, dtype=np.float64).ravel()
+                    d = self._staging.get((bi, name))
+                    if d is None or d.size != a.size:
+                        d = DeviceArray.empty(self.ctx, (a.size,), np.float64)
+                        self._staging[(bi, name)] = d
+                    d.upload(a, sync=False)
+                n = _device_len(d)
+                lst.append((device_ptr(d), n, 1, n))
+            segs[name] = lst
+        return names, segs, False
+
+    def consume(self, s) -> int:
+        names, segs, collective = self._segments(s)
+        rows = []
+        for name in names:
+            mn, mx, mean = self.ctx.stats(segs[name], collective)
+            rows.append(f"{s.step},{s.time:.17g},{name},{mn:.17g},{mx:.17g},{mean:.17g}")
+        text = "\n".join(rows) + "\n"
+        if not self.root:
+            return 0
+        with open(self.path, "a") as f:
+            f.write(text)
+        return len(text)
+
+    def finalize(self):
+        pass
+
+
 class NullSink:
     def __init__(self, params: dict[str, str] | None = None, comm=None):
         self.count = 0
@@ -249,6 +333,7 @@ class NullSink:
 _SINK_TYPES = {
     "render": RenderSink,
     "insitu": InsituSink,
+    "stats": StatsSink,
     "null": NullSink,
 }
 

@@ -86,3 +86,55 @@ def test_composite_equals_single_gpu(tmp_path, size, mode):
     assert np.array_equal(a["rng"], b["rng"])
     assert np.array_equal(a["rgba"], b["rgba"])
     assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
+
+
+_STAT_SIZES = {2: [70, 1000001], 4: [100003, 5, 0, 250], 3: [40, 300000, 77]}
+
+
+def _stats_worker(rank, size, port, out_dir):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        from paper_2312_09888_b200.comm import Communicator
+        from paper_2312_09888_b200.context import Context
+        from paper_2312_09888_b200.device import DeviceArray
+
+        sizes = _STAT_SIZES[size]
+        rng = np.random.default_rng(99)
+        glob = rng.standard_normal(sum(sizes)) * 10.0 ** rng.integers(-4, 5, sum(sizes))
+        lo = sum(sizes[:rank])
+        mine = glob[lo:lo + sizes[rank]]
+        ctx = Context(rank)
+        comm = Communicator.from_torch(ctx)
+        segs = []
+        if mine.size:
+            d = DeviceArray.empty(ctx, (mine.size,), np.float64)
+            d.upload(np.ascontiguousarray(mine))
+            segs = [(d.ptr, mine.size, 1, mine.size)]
+        got = ctx.stats(segs, collective=True)
+        if rank == 0:
+            np.save(os.path.join(out_dir, f"stats{size}.npy"), np.array(got))
+        dist.barrier()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size", [2, 3, 4])
+def test_collective_stats_equal_numpy_on_concatenation(tmp_path, size):
+    """Global min/max/mean over uneven (even empty and tiny) rank partitions,
+    bit-identical to numpy on the rank-ordered concatenation: chunks that
+    straddle rank boundaries are rebuilt from the exchanged edge windows."""
+    if _ngpus() < size:
+        pytest.skip(f"needs {size} GPUs")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_stats_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    sizes = _STAT_SIZES[size]
+    rng = np.random.default_rng(99)
+    glob = rng.standard_normal(sum(sizes)) * 10.0 ** rng.integers(-4, 5, sum(sizes))
+    got = np.load(tmp_path / f"stats{size}.npy")
+    exp = np.array([glob.min(), glob.max(), glob.mean()])
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)), (got, exp)
