@@ -171,6 +171,15 @@ int nkb_get_mesh(nkb_ctx* ctx, double* points, int64_t* conn, int64_t* offsets,
  * replaces: scalar_field (sinks.py:227-242) / FieldArray export */
 int nkb_add_array(nkb_ctx* ctx, const char* name, int association,
                   double* out, int* ncomp_out, void* stream);
+/* Checkpoint export (legacy-VTK UNSTRUCTURED_GRID, the SEM analogue of the
+ * reference's _encode_vtk, sinks.py:58-102): one BINARY section, big-endian
+ * as the legacy format requires, encoded on the GPU into the caller's DEVICE
+ * buffer `dst` (cap bytes).  what = "POINTS" (f64 x,y,z per point),
+ * "CELLS" (int32 {8, ids...} per sub-hex, VTK_HEXAHEDRON order), "CELL_TYPES"
+ * (int32 12) or any AddArray name (f64, components fastest).  dst == NULL:
+ * *nbytes = the size only.  NKB_ERANGE when cap is too small or the point ids
+ * do not fit int32. */
+int nkb_encode_be(nkb_ctx* ctx, const char* what, void* dst, int64_t cap, int64_t* nbytes, void* stream);
 int nkb_array_components(nkb_ctx* ctx, const char* name, int* ncomp_out);
 /* name of the vector field derived quantities are computed from (default "velocity") */
 int nkb_set_velocity_name(nkb_ctx* ctx, const char* name);

@@ -36,6 +36,7 @@ _ATTRS_BY_KIND: dict[str, frozenset[str]] = {
     "insitu": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
                          "velocity", "composite"}),
     "stats": frozenset({"path"}),
+    "checkpoint": frozenset({"dir", "format", "arrays"}),
     "null": frozenset(),
 }
 _ALIASES = {"catalyst": "render"}

@@ -481,6 +481,37 @@ int nkb_get_mesh(nkb_ctx* ctx, double* points, int64_t* conn, int64_t* offsets, 
   return NKB_OK;
 }
 
+int nkb_encode_be(nkb_ctx* ctx, const char* what, void* dst, int64_t cap, int64_t* nbytes, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!what || !nbytes) return fail(NKB_EINVAL, "null argument");
+  if (!ctx->x) return fail(NKB_ESTATE, "encode before mesh_set");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npts = ctx->E * kNN, ncells = ctx->E * kNC;
+  const std::string w(what);
+  int64_t need;
+  int ncomp = 0;
+  if (w == "POINTS") {
+    need = 24 * npts;
+  } else if (w == "CELLS") {
+    if (npts > 0x7fffffffLL) return fail(NKB_ERANGE, "legacy VTK CELLS hold int32 point ids: too many points");
+    need = 36 * ncells;
+  } else if (w == "CELL_TYPES") {
+    need = 4 * ncells;
+  } else {
+    NKB_TRY(nkb_array_components(ctx, what, &ncomp));
+    need = 8 * (int64_t)ncomp * npts;
+  }
+  *nbytes = need;
+  if (!dst) return NKB_OK;                                     // size query
+  if (cap < need) return fail(NKB_ERANGE, "destination too small: need " + std::to_string(need) + " bytes");
+  if (w == "POINTS") return launch_be_points(ctx->x, ctx->y, ctx->z, npts, dst, s);
+  if (w == "CELLS") return launch_be_cells(ncells, dst, s);
+  if (w == "CELL_TYPES") return launch_be_types(ncells, dst, s);
+  int nc = 0;
+  NKB_TRY(nkb_add_array(ctx, what, 0, reinterpret_cast<double*>(dst), &nc, stream));   // AoS f64
+  return launch_bswap64(dst, (int64_t)nc * npts, s);
+}
+
 int nkb_mesh_bounds(nkb_ctx* ctx, double* out6, void* stream) {
   NKB_TRY(ctx_check(ctx));
   if (!out6) return fail(NKB_EINVAL, "null out");

@@ -78,6 +78,57 @@ __global__ void field_mag_kernel(const double* __restrict__ base, long long stri
   }
 }
 
+// ---- big-endian sections of a legacy-VTK UNSTRUCTURED_GRID (checkpoint) ----
+__device__ __forceinline__ unsigned long long bswap64(unsigned long long v) {
+  const unsigned lo = (unsigned)v, hi = (unsigned)(v >> 32);
+  return ((unsigned long long)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+__device__ __forceinline__ unsigned bswap32(unsigned v) { return __byte_perm(v, 0, 0x0123); }
+
+__global__ void be_points_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                 const double* __restrict__ z, long long n, unsigned long long* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    out[3 * i + 0] = bswap64((unsigned long long)__double_as_longlong(__ldcs(x + i)));
+    out[3 * i + 1] = bswap64((unsigned long long)__double_as_longlong(__ldcs(y + i)));
+    out[3 * i + 2] = bswap64((unsigned long long)__double_as_longlong(__ldcs(z + i)));
+  }
+}
+
+// CELLS section: per cell int32 {8, 8 point ids} (VTK_HEXAHEDRON corner order)
+__global__ void be_cells_kernel(long long ncells, unsigned* __restrict__ out) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < ncells;
+       c += (long long)gridDim.x * blockDim.x) {
+    const long long e = c / kNC;
+    const int l = (int)(c - e * kNC);
+    const int a = l % kN, b = (l / kN) % kN, k = l / (kN * kN);
+    const unsigned n0 = (unsigned)(e * kNN + a + kNP * b + kNP * kNP * k);
+    const unsigned dj = kNP, dk = kNP * kNP;
+    unsigned* o = out + 9 * c;
+    o[0] = bswap32(8u);
+    o[1] = bswap32(n0);
+    o[2] = bswap32(n0 + 1);
+    o[3] = bswap32(n0 + 1 + dj);
+    o[4] = bswap32(n0 + dj);
+    o[5] = bswap32(n0 + dk);
+    o[6] = bswap32(n0 + 1 + dk);
+    o[7] = bswap32(n0 + 1 + dj + dk);
+    o[8] = bswap32(n0 + dj + dk);
+  }
+}
+
+__global__ void be_types_kernel(long long ncells, unsigned* __restrict__ out) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < ncells;
+       c += (long long)gridDim.x * blockDim.x)
+    out[c] = bswap32((unsigned)NKB_VTK_HEXAHEDRON);
+}
+
+__global__ void bswap64_kernel(unsigned long long* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = bswap64(p[i]);
+}
+
 __device__ __forceinline__ unsigned long long enc_ordered(double d) {
   unsigned long long b = (unsigned long long)__double_as_longlong(d);
   return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
@@ -120,6 +171,34 @@ int launch_bounds_kernel(const double* x, const double* y, const double* z, int6
                          unsigned long long* enc6, cudaStream_t s) {
   if (n <= 0) return NKB_OK;
   bounds_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, y, z, n, enc6);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_be_points(const double* x, const double* y, const double* z, int64_t npts, void* out, cudaStream_t s) {
+  if (npts <= 0) return NKB_OK;
+  be_points_kernel<<<grid_for(npts, 256), 256, 0, s>>>(x, y, z, npts, reinterpret_cast<unsigned long long*>(out));
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_be_cells(int64_t ncells, void* out, cudaStream_t s) {
+  if (ncells <= 0) return NKB_OK;
+  be_cells_kernel<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, reinterpret_cast<unsigned*>(out));
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_be_types(int64_t ncells, void* out, cudaStream_t s) {
+  if (ncells <= 0) return NKB_OK;
+  be_types_kernel<<<grid_for(ncells, 256), 256, 0, s>>>(ncells, reinterpret_cast<unsigned*>(out));
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_bswap64(void* p, int64_t n, cudaStream_t s) {
+  if (n <= 0) return NKB_OK;
+  bswap64_kernel<<<grid_for(n, 256), 256, 0, s>>>(reinterpret_cast<unsigned long long*>(p), n);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

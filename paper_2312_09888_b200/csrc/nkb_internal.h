@@ -201,6 +201,10 @@ void pairwise_shape(long long n, StatShapeHost& sh);
 int launch_pairwise_chunks(const StatsParams& p, cudaStream_t s);
 int launch_stat_windows(const StatsParams& p, double* out, cudaStream_t s);
 
+int launch_be_points(const double* x, const double* y, const double* z, int64_t npts, void* out, cudaStream_t s);
+int launch_be_cells(int64_t ncells, void* out, cudaStream_t s);
+int launch_be_types(int64_t ncells, void* out, cudaStream_t s);
+int launch_bswap64(void* p, int64_t n, cudaStream_t s);
 int launch_pack_rgb(const unsigned char* rgba, unsigned char* rgb, int64_t npx, cudaStream_t s);
 int launch_points_aos(const double* x, const double* y, const double* z, int64_t npts,
                       double* out, cudaStream_t s);

@@ -16,10 +16,11 @@ bytes written, ``finalize()`` flushes.  Registered kinds:
 * ``stats`` -- drop-in for the reference's StatsSink (:366-393): appends
   ``step,time,field,min,max,mean`` rows; the reductions run on the GPU
   (nkb_stats) with numpy's exact arithmetic, so the rows are byte-identical.
+* ``checkpoint`` -- legacy-VTK checkpoints (:310-324): structured snapshots
+  in the reference's exact STRUCTURED_POINTS layout; SEM snapshots as an
+  UNSTRUCTURED_GRID of the sub-hex mesh with the snapshot's fields plus any
+  AddArray arrays (``arrays="Q,vorticity:mag"``), encoded on the GPU (vtk.py).
 * ``null`` -- counts invocations (:354-363).
-
-The reference's checkpoint sink is outside the hot path
-and is not provided.
 """
 from __future__ import annotations
 
@@ -318,6 +319,45 @@ class StatsSink:
         pass
 
 
+class CheckpointSink:
+    """One legacy-VTK file per block and trigger (sinks.py:310-324)."""
+
+    def __init__(self, params: dict[str, str], comm=None):
+        self.dir = Path(params.get("dir", "checkpoint_out"))
+        self.format = params.get("format", "binary")
+        if self.format not in ("ascii", "binary"):
+            raise ValueError(f"checkpoint format must be ascii or binary, got {self.format!r}")
+        self.extra = [a.strip() for a in params.get("arrays", "").split(",") if a.strip()]
+        self.comm = comm
+        self.dir.mkdir(parents=True, exist_ok=True)
+        _probe_writable(self.dir)
+        self._adaptor: SemDataAdaptor | None = None
+        self._writer = None
+
+    def consume(self, s) -> int:
+        from .vtk import SemVtkWriter, checkpoint_filename, checkpoint_write
+
+        blocks = list(s.blocks)
+        if not (blocks and isinstance(blocks[0], SemBlock)):
+            _, total = checkpoint_write(s, self.dir, self.format)
+            return total
+        if self.format != "binary":
+            raise ValueError("SEM checkpoints are written in binary only")
+        if self._adaptor is None:
+            ctx = self.comm.ctx if self.comm is not None else default_context()
+            self._adaptor = SemDataAdaptor(ctx)
+            self._writer = SemVtkWriter(ctx)
+        self._adaptor.initialize(s)
+        arrays = list(dict.fromkeys([f.name for f in blocks[0].fields] + self.extra))
+        data = self._writer.encode(self._adaptor, arrays, s.step, s.producer_id, s.time)
+        with open(self.dir / checkpoint_filename(s.step, s.producer_id), "wb") as f:
+            f.write(data)
+        return len(data)
+
+    def finalize(self):
+        pass
+
+
 class NullSink:
     def __init__(self, params: dict[str, str] | None = None, comm=None):
         self.count = 0
@@ -334,6 +374,7 @@ _SINK_TYPES = {
     "render": RenderSink,
     "insitu": InsituSink,
     "stats": StatsSink,
+    "checkpoint": CheckpointSink,
     "null": NullSink,
 }
 

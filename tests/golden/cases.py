@@ -43,3 +43,32 @@ RENDER_CASES = [
     (9, 30, 20, 1, 2, 2, "temperature", 256, 256, None, None),
     (10, 6, 6, 1, 1, 2, "temperature", 13, 7, 2.0, 2.0),
 ]
+
+
+def cell_count(ni, nj, nk):
+    """Block.cell_count (reference data_model.py:83-86): a flat axis counts 1."""
+    return max(ni - 1, 1) * max(nj - 1, 1) * max(nk - 1, 1)
+
+
+CHECKPOINT_CASES = [
+    # (seed, ni, nj, nk, nblocks, comps, with_cell_field, fmt, step, producer, time)
+    (21, 6, 5, 1, 1, 2, False, "binary", 0, 0, 0.0),
+    (22, 6, 5, 1, 1, 3, True, "binary", 17, 3, 0.1 + 0.2),
+    (23, 4, 3, 2, 3, 2, True, "binary", 400, 1, 12.5),
+    (24, 5, 4, 1, 2, 2, True, "ascii", 9, 2, 1.0 / 3.0),
+    (25, 1, 1, 1, 1, 1, False, "ascii", 1, 0, -2.0),
+]
+
+
+def checkpoint_arrays(seed, ni, nj, nk, nblocks, comps, with_cell):
+    """Per block: (temperature, velocity AoS, pressure cell field or None, extents)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for b in range(nblocks):
+        npts = ni * nj * nk
+        temp = rng.standard_normal(npts) * 10.0 ** rng.integers(-5, 6, npts)
+        vel = rng.standard_normal(comps * npts)
+        pres = rng.standard_normal(cell_count(ni, nj, nk)) if with_cell else None
+        o = b * ni
+        out.append((temp, vel, pres, (o, o + ni - 1, 0, nj - 1, 0, nk - 1)))
+    return out

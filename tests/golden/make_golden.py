@@ -12,6 +12,8 @@ Fixtures (tests/golden/*.npz):
                  data_model.py:188-225), explicit ranges, degenerate range,
                  odd sizes, 1-pixel images, 3D (nk > 1) blocks
   ppm.npz        write_ppm byte streams (sinks.py:298-303)
+  checkpoint.npz checkpoint_write files (sinks.py:60-102): binary and ascii,
+                 point + cell fields, 1..3 blocks, title line round-trip values
 """
 from __future__ import annotations
 
@@ -25,11 +27,11 @@ REF = "/root/reference/pkg/src"
 if REF not in sys.path:
     sys.path.insert(0, REF)
 
-from nekmini.data_model import POINT, Block, FieldArray, Snapshot  # noqa: E402
-from nekmini.sinks import DEFAULT_COLORMAP, ImageRGB, render, write_ppm  # noqa: E402
+from nekmini.data_model import CELL, POINT, Block, FieldArray, Snapshot  # noqa: E402
+from nekmini.sinks import DEFAULT_COLORMAP, ImageRGB, checkpoint_write, render, write_ppm  # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from cases import RENDER_CASES, colormap_samples, snapshot_arrays  # noqa: E402
+from cases import CHECKPOINT_CASES, RENDER_CASES, checkpoint_arrays, colormap_samples, snapshot_arrays  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -66,6 +68,23 @@ def main():
             assert n == len(raw)
             ppms[f"ppm_{w}x{h}"] = np.frombuffer(raw, np.uint8).copy()
     np.savez_compressed(os.path.join(HERE, "ppm.npz"), **ppms)
+
+    with tempfile.TemporaryDirectory() as d:
+        files = {}
+        for case in CHECKPOINT_CASES:
+            seed, ni, nj, nk, nb, comps, cellf, fmt, step, prod, tm = case
+            blocks = []
+            for temp, vel, pres, ext in checkpoint_arrays(seed, ni, nj, nk, nb, comps, cellf):
+                fields = [FieldArray("temperature", POINT, 1, temp), FieldArray("velocity", POINT, comps, vel)]
+                if pres is not None:
+                    fields.append(FieldArray("pressure", CELL, 1, pres))
+                blocks.append(Block((ext[0] * 0.5, -1.25, 1e-3), (0.5, 0.25, 1.0 / 3.0), ext, tuple(fields)))
+            paths, total = checkpoint_write(Snapshot(tm, step, prod, tuple(blocks)), d, fmt)
+            assert total == sum(os.path.getsize(p) for p in paths)
+            for bi, p in enumerate(paths):
+                files[f"case{seed}_b{bi}"] = np.frombuffer(open(p, "rb").read(), np.uint8).copy()
+                files[f"case{seed}_b{bi}_name"] = np.array(os.path.basename(p))
+        np.savez_compressed(os.path.join(HERE, "checkpoint.npz"), **files)
     print("golden fixtures written to", HERE)
 
 
