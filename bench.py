@@ -346,6 +346,8 @@ def run_ours(a):
         "gpu_launches": 5 * a.steps,
         "clocks": clk,
     }
+    if world == 1:
+        out["next_rows"] = next_rows(ctx, da, case, hcase, peaks["hbm_gbs"])
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(hcase if hcase is not None else case.to_host(), pipe, an.view_for(da), a)
     if rank == 0:
@@ -354,6 +356,51 @@ def run_ours(a):
         comm.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def next_rows(ctx, da, case, hcase, hbm_gbs):
+    """SURVEY.md §8f rows built after the hot path, measured on the same
+    partition: the stats sink (nkb_stats, numpy-exact min/max/mean of every
+    field) and the GPU checkpoint encoder (legacy-VTK sections).  Device
+    time per call (synchronous ABI calls, wall clock around them) against the
+    HBM roofline; numpy on the host copy of the same values beside it."""
+    import time as _t
+
+    import numpy as np
+
+    from paper_2312_09888_b200.vtk import SemVtkWriter
+
+    res = {}
+    names = list(case.fields)
+    segs = {n: [da.field_segment(n)] for n in names}
+    nbytes = sum(8 * case.fields[n].shape[0] * case.n_points for n in names)
+    for n in names:
+        ctx.stats(segs[n])                                   # warm-up (plan + shapes)
+    reps = 5
+    t0 = _t.perf_counter()
+    for _ in range(reps):
+        got = {n: ctx.stats(segs[n]) for n in names}
+    dt = (_t.perf_counter() - t0) / reps
+    row = {"fields": names, "bytes": nbytes, "ms": dt * 1e3, "gb_per_s": nbytes / dt / 1e9,
+           "frac_of_hbm": nbytes / dt / 1e9 / hbm_gbs}
+    if hcase is not None:
+        aos = {n: np.ascontiguousarray(hcase.fields[n].T).ravel() for n in names}
+        t0 = _t.perf_counter()
+        ref = {n: (v.min(), v.max(), v.mean()) for n, v in aos.items()}
+        row["numpy_ms"] = (_t.perf_counter() - t0) * 1e3
+        row["bit_exact_vs_numpy"] = all(
+            np.array_equal(np.array(got[n]).view(np.uint64), np.array(ref[n]).view(np.uint64)) for n in names)
+    res["stats_sink"] = row
+    w = SemVtkWriter(ctx)
+    arrays = names + ["Q"]
+    w.encode(da, arrays, 0, 0, 0.0)
+    t0 = _t.perf_counter()
+    data = w.encode(da, arrays, 0, 0, 0.0)
+    dt = _t.perf_counter() - t0
+    res["checkpoint_encode"] = {"arrays": arrays, "file_bytes": len(data), "ms": dt * 1e3,
+                                "gb_per_s": len(data) / dt / 1e9,
+                                "path": "GPU big-endian encode -> D2H into pinned host (file write not timed)"}
+    return res
 
 
 def _cores() -> int:

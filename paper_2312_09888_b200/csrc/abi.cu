@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -104,6 +105,50 @@ int launch_bounds_kernel(const double* x, const double* y, const double* z, int6
 
 using namespace nkb;
 
+// device copies of one pairwise plan (tables for the chunks this rank owns)
+struct StatsTables {
+  std::vector<PlanChunk> plan;
+  std::vector<StatChunk> mine;                 // owned chunks, local offsets
+  std::vector<int> mine_idx;                   // their plan indices
+  std::vector<int> owned_count;                // per rank
+  std::vector<StatShapeHost> shapes;
+  std::map<long long, int> shape_of_len;
+  StatChunk* d_chunks = nullptr;
+  StatShape* d_shapes = nullptr;
+  int2* d_leaves = nullptr;
+  int2* d_nodes = nullptr;
+  int* d_levels = nullptr;
+  double* d_out = nullptr;                     // sums [n] + mm [3n]
+  int n_dev = 0;
+};
+
+static int shape_id(StatsTables& T, long long len) {
+  auto it = T.shape_of_len.find(len);
+  if (it != T.shape_of_len.end()) return it->second;
+  StatShapeHost sh;
+  pairwise_shape(len, sh);
+  if ((int)sh.leaves.size() > kMaxChunkLeaves) return -1;
+  T.shapes.push_back(std::move(sh));
+  const int id = (int)T.shapes.size() - 1;
+  T.shape_of_len[len] = id;
+  return id;
+}
+
+static void stats_tables_free(StatsTables& T) {
+  cudaFree(T.d_chunks);
+  cudaFree(T.d_shapes);
+  cudaFree(T.d_leaves);
+  cudaFree(T.d_nodes);
+  cudaFree(T.d_levels);
+  cudaFree(T.d_out);
+  T.d_chunks = nullptr;
+  T.d_shapes = nullptr;
+  T.d_leaves = nullptr;
+  T.d_nodes = nullptr;
+  T.d_levels = nullptr;
+  T.d_out = nullptr;
+}
+
 struct nkb_ctx {
   int device = 0;
   // mesh (borrowed)
@@ -160,6 +205,7 @@ struct nkb_ctx {
   bool geo_used = false;                     // last step used it
   bool geo_built = false;                    // last step (re)built it
   unsigned long long* prof = nullptr;        // debug phase profile (NKB_PROFILE_PHASES=1)
+  std::map<std::vector<long long>, std::unique_ptr<StatsTables>> stats_cache;   // nkb_stats plans
   // P2P composite state (composite.cu)
   struct {
     bool ready = false, unavailable = false;
@@ -332,6 +378,8 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->range_dev);
   cudaFree(ctx->geo);
   cudaFree(ctx->prof);
+  for (auto& kv : ctx->stats_cache)
+    if (kv.second) stats_tables_free(*kv.second);
   cudaFree(ctx->rgb_dev);
   cudaFreeHost(ctx->h_ppm);
   cudaFree(ctx->s_ptrs);
@@ -538,48 +586,15 @@ int nkb_mesh_bounds(nkb_ctx* ctx, double* out6, void* stream) {
 
 // ---- field statistics (stats sink) --------------------------------------------
 
-// device copies of one pairwise plan (tables for the chunks this rank owns)
-struct StatsTables {
-  std::vector<PlanChunk> plan;
-  std::vector<StatChunk> mine;                 // owned chunks, local offsets
-  std::vector<int> mine_idx;                   // their plan indices
-  std::vector<int> owned_count;                // per rank
-  std::vector<StatShapeHost> shapes;
-  std::map<long long, int> shape_of_len;
-  StatChunk* d_chunks = nullptr;
-  StatShape* d_shapes = nullptr;
-  int2* d_leaves = nullptr;
-  int2* d_nodes = nullptr;
-  int* d_levels = nullptr;
-  double* d_out = nullptr;                     // sums [n] + mm [3n]
-  int n_dev = 0;
-};
-
-static int shape_id(StatsTables& T, long long len) {
-  auto it = T.shape_of_len.find(len);
-  if (it != T.shape_of_len.end()) return it->second;
-  StatShapeHost sh;
-  pairwise_shape(len, sh);
-  if ((int)sh.leaves.size() > kMaxChunkLeaves) return -1;
-  T.shapes.push_back(std::move(sh));
-  const int id = (int)T.shapes.size() - 1;
-  T.shape_of_len[len] = id;
-  return id;
-}
-
-static void stats_tables_free(StatsTables& T) {
-  cudaFree(T.d_chunks);
-  cudaFree(T.d_shapes);
-  cudaFree(T.d_leaves);
-  cudaFree(T.d_nodes);
-  cudaFree(T.d_levels);
-  cudaFree(T.d_out);
-  T.d_chunks = nullptr;
-  T.d_shapes = nullptr;
-  T.d_leaves = nullptr;
-  T.d_nodes = nullptr;
-  T.d_levels = nullptr;
-  T.d_out = nullptr;
+static void stats_bind(const StatsTables& T, StatsParams& P) {
+  P.chunks = T.d_chunks;
+  P.n_chunks = T.n_dev;
+  P.shapes = T.d_shapes;
+  P.leaves = T.d_leaves;
+  P.nodes = T.d_nodes;
+  P.level_start = T.d_levels;
+  P.out_sum = T.d_out;
+  P.out_mm = T.d_out + std::max(T.n_dev, 1);
 }
 
 // upload chunk list + shape tables; returns the kernel parameters
@@ -616,14 +631,7 @@ static int stats_upload(StatsTables& T, const std::vector<StatChunk>& chunks, St
   NKB_CUDA(cudaMemcpy(T.d_nodes, nd.data(), sizeof(int2) * nd.size(), cudaMemcpyHostToDevice));
   NKB_CUDA(cudaMemcpy(T.d_levels, ls.data(), sizeof(int) * ls.size(), cudaMemcpyHostToDevice));
   T.n_dev = n;
-  P.chunks = T.d_chunks;
-  P.n_chunks = n;
-  P.shapes = T.d_shapes;
-  P.leaves = T.d_leaves;
-  P.nodes = T.d_nodes;
-  P.level_start = T.d_levels;
-  P.out_sum = T.d_out;
-  P.out_mm = T.d_out + std::max(n, 1);
+  stats_bind(T, P);
   return NKB_OK;
 }
 
@@ -671,17 +679,36 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
   const long long N = lo[R];
   if (N == 0) return fail(NKB_EINVAL, "zero-size array to reduction operation minimum which has no identity");
 
-  StatsTables T;
-  pairwise_plan(N, lo, T.plan);
-  const int nc = (int)T.plan.size();
-  T.owned_count.assign(R, 0);
+  // the plan and its device tables depend only on the rank layout: cached
+  auto key = lo;
+  key.push_back(me);
+  auto& slot = ctx->stats_cache[key];
+  const bool fresh = !slot;
+  if (fresh) {
+    if (ctx->stats_cache.size() > 32) {           // bounded: drop the others
+      for (auto& kv : ctx->stats_cache)
+        if (kv.second && kv.first != key) stats_tables_free(*kv.second);
+      auto keep = std::move(slot);
+      ctx->stats_cache.clear();
+      ctx->stats_cache[key] = std::move(keep);
+    }
+    ctx->stats_cache[key].reset(new StatsTables());
+  }
+  StatsTables& T = *ctx->stats_cache[key];
   std::vector<int> boundary;
+  const int nc_plan = fresh ? -1 : (int)T.plan.size();
+  if (fresh) {
+    pairwise_plan(N, lo, T.plan);
+    T.owned_count.assign(R, 0);
+  }
+  const int nc = (int)T.plan.size();
   for (int i = 0; i < nc; ++i) {
     const PlanChunk& c = T.plan[i];
     if (c.owner < 0) {
       boundary.push_back(i);
       continue;
     }
+    if (!fresh) continue;
     ++T.owned_count[c.owner];
     if (c.owner == me) {
       const int sid = shape_id(T, c.n);
@@ -690,12 +717,14 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
       T.mine_idx.push_back(i);
     }
   }
+  (void)nc_plan;
   std::vector<double> sums(nc, 0.0);
   double mn = INFINITY, mx = -INFINITY;
   bool nan = false;
-  auto run = [&](const std::vector<StatChunk>& chunks, StatsParams& Q, std::vector<double>& hs,
-                 std::vector<double>& hm) -> int {
-    NKB_TRY(stats_upload(T, chunks, Q));
+  auto run = [&](StatsTables& TT, const std::vector<StatChunk>& chunks, bool upload, StatsParams& Q,
+                 std::vector<double>& hs, std::vector<double>& hm) -> int {
+    if (upload) NKB_TRY(stats_upload(TT, chunks, Q));
+    else stats_bind(TT, Q);
     NKB_TRY(launch_pairwise_chunks(Q, s));
     const int m = (int)chunks.size();
     hs.resize(m);
@@ -708,7 +737,7 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
     return NKB_OK;
   };
   std::vector<double> hs, hm;
-  NKB_TRY(run(T.mine, P, hs, hm));
+  NKB_TRY(run(T, T.mine, fresh, P, hs, hm));
   double lmn = INFINITY, lmx = -INFINITY, lnan = 0.0;
   for (size_t k = 0; k < T.mine.size(); ++k) {
     lmn = fmin(lmn, hm[3 * k]);
@@ -763,11 +792,10 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
       // summed on the GPU like any other chunk (every rank, same result)
       std::vector<double> vals;
       std::vector<StatChunk> bch;
-      T.shapes.clear();
-      T.shape_of_len.clear();
+      StatsTables TB;
       for (int i : boundary) {
         const PlanChunk& c = T.plan[i];
-        bch.push_back({(long long)vals.size(), shape_id(T, c.n)});
+        bch.push_back({(long long)vals.size(), shape_id(TB, c.n)});
         for (long long g = c.off; g < c.off + c.n; ++g) {
           const int r = (int)(std::upper_bound(lo.begin(), lo.end(), g) - lo.begin()) - 1;
           const long long l = g - lo[r], nr = lo[r + 1] - lo[r];
@@ -784,8 +812,9 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
       B.seg[0] = {dv, (long long)vals.size(), 1, (long long)vals.size(), 0};
       B.n = (long long)vals.size();
       std::vector<double> bs, bm;
-      const int rc = run(bch, B, bs, bm);
+      const int rc = run(TB, bch, true, B, bs, bm);
       cudaFree(dv);
+      stats_tables_free(TB);
       NKB_TRY(rc);
       for (size_t k = 0; k < boundary.size(); ++k) {
         sums[boundary[k]] = bs[k];
@@ -795,7 +824,6 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
       }
     }
   }
-  stats_tables_free(T);
   const double total = 0.0 + pairwise_combine(N, lo, sums);      // np.add.reduce: identity + pairwise
   out[0] = nan ? NAN : mn;
   out[1] = nan ? NAN : mx;

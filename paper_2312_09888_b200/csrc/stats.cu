@@ -70,39 +70,81 @@ struct MinMax {
   }
 };
 
-__device__ double leaf_sum(Walker& w, int n, MinMax& m) {
+// AoS value i through the segment table (slow path: leaves across segments)
+__device__ double value_at(const StatsParams& p, long long i) {
+  int s = 0;
+  while (s + 1 < p.nseg && i >= p.seg[s + 1].start) ++s;
+  const long long r = i - p.seg[s].start;
+  const int nc = p.seg[s].ncomp;
+  const long long j = r / nc;
+  return p.seg[s].base[(long long)(r - j * nc) * p.seg[s].comp_stride + j];
+}
+
+// One leaf (57..128 values, or < 8 for a tiny root) summed by an OCTET of
+// lanes: lane q owns numpy's accumulator r[q] (values q, q+8, q+16, ... in
+// order), the octet then folds ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) with
+// shuffles and lane 0 adds the n%8 tail.  Adjacent octets hold adjacent
+// leaves, so a warp reads 4 x 64 contiguous bytes per step.
+__device__ double octet_leaf(const StatsParams& p, long long off, int n, int q, unsigned mask, MinMax& m) {
+  // locate (segment, tuple, component) of value off + q once; advance by 8
+  int s = 0;
+  while (s + 1 < p.nseg && off >= p.seg[s + 1].start) ++s;
+  const StatSeg& g = p.seg[s];
+  const bool one_seg = off + n <= g.start + g.n_tuples * g.ncomp;
+  const int nc = g.ncomp, dj = 8 / nc, dc = 8 % nc;
+  const long long r0 = off + q - g.start;
+  long long j = r0 / nc;
+  int c = (int)(r0 - j * nc);
+  auto get = [&](long long i) -> double {          // i = offset of this lane's value in the leaf
+    if (one_seg) {
+      const double v = g.base[(long long)c * g.comp_stride + j];
+      j += dj;
+      c += dc;
+      if (c >= nc) {
+        c -= nc;
+        ++j;
+      }
+      return v;
+    }
+    return value_at(p, off + i);
+  };
+  double res;
   if (n < 8) {
-    double r = -0.0;
-    for (int i = 0; i < n; ++i) {
-      const double v = w.next();
-      m.add(v);
-      r = __dadd_rn(r, v);
-    }
-    return r;
+    res = -0.0;
+    if (q == 0)
+      for (int i = 0; i < n; ++i) {
+        const double v = value_at(p, off + i);
+        m.add(v);
+        res = __dadd_rn(res, v);
+      }
+    return res;
   }
-  double r[8];
+  const int lim = n - (n % 8), steps = lim / 8;   // <= 16
+  double v[16];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    r[q] = w.next();
-    m.add(r[q]);
-  }
-  int i = 8;
-  const int lim = n - (n % 8);
-  for (; i < lim; i += 8) {
+  for (int k = 0; k < 16; ++k)                     // all loads first: 16 in flight per lane
+    if (k < steps) v[k] = get(8 * k + q);
+  double r = v[0];
+  m.add(r);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const double v = w.next();
-      m.add(v);
-      r[q] = __dadd_rn(r[q], v);
+  for (int k = 1; k < 16; ++k)
+    if (k < steps) {
+      m.add(v[k]);
+      r = __dadd_rn(r, v[k]);
     }
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) {
-    const double v = w.next();
-    m.add(v);
-    res = __dadd_rn(res, v);
-  }
+  // fold in numpy's order: pairs, then quads, then the halves
+  double o = __shfl_down_sync(mask, r, 1, 8);
+  r = __dadd_rn(r, o);                             // lanes 0,2,4,6: r[q] + r[q+1]
+  o = __shfl_down_sync(mask, r, 2, 8);
+  r = __dadd_rn(r, o);                             // lanes 0,4
+  o = __shfl_down_sync(mask, r, 4, 8);
+  res = __dadd_rn(r, o);                           // lane 0
+  if (q == 0)
+    for (int i = lim; i < n; ++i) {
+      const double v = value_at(p, off + i);
+      m.add(v);
+      res = __dadd_rn(res, v);
+    }
   return res;
 }
 
@@ -116,11 +158,15 @@ __global__ void __launch_bounds__(kStatThreads) pairwise_chunk_kernel(const Stat
     const StatShape S = p.shapes[C.shape];
     if (tid == 0) s_nan = 0;
     MinMax m;
-    for (int l = tid; l < S.n_leaves; l += kStatThreads) {
-      const int2 lf = p.leaves[S.leaf0 + l];           // (offset in chunk, length)
-      Walker w{&p, 0, 0, 0};
-      w.seek(C.off + lf.x);
-      val[l] = leaf_sum(w, lf.y, m);
+    const int oct = tid >> 3, q = tid & 7;
+    const unsigned mask = 0xffu << (tid & 24);        // my octet's lanes
+    for (int l0 = 0; l0 < S.n_leaves; l0 += kStatThreads / 8) {
+      const int l = l0 + oct;
+      if (l < S.n_leaves) {                          // whole octets take the branch together
+        const int2 lf = p.leaves[S.leaf0 + l];         // (offset in chunk, length)
+        const double v = octet_leaf(p, C.off + lf.x, lf.y, q, mask, m);
+        if (q == 0) val[l] = v;
+      }
     }
     __syncthreads();
     for (int lv = 0; lv < S.n_levels; ++lv) {
