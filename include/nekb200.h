@@ -96,6 +96,9 @@ typedef struct {
     int          emit_meta;                        /* 1: record per-triangle (element, cell, surface, case) */
     int          composite;                        /* 1: depth-composite across the comm (nkb_comm_init) */
     int          timing;                           /* 1: fill per-stage CUDA-event times in nkb_report */
+    int          continuous;                       /* 1: DSSUM-average derived sources (Q, vorticity:mag)
+                                                      before surfaces / colour (C0 across element faces);
+                                                      needs nkb_mesh_set_global_ids */
 } nkb_pipeline;
 
 typedef struct {
@@ -145,6 +148,16 @@ int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order,
  * with the same pointers, sizes and offsets keeps the cache (static mesh);
  * after editing coordinates in place (moving mesh) call nkb_mesh_modified.
  * nkb_set_geometry_cache(ctx, 0) disables it (default on; env NKB_GEOM_CACHE=0). */
+/* Global GLL node ids (NekRS mesh->globalIds), DEVICE int64[E*(N+1)^3],
+ * read during the call: builds the gather-scatter of nkb_dssum.  Collective
+ * when a communicator is initialised (finds the ids shared with other ranks).
+ * Dropped by nkb_mesh_set with a different mesh.  SURVEY.md §8f row 1. */
+int nkb_mesh_set_global_ids(nkb_ctx* ctx, const int64_t* gid, void* stream);
+/* Direct stiffness average, in place, of a DEVICE point field (E*(N+1)^3
+ * doubles): every copy of a global node gets
+ *   ((P_r0 + P_r1) + ...) / count,  P_r = sum of rank r's copies in
+ * increasing local index order (ranks in increasing order).  Collective. */
+int nkb_dssum(nkb_ctx* ctx, double* field, void* stream);
 int nkb_mesh_modified(nkb_ctx* ctx);
 int nkb_set_geometry_cache(nkb_ctx* ctx, int enable);
 /* register (or re-point) a device-resident point field, borrowed.

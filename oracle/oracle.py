@@ -268,3 +268,42 @@ def derived_numpy(x, y, z, u, v, w, D=None):
     umag = np.sqrt(np.asarray(u) ** 2 + np.asarray(v) ** 2 + np.asarray(w) ** 2)
     gradnorm2 = np.sum(A * A, axis=(1, 2))
     return Q, vort, umag.ravel(), gradnorm2
+
+
+def dssum(gid: np.ndarray, vals: np.ndarray, rank_lo=None) -> np.ndarray:
+    """Direct stiffness average (test oracle for nkb_dssum, dssum.cu header).
+
+    gid/vals: global arrays in rank order; rank_lo: first global index of
+    every rank (default: one rank).  For a global id with copies on ranks
+    r0 < r1 < ...: P_r = left fold of rank r's copies in increasing index,
+    total = ((P_r0 + P_r1) + ...), and every copy becomes total / count.
+    Plain float64 numpy arithmetic (IEEE, no FMA), vectorised over ids."""
+    gid = np.asarray(gid, dtype=np.int64)
+    v = np.asarray(vals, dtype=np.float64)
+    n = v.size
+    rank = np.zeros(n, np.int64) if rank_lo is None else np.searchsorted(np.asarray(rank_lo), np.arange(n), "right") - 1
+    order = np.argsort(gid, kind="stable")                 # copies of an id in increasing global index
+    g = gid[order]
+    start = np.flatnonzero(np.r_[True, g[1:] != g[:-1]])
+    count = np.diff(np.r_[start, n])
+    part = v[order[start]].copy()                          # running partial of the current rank
+    prank = rank[order[start]].copy()
+    total = np.zeros_like(part)
+    have = np.zeros(part.size, bool)
+    for k in range(1, int(count.max())):
+        live = count > k
+        idx = order[start[live] + k]
+        same = rank[idx] == prank[live]
+        li = np.flatnonzero(live)
+        a = li[same]                                       # same rank: extend the partial
+        part[a] = part[a] + v[idx[same]]
+        b = li[~same]                                      # next rank: close the partial
+        total[b] = np.where(have[b], total[b] + part[b], part[b])
+        have[b] = True
+        part[b] = v[idx[~same]]
+        prank[b] = rank[idx[~same]]
+    total = np.where(have, total + part, part)
+    avg = total / count
+    out = np.empty_like(v)
+    out[order] = np.repeat(avg, count)
+    return out

@@ -54,6 +54,7 @@ class NkbPipeline(C.Structure):
         ("emit_meta", C.c_int),
         ("composite", C.c_int),
         ("timing", C.c_int),
+        ("continuous", C.c_int),
     ]
 
 
@@ -123,6 +124,8 @@ _SIGS = {
     "nkb_image_ppm": ([_vp, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), _vp], C.c_int),
     "nkb_stats": ([_vp, C.POINTER(NkbSegment), C.c_int, C.c_int, C.POINTER(C.c_double), _vp], C.c_int),
     "nkb_encode_be": ([_vp, C.c_char_p, _vp, _i64, C.POINTER(C.c_int64), _vp], C.c_int),
+    "nkb_mesh_set_global_ids": ([_vp, _vp, _vp], C.c_int),
+    "nkb_dssum": ([_vp, _vp, _vp], C.c_int),
     "nkb_triangles_device": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)], C.c_int),
     "nkb_nccl_unique_id": ([_vp], C.c_int),
     "nkb_comm_init": ([_vp, _vp, C.c_int, C.c_int], C.c_int),

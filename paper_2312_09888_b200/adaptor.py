@@ -54,6 +54,7 @@ class SemDataAdaptor:
         self._staging: dict[str, DeviceArray] = {}
         self._fields: dict[str, FieldArray] = {}
         self._coords = None
+        self._gid = None
         self._segments: dict[str, tuple[int, int, int]] = {}   # name -> (ptr, ncomp, comp_stride)
         self.time = 0.0
         self.step = 0
@@ -89,6 +90,25 @@ class SemDataAdaptor:
         if not static and not all(is_device_array(a) for a in coords):
             self.ctx.mesh_modified()
         self._coords = coords
+        gid = b.global_ids
+        if gid is None:
+            self._gid = None
+        elif not (static and gid is self._gid):
+            # global node ids: the DSSUM gather-scatter (nkb_mesh_set_global_ids)
+            if is_device_array(gid):
+                dg = gid
+            else:
+                a = np.ascontiguousarray(gid, dtype=np.int64).ravel()
+                if a.size != npts:
+                    raise ValueError(f"global_ids: expected {npts} ids, got {a.size}")
+                dg = self._staging.get("__gid")
+                if dg is None or dg.size != a.size:
+                    dg = DeviceArray.empty(self.ctx, (a.size,), np.int64)
+                    self._staging["__gid"] = dg
+                dg.upload(a, sync=False)
+                self.h2d_bytes += a.nbytes
+            self.ctx.mesh_set_global_ids(dg)
+            self._gid = gid
         self.ctx.field_clear()
         self._fields = {}
         self._segments = {}

@@ -52,6 +52,7 @@ class Pipeline:
     background: tuple[int, int, int, int] = (0, 0, 0, 0)
     emit_meta: bool = False
     composite: bool = True
+    continuous: bool = False      # DSSUM-average Q / vorticity:mag first (needs SemBlock.global_ids)
     timing: bool = False
 
     def native(self, view: tuple[float, ...]) -> N.NkbPipeline:
@@ -89,6 +90,7 @@ class Pipeline:
             p.background[c] = int(self.background[c])
         p.emit_meta = int(self.emit_meta)
         p.composite = int(self.composite)
+        p.continuous = int(self.continuous)
         p.timing = int(self.timing)
         return p
 
@@ -164,6 +166,7 @@ def pipeline_from_params(params: dict[str, str]) -> Pipeline:
         vmin=float(params["vmin"]) if "vmin" in params else None,
         vmax=float(params["vmax"]) if "vmax" in params else None,
         composite=params.get("composite", "1") not in ("0", "false", "no"),
+        continuous=params.get("continuous", "0") in ("1", "true", "yes"),
     )
 
 

@@ -34,7 +34,7 @@ log = logging.getLogger(__name__)
 _ATTRS_BY_KIND: dict[str, frozenset[str]] = {
     "render": frozenset({"dir", "width", "height", "field", "vmin", "vmax"}),
     "insitu": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
-                         "velocity", "composite"}),
+                         "velocity", "composite", "continuous"}),
     "stats": frozenset({"path"}),
     "checkpoint": frozenset({"dir", "format", "arrays"}),
     "null": frozenset(),

@@ -80,6 +80,15 @@ class Context:
         N.call("nkb_mesh_set", self.handle, int(n_elements), int(order), device_ptr(x), device_ptr(y),
                device_ptr(z), int(element_offset), int(n_elements_global))
 
+    def mesh_set_global_ids(self, gid, stream: int = 0) -> None:
+        """Global node ids (device int64, one per GLL copy): builds the DSSUM
+        gather-scatter (collective with a communicator)."""
+        N.call("nkb_mesh_set_global_ids", self.handle, device_ptr(gid), stream or None)
+
+    def dssum(self, field, stream: int = 0) -> None:
+        """In-place direct stiffness average of a device point field."""
+        N.call("nkb_dssum", self.handle, device_ptr(field), stream or None)
+
     def mesh_modified(self) -> None:
         """Coordinates were edited in place (moving mesh): drop the geometry cache."""
         N.call("nkb_mesh_modified", self.handle)

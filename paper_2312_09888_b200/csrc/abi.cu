@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <map>
 #include <memory>
 #include <string>
@@ -44,6 +45,8 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -67,6 +70,8 @@ static int load_nccl() {
   NKB_SYM(Reduce, "ncclReduce");
   NKB_SYM(AllReduce, "ncclAllReduce");
   NKB_SYM(AllGather, "ncclAllGather");
+  NKB_SYM(Send, "ncclSend");
+  NKB_SYM(Recv, "ncclRecv");
   NKB_SYM(GroupStart, "ncclGroupStart");
   NKB_SYM(GroupEnd, "ncclGroupEnd");
   NKB_SYM(GetErrorString, "ncclGetErrorString");
@@ -206,6 +211,11 @@ struct nkb_ctx {
   bool geo_built = false;                    // last step (re)built it
   unsigned long long* prof = nullptr;        // debug phase profile (NKB_PROFILE_PHASES=1)
   std::map<std::vector<long long>, std::unique_ptr<StatsTables>> stats_cache;   // nkb_stats plans
+  GsLocal gs;                                // DSSUM gather-scatter plan (nkb_mesh_set_global_ids)
+  bool gs_ready = false;
+  double* dq = nullptr;                      // continuous pipeline: DSSUM'd Q / |w| scratch
+  double* dw = nullptr;
+  int64_t dcap = 0;
   // P2P composite state (composite.cu)
   struct {
     bool ready = false, unavailable = false;
@@ -380,6 +390,9 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->prof);
   for (auto& kv : ctx->stats_cache)
     if (kv.second) stats_tables_free(*kv.second);
+  gs_free(ctx->gs);
+  cudaFree(ctx->dq);
+  cudaFree(ctx->dw);
   cudaFree(ctx->rgb_dev);
   cudaFreeHost(ctx->h_ppm);
   cudaFree(ctx->s_ptrs);
@@ -404,7 +417,10 @@ int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order, const double* x, c
   if (n_elements > 0 && (!x || !y || !z)) return fail(NKB_EINVAL, "null coordinate pointer");
   if (n_elements > (int64_t)0x7fffffff) return fail(NKB_EINVAL, "too many elements for one rank");
   const bool same = ctx->E == n_elements && ctx->N == order && ctx->x == x && ctx->y == y && ctx->z == z;
-  if (!same) ctx->geo_valid = false;       // a different mesh: rebuild the geometry cache on demand
+  if (!same) {
+    ctx->geo_valid = false;                // a different mesh: rebuild the geometry cache on demand
+    ctx->gs_ready = false;                 // ... and the global-id gather-scatter must be set again
+  }
   ctx->E = n_elements;
   ctx->N = order;
   ctx->x = x;
@@ -558,6 +574,208 @@ int nkb_encode_be(nkb_ctx* ctx, const char* what, void* dst, int64_t cap, int64_
   int nc = 0;
   NKB_TRY(nkb_add_array(ctx, what, 0, reinterpret_cast<double*>(dst), &nc, stream));   // AoS f64
   return launch_bswap64(dst, (int64_t)nc * npts, s);
+}
+
+// ---- DSSUM: global node ids and the gather-scatter -----------------------------
+
+int nkb_mesh_set_global_ids(nkb_ctx* ctx, const int64_t* gid, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->x) return fail(NKB_ESTATE, "global ids before mesh_set");
+  const int64_t n = ctx->E * kNN;
+  if (n > 0 && !gid) return fail(NKB_EINVAL, "null global id pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->gs_ready = false;
+  gs_free(ctx->gs);
+  GsLocal& g = ctx->gs;
+  NKB_TRY(gs_build_local(reinterpret_cast<const long long*>(gid), n, g, s));
+  if (g.U > 0) {
+    long long first = 0;
+    NKB_CUDA(cudaMemcpy(&first, g.ugid, sizeof(first), cudaMemcpyDeviceToHost));
+    if (first < 0) return fail(NKB_EINVAL, "global ids must be non-negative");
+  }
+  const int R = (ctx->comm && ctx->nranks > 1) ? ctx->nranks : 1, me = ctx->rank;
+  g.ncount.assign(R, 0);
+  g.noff.assign(R + 1, 0);
+  if (R == 1) {
+    ctx->gs_ready = true;
+    return NKB_OK;
+  }
+  // (1) every unique (gid, local count) to its owner rank gid % R
+  long long* sendb = nullptr;
+  NKB_CUDA(cudaMalloc(&sendb, sizeof(long long) * 2 * std::max<long long>(g.U, 1)));
+  std::vector<int> scount;
+  NKB_TRY(gs_bucket_by_owner(g, R, sendb, scount, s));
+  auto all_counts = [&](const std::vector<int>& mine, std::vector<int>& recv_from) -> int {
+    // recv_from[q] = what rank q sends to me
+    long long* d = nullptr;
+    NKB_CUDA(cudaMalloc(&d, sizeof(long long) * R * (R + 1)));
+    std::vector<long long> m(mine.begin(), mine.end());
+    NKB_CUDA(cudaMemcpy(d + (size_t)R * R, m.data(), sizeof(long long) * R, cudaMemcpyHostToDevice));
+    NKB_NCCL(g_nccl.AllGather(d + (size_t)R * R, d, R, ncclInt64, ctx->comm, s));
+    std::vector<long long> all((size_t)R * R);
+    NKB_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(long long) * R * R, cudaMemcpyDeviceToHost, s));
+    NKB_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d);
+    recv_from.assign(R, 0);
+    for (int q = 0; q < R; ++q) recv_from[q] = (int)all[(size_t)q * R + me];
+    return NKB_OK;
+  };
+  auto alltoallv = [&](const long long* sb, const std::vector<int>& sc, long long* rb, const std::vector<int>& rc,
+                       int width) -> int {
+    size_t so = 0, ro = 0;
+    NKB_NCCL(g_nccl.GroupStart());
+    for (int q = 0; q < R; ++q) {
+      if (sc[q]) NKB_NCCL(g_nccl.Send(sb + so, (size_t)sc[q] * width, ncclInt64, q, ctx->comm, s));
+      if (rc[q]) NKB_NCCL(g_nccl.Recv(rb + ro, (size_t)rc[q] * width, ncclInt64, q, ctx->comm, s));
+      so += (size_t)sc[q] * width;
+      ro += (size_t)rc[q] * width;
+    }
+    NKB_NCCL(g_nccl.GroupEnd());
+    NKB_CUDA(cudaStreamSynchronize(s));
+    return NKB_OK;
+  };
+  std::vector<int> rcount;
+  NKB_TRY(all_counts(scount, rcount));
+  long long nrecv = 0;
+  for (int q = 0; q < R; ++q) nrecv += rcount[q];
+  long long* recvb = nullptr;
+  NKB_CUDA(cudaMalloc(&recvb, sizeof(long long) * 2 * std::max<long long>(nrecv, 1)));
+  NKB_TRY(alltoallv(sendb, scount, recvb, rcount, 2));
+  cudaFree(sendb);
+  // (2) owner: per gid, total copies and the set of ranks (host; setup only)
+  std::vector<long long> rec((size_t)2 * nrecv);
+  if (nrecv) NKB_CUDA(cudaMemcpy(rec.data(), recvb, sizeof(long long) * 2 * nrecv, cudaMemcpyDeviceToHost));
+  cudaFree(recvb);
+  std::vector<std::pair<long long, int>> ent;   // (gid, entry index)
+  ent.reserve(nrecv);
+  std::vector<int> src(nrecv);
+  {
+    long long k = 0;
+    for (int q = 0; q < R; ++q)
+      for (int i = 0; i < rcount[q]; ++i, ++k) {
+        src[k] = q;
+        ent.emplace_back(rec[2 * k], (int)k);
+      }
+  }
+  std::sort(ent.begin(), ent.end());
+  std::vector<std::vector<long long>> reply(R);   // per source rank: (gid, total, mask) triplets
+  for (size_t a = 0; a < ent.size();) {
+    size_t b = a;
+    long long total = 0;
+    unsigned mask = 0;
+    while (b < ent.size() && ent[b].first == ent[a].first) {
+      total += rec[2 * ent[b].second + 1];
+      mask |= 1u << src[ent[b].second];
+      ++b;
+    }
+    if (__builtin_popcount(mask) > 1)
+      for (size_t c = a; c < b; ++c) {
+        auto& r = reply[src[ent[c].second]];
+        r.push_back(ent[a].first);
+        r.push_back(total);
+        r.push_back(mask);
+      }
+    a = b;
+  }
+  // (3) answers back to the ranks that hold each shared gid
+  std::vector<int> rep_count(R), got_count;
+  std::vector<long long> rep_flat;
+  for (int q = 0; q < R; ++q) {
+    rep_count[q] = (int)(reply[q].size() / 3);
+    rep_flat.insert(rep_flat.end(), reply[q].begin(), reply[q].end());
+  }
+  NKB_TRY(all_counts(rep_count, got_count));
+  long long ngot = 0;
+  for (int q = 0; q < R; ++q) ngot += got_count[q];
+  long long *d_rep = nullptr, *d_got = nullptr;
+  NKB_CUDA(cudaMalloc(&d_rep, sizeof(long long) * std::max<size_t>(rep_flat.size(), 1)));
+  NKB_CUDA(cudaMalloc(&d_got, sizeof(long long) * 3 * std::max<long long>(ngot, 1)));
+  if (!rep_flat.empty())
+    NKB_CUDA(cudaMemcpy(d_rep, rep_flat.data(), sizeof(long long) * rep_flat.size(), cudaMemcpyHostToDevice));
+  NKB_TRY(alltoallv(d_rep, rep_count, d_got, got_count, 3));
+  std::vector<long long> got((size_t)3 * ngot);
+  if (ngot) NKB_CUDA(cudaMemcpy(got.data(), d_got, sizeof(long long) * 3 * ngot, cudaMemcpyDeviceToHost));
+  cudaFree(d_rep);
+  cudaFree(d_got);
+  // (4) my shared gids in increasing gid order; neighbour lists; global counts
+  std::vector<std::array<long long, 3>> sh((size_t)ngot);
+  for (long long k = 0; k < ngot; ++k) sh[k] = {got[3 * k], got[3 * k + 1], got[3 * k + 2]};
+  std::sort(sh.begin(), sh.end());
+  std::vector<long long> ug(g.U);
+  if (g.U) NKB_CUDA(cudaMemcpy(ug.data(), g.ugid, sizeof(long long) * g.U, cudaMemcpyDeviceToHost));
+  std::vector<int> mult(g.U);
+  if (g.U) NKB_CUDA(cudaMemcpy(mult.data(), g.mult, sizeof(int) * g.U, cudaMemcpyDeviceToHost));
+  const int ns = (int)sh.size();
+  std::vector<int> su(ns), spos((size_t)ns * R, -1);
+  std::vector<unsigned char> smask(ns);
+  std::vector<std::vector<int>> lists(R);
+  for (int j = 0; j < ns; ++j) {
+    const long long gg = sh[j][0];
+    const auto it = std::lower_bound(ug.begin(), ug.end(), gg);
+    if (it == ug.end() || *it != gg) return fail(NKB_EINVAL, "internal: shared gid not found locally");
+    const int u = (int)(it - ug.begin());
+    su[j] = u;
+    mult[u] = (int)sh[j][1];
+    smask[j] = (unsigned char)sh[j][2];
+    for (int q = 0; q < R; ++q)
+      if (q != me && (sh[j][2] & (1LL << q))) {
+        spos[(size_t)j * R + q] = (int)lists[q].size();
+        lists[q].push_back(u);
+      }
+  }
+  std::vector<int> flat;
+  for (int q = 0; q < R; ++q) {
+    g.noff[q] = (int)flat.size();
+    g.ncount[q] = (int)lists[q].size();
+    flat.insert(flat.end(), lists[q].begin(), lists[q].end());
+  }
+  g.noff[R] = (int)flat.size();
+  g.n_shared = ns;
+  if (g.U) NKB_CUDA(cudaMemcpy(g.mult, mult.data(), sizeof(int) * g.U, cudaMemcpyHostToDevice));
+  const size_t nf = std::max<size_t>(flat.size(), 1);
+  NKB_CUDA(cudaMalloc(&g.su, sizeof(int) * std::max(ns, 1)));
+  NKB_CUDA(cudaMalloc(&g.smask, std::max(ns, 1)));
+  NKB_CUDA(cudaMalloc(&g.spos, sizeof(int) * std::max<size_t>(spos.size(), 1)));
+  NKB_CUDA(cudaMalloc(&g.slist, sizeof(int) * nf));
+  NKB_CUDA(cudaMalloc(&g.sbuf, sizeof(double) * nf));
+  NKB_CUDA(cudaMalloc(&g.rbuf, sizeof(double) * nf));
+  NKB_CUDA(cudaMalloc(&g.rptr, sizeof(double*) * R));
+  if (ns) {
+    NKB_CUDA(cudaMemcpy(g.su, su.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+    NKB_CUDA(cudaMemcpy(g.smask, smask.data(), ns, cudaMemcpyHostToDevice));
+    NKB_CUDA(cudaMemcpy(g.spos, spos.data(), sizeof(int) * spos.size(), cudaMemcpyHostToDevice));
+  }
+  if (!flat.empty()) NKB_CUDA(cudaMemcpy(g.slist, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
+  std::vector<const double*> rp(R);
+  for (int q = 0; q < R; ++q) rp[q] = g.rbuf + g.noff[q];
+  NKB_CUDA(cudaMemcpy(g.rptr, rp.data(), sizeof(double*) * R, cudaMemcpyHostToDevice));
+  ctx->gs_ready = true;
+  return NKB_OK;
+}
+
+static int gs_apply(nkb_ctx* ctx, double* field, cudaStream_t s) {
+  GsLocal& g = ctx->gs;
+  NKB_TRY(gs_sum(g, field, s));
+  const int R = (ctx->comm && ctx->nranks > 1) ? ctx->nranks : 1;
+  if (R > 1 && g.n_shared > 0) {
+    for (int q = 0; q < R; ++q) NKB_TRY(gs_pack(g, q, s));
+    NKB_NCCL(g_nccl.GroupStart());
+    for (int q = 0; q < R; ++q)
+      if (g.ncount[q]) {
+        NKB_NCCL(g_nccl.Send(g.sbuf + g.noff[q], g.ncount[q], ncclFloat64, q, ctx->comm, s));
+        NKB_NCCL(g_nccl.Recv(g.rbuf + g.noff[q], g.ncount[q], ncclFloat64, q, ctx->comm, s));
+      }
+    NKB_NCCL(g_nccl.GroupEnd());
+    NKB_TRY(gs_combine(g, R, ctx->rank, s));
+  }
+  return gs_scatter(g, field, s);
+}
+
+int nkb_dssum(nkb_ctx* ctx, double* field, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->gs_ready) return fail(NKB_ESTATE, "dssum needs nkb_mesh_set_global_ids");
+  if (ctx->E > 0 && !field) return fail(NKB_EINVAL, "null field");
+  return gs_apply(ctx, field, (cudaStream_t)stream);
 }
 
 int nkb_mesh_bounds(nkb_ctx* ctx, double* out6, void* stream) {
@@ -1195,6 +1413,71 @@ static int64_t needed_capacity(nkb_ctx* ctx, bool ordered) {
   return mx * ctx->n_regions;
 }
 
+// Continuous derived fields: compute Q / |w| for every node in one gradient
+// pass, DSSUM-average them, and let the main pass read them as scalar
+// fields (no gradients there).
+static int continuous_prepass(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams& fp, cudaStream_t s) {
+  bool uq = fp.color_src == SRC_Q, uw = fp.color_src == SRC_WMAG;
+  for (int k = 0; k < fp.n_surf; ++k) {
+    uq |= fp.surf_src[k] == SRC_Q;
+    uw |= fp.surf_src[k] == SRC_WMAG;
+  }
+  if (!uq && !uw) return NKB_OK;
+  if (!ctx->gs_ready) return fail(NKB_ESTATE, "continuous derived fields need nkb_mesh_set_global_ids");
+  const int64_t npts = ctx->E * kNN;
+  if (ctx->dcap < npts) {
+    cudaFree(ctx->dq);
+    cudaFree(ctx->dw);
+    ctx->dq = ctx->dw = nullptr;
+    ctx->dcap = 0;
+    NKB_CUDA(cudaMalloc(&ctx->dq, sizeof(double) * std::max<int64_t>(npts, 1)));
+    NKB_CUDA(cudaMalloc(&ctx->dw, sizeof(double) * std::max<int64_t>(npts, 1)));
+    ctx->dcap = npts;
+  }
+  if (npts > 0) {
+    FusedParams fq;
+    NKB_TRY(fused_params_base(ctx, fq));
+    fq.need_grad = 1;
+    fq.need_vel = 1;
+    for (int c = 0; c < 3; ++c) fq.vel[c] = fp.vel[c];
+    fq.need_wmag = uw ? 1 : 0;
+    fq.color_src = -1;
+    fq.n_surf = 0;
+    fq.q_out = uq ? ctx->dq : nullptr;
+    fq.wmag_out = uw ? ctx->dw : nullptr;
+    NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
+    NKB_TRY(geo_attach(ctx, fq, s));
+    NKB_TRY(launch_fused(fq, s));
+  }
+  if (uq) NKB_TRY(gs_apply(ctx, ctx->dq, s));
+  if (uw) NKB_TRY(gs_apply(ctx, ctx->dw, s));
+  // the main pass reads the averaged fields as scalars
+  auto slot = [&](const double* base, int* src) -> int {
+    for (int k = 0; k < fp.n_scalars; ++k)
+      if (fp.scalar[k] == base) {
+        *src = SRC_SCALAR0 + k;
+        return NKB_OK;
+      }
+    if (fp.n_scalars >= kMaxScalars) return fail(NKB_EINVAL, "too many scalar fields for a continuous pipeline");
+    fp.scalar[fp.n_scalars] = base;
+    *src = SRC_SCALAR0 + fp.n_scalars++;
+    return NKB_OK;
+  };
+  int sq = -1, sw = -1;
+  if (uq) NKB_TRY(slot(ctx->dq, &sq));
+  if (uw) NKB_TRY(slot(ctx->dw, &sw));
+  for (int k = 0; k < fp.n_surf; ++k) {
+    if (fp.surf_src[k] == SRC_Q) fp.surf_src[k] = sq;
+    else if (fp.surf_src[k] == SRC_WMAG) fp.surf_src[k] = sw;
+  }
+  if (fp.color_src == SRC_Q) fp.color_src = sq;
+  else if (fp.color_src == SRC_WMAG) fp.color_src = sw;
+  fp.need_grad = 0;
+  fp.need_wmag = 0;
+  if (!fp.need_umag) fp.need_vel = 0;
+  return NKB_OK;
+}
+
 int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stream) {
   NKB_TRY(ctx_check(ctx));
   if (!p) return fail(NKB_EINVAL, "null pipeline");
@@ -1255,6 +1538,7 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   }
   ctx->geo_used = ctx->geo_built = false;
   if (p->timing) NKB_CUDA(cudaEventRecord(ctx->ev[5], s));
+  if (p->continuous) NKB_TRY(continuous_prepass(ctx, p, fp, s));
   NKB_TRY(geo_attach(ctx, fp, s));
   const bool prof = getenv("NKB_PROFILE_PHASES") != nullptr && !ordered;
   if (prof) {

@@ -856,6 +856,8 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   const int slot_sc = k;
   for (int c = 0; c < p.n_scalars; ++c) q.in_ptr[k++] = p.scalar[c];
   const int nin = k;
+  if (nin > kMaxIn) return fail(NKB_EINVAL, "too many staged fields for one pass (coordinates, velocity and "
+                                            "scalars exceed 8)");
   const size_t shm = fused_smem_bytes(nin);
   static bool attr_set = false;
   if (!attr_set) {

@@ -50,7 +50,7 @@ enum Src : int {
   SRC_SCALAR1 = 4,  // loaded scalar field slot 1
   SRC_PLANE = 8,    // plane distance of surface k: SRC_PLANE + k
 };
-constexpr int kMaxScalars = 2;
+constexpr int kMaxScalars = 4;
 
 struct FusedParams {
   int64_t n_elements;
@@ -205,6 +205,33 @@ int launch_be_points(const double* x, const double* y, const double* z, int64_t 
 int launch_be_cells(int64_t ncells, void* out, cudaStream_t s);
 int launch_be_types(int64_t ncells, void* out, cudaStream_t s);
 int launch_bswap64(void* p, int64_t n, cudaStream_t s);
+// ---- dssum.cu: gather-scatter (direct stiffness summation) ----
+struct GsLocal {
+  long long n = 0, U = 0;            // local GLL copies, unique global ids
+  int* idx = nullptr;                // [n] local indices sorted by gid (stable)
+  int* off = nullptr;                // [U+1] CSR runs
+  long long* ugid = nullptr;         // [U] sorted unique gids
+  int* mult = nullptr;               // [U] copies over all ranks
+  double* part = nullptr;            // [U] partial / total sums
+  // shared with other ranks (multi-rank only)
+  int n_shared = 0;
+  int* su = nullptr;                 // [n_shared] unique index of each shared gid (increasing gid)
+  unsigned char* smask = nullptr;    // [n_shared] ranks holding it
+  int* spos = nullptr;               // [n_shared * R] position in rank q's buffer
+  int* slist = nullptr;              // per neighbour q: unique indices to send, at noff[q]
+  double* sbuf = nullptr;            // send buffers (same layout)
+  double* rbuf = nullptr;            // receive buffers (same layout: list lengths match)
+  const double** rptr = nullptr;     // [R] device pointers into rbuf (mine unused)
+  std::vector<int> ncount, noff;     // per neighbour list length / offset (host)
+};
+int gs_build_local(const long long* gid, long long n, GsLocal& g, cudaStream_t s);
+void gs_free(GsLocal& g);
+int gs_sum(const GsLocal& g, const double* v, cudaStream_t s);
+int gs_pack(const GsLocal& g, int q, cudaStream_t s);
+int gs_combine(const GsLocal& g, int R, int me, cudaStream_t s);
+int gs_scatter(const GsLocal& g, double* v, cudaStream_t s);
+int gs_bucket_by_owner(const GsLocal& g, int R, long long* out, std::vector<int>& counts, cudaStream_t s);
+
 int launch_pack_rgb(const unsigned char* rgba, unsigned char* rgb, int64_t npx, cudaStream_t s);
 int launch_points_aos(const double* x, const double* y, const double* z, int64_t npts,
                       double* out, cudaStream_t s);

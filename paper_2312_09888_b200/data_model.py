@@ -157,6 +157,7 @@ class SemBlock:
     fields: tuple[FieldArray, ...] = field(default_factory=tuple)
     element_offset: int = 0
     n_elements_global: int = 0
+    global_ids: object = None     # optional int64 global node ids (NekRS mesh->globalIds): enables DSSUM
 
     def __post_init__(self):
         object.__setattr__(self, "fields", tuple(self.fields))

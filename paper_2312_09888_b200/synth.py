@@ -43,10 +43,17 @@ class SemCase:
     z: np.ndarray
     fields: dict[str, np.ndarray] = field(default_factory=dict)   # name -> (ncomp, npts) SoA
     params: dict[str, str] = field(default_factory=dict)           # insitu sink attributes
+    nel: tuple[int, int, int] | None = None                        # element lattice (global ids)
 
     @property
     def n_points(self) -> int:
         return self.n_elements * NN
+
+    def global_ids(self) -> np.ndarray:
+        """NekRS-style global node ids of this partition (int64, one per GLL copy)."""
+        if self.nel is None:
+            raise ValueError("this case has no element lattice")
+        return lattice_ids(self.nel, self.e0, self.e0 + self.n_elements)
 
 
 def _ref_coords(nel: tuple[int, int, int], e0: int, e1: int):
@@ -63,6 +70,21 @@ def _ref_coords(nel: tuple[int, int, int], e0: int, e1: int):
     shp = (e1 - e0, NP, NP, NP)
     return (np.broadcast_to(X, shp).reshape(-1).copy(), np.broadcast_to(Y, shp).reshape(-1).copy(),
             np.broadcast_to(Z, shp).reshape(-1).copy())
+
+
+def lattice_ids(nel: tuple[int, int, int], e0: int, e1: int) -> np.ndarray:
+    """Global node ids on the (7 nx + 1) x (7 ny + 1) x (7 nz + 1) lattice of a
+    structured element grid: copies of a node on shared faces, edges and
+    corners get the same id."""
+    nx, ny, nz = nel
+    e = np.arange(e0, e1)
+    ex, ey, ez = e % nx, (e // nx) % ny, e // (nx * ny)
+    i = np.arange(NP)
+    gx = (7 * ex)[:, None, None, None] + i[None, None, None, :]
+    gy = (7 * ey)[:, None, None, None] + i[None, None, :, None]
+    gz = (7 * ez)[:, None, None, None] + i[None, :, None, None]
+    lx, ly = 7 * nx + 1, 7 * ny + 1
+    return (gx + lx * (gy + ly * gz)).astype(np.int64).reshape(-1)
 
 
 def partition(n_global: int, rank: int, nranks: int) -> tuple[int, int]:
@@ -87,7 +109,7 @@ def taylor_green(e0: int = 0, e1: int | None = None, n: int = 8) -> SemCase:
     p = (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0) / 16.0
     return SemCase("c1", e1 - e0, e0, E, x, y, z,
                    {"velocity": np.stack([u, v, w]), "pressure": p[None]},
-                   {"iso": "Q=0.1", "field": "velocity:mag", "view": "35,30"})
+                   {"iso": "Q=0.1", "field": "velocity:mag", "view": "35,30"}, nel=(n, n, n))
 
 
 def rbc_cylinder(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (32, 32, 32),
@@ -116,7 +138,7 @@ def rbc_cylinder(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] =
     return SemCase("c2", e1 - e0, e0, E, x, y, z,
                    {"velocity": np.stack(vel), "temperature": T[None]},
                    {"iso": "temperature=0.5;Q=1.0", "slice": "y=0", "field": "temperature",
-                    "view": "-60,25"})
+                    "view": "-60,25"}, nel=tuple(nel))
 
 
 def turb_pipe(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (25, 25, 400),
@@ -139,7 +161,7 @@ def turb_pipe(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (2
         for c in range(3):
             vel[c] = vel[c] + amp[c] * damp * np.sin(arg + ph[c])
     return SemCase("c3", e1 - e0, e0, E, x, y, z, {"velocity": np.stack(vel)},
-                   {"iso": "Q=5.0", "field": "vorticity:mag", "view": "-70,20"})
+                   {"iso": "Q=5.0", "field": "vorticity:mag", "view": "-70,20"}, nel=tuple(nel))
 
 
 def pebble_bed(e0: int = 0, e1: int | None = None, n: int = 128, n_spheres: int = 146, seed: int = 3) -> SemCase:
@@ -163,7 +185,8 @@ def pebble_bed(e0: int = 0, e1: int | None = None, n: int = 128, n_spheres: int 
         v = v - k * 3.0 * dx * dy / d5
         w = w - k * 3.0 * dx * dz / d5
     return SemCase("c4", e1 - e0, e0, E, x, y, z, {"velocity": np.stack([u, v, w])},
-                   {"iso": "velocity:mag=1.2", "slice": "z=0.5", "field": "velocity:mag", "view": "+z"})
+                   {"iso": "velocity:mag=1.2", "slice": "z=0.5", "field": "velocity:mag", "view": "+z"},
+                   nel=(n, n, n))
 
 
 def box(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (4, 4, 4), seed: int = 0) -> SemCase:
@@ -183,7 +206,7 @@ def box(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (4, 4, 4
     T = np.cos(1.3 * x + 0.4) * np.sin(2.1 * y - 0.3) + z
     return SemCase("box", e1 - e0, e0, E, x, y, z, {"velocity": np.stack(vel), "temperature": T[None]},
                    {"iso": "Q=0.5;temperature=0.6", "slice": "0.3,1,0.2,0.9", "field": "temperature",
-                    "view": "30,40"})
+                    "view": "30,40"}, nel=tuple(nel))
 
 
 CONFIGS = {

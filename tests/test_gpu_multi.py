@@ -138,3 +138,62 @@ def test_collective_stats_equal_numpy_on_concatenation(tmp_path, size):
     got = np.load(tmp_path / f"stats{size}.npy")
     exp = np.array([glob.min(), glob.max(), glob.mean()])
     assert np.array_equal(got.view(np.uint64), exp.view(np.uint64)), (got, exp)
+
+
+def _dssum_worker(rank, size, port, out_dir):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        from paper_2312_09888_b200 import synth
+        from paper_2312_09888_b200.adaptor import SemDataAdaptor
+        from paper_2312_09888_b200.comm import Communicator
+        from paper_2312_09888_b200.context import Context
+        from paper_2312_09888_b200.data_model import POINT, FieldArray, SemBlock, Snapshot
+        from paper_2312_09888_b200.device import DeviceArray
+
+        nel = (3, 3, 5)
+        E = nel[0] * nel[1] * nel[2]
+        e0, e1 = synth.partition(E, rank, size)
+        c = synth.rbc_cylinder(e0, e1, nel=nel)
+        ctx = Context(rank)
+        comm = Communicator.from_torch(ctx)
+        da = SemDataAdaptor(ctx)
+        fields = tuple(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=c.n_points) for k, v in c.fields.items())
+        da.initialize(Snapshot(0.0, 0, rank, (SemBlock(c.n_elements, c.x, c.y, c.z, fields=fields, element_offset=e0,
+                                                       n_elements_global=E, global_ids=c.global_ids()),)))
+        rng = np.random.default_rng(7)
+        glob = rng.standard_normal(E * 512)
+        mine = np.ascontiguousarray(glob[e0 * 512:e1 * 512])
+        d = DeviceArray.empty(ctx, (mine.size,), np.float64)
+        d.upload(mine)
+        ctx.dssum(d)
+        np.save(os.path.join(out_dir, f"dssum{size}_{rank}.npy"), d.to_host())
+        dist.barrier()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size", [2, 3, 4])
+def test_dssum_across_ranks_matches_oracle(tmp_path, size):
+    """Shared-face nodes between partitions are averaged over all ranks: the
+    result equals the oracle on the rank-partitioned global array."""
+    if _ngpus() < size:
+        pytest.skip(f"needs {size} GPUs")
+    import torch.multiprocessing as mp
+
+    from oracle import oracle as O
+    from paper_2312_09888_b200 import synth
+
+    mp.spawn(_dssum_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    nel = (3, 3, 5)
+    E = nel[0] * nel[1] * nel[2]
+    rng = np.random.default_rng(7)
+    glob = rng.standard_normal(E * 512)
+    lo = [synth.partition(E, r, size)[0] * 512 for r in range(size)]
+    gid = synth.lattice_ids(nel, 0, E)
+    exp = O.dssum(gid, glob, lo)
+    got = np.concatenate([np.load(tmp_path / f"dssum{size}_{r}.npy") for r in range(size)])
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
