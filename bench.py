@@ -347,7 +347,7 @@ def run_ours(a):
         "clocks": clk,
     }
     if world == 1:
-        out["next_rows"] = next_rows(ctx, da, case, hcase, peaks["hbm_gbs"])
+        out["next_rows"] = next_rows(ctx, da, case, hcase, peaks["hbm_gbs"], pipe)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(hcase if hcase is not None else case.to_host(), pipe, an.view_for(da), a)
     if rank == 0:
@@ -358,7 +358,7 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
-def next_rows(ctx, da, case, hcase, hbm_gbs):
+def next_rows(ctx, da, case, hcase, hbm_gbs, pipe=None):
     """SURVEY.md §8f rows built after the hot path, measured on the same
     partition: the stats sink (nkb_stats, numpy-exact min/max/mean of every
     field) and the GPU checkpoint encoder (legacy-VTK sections).  Device
@@ -391,6 +391,49 @@ def next_rows(ctx, da, case, hcase, hbm_gbs):
         row["bit_exact_vs_numpy"] = all(
             np.array_equal(np.array(got[n]).view(np.uint64), np.array(ref[n]).view(np.uint64)) for n in names)
     res["stats_sink"] = row
+    # DSSUM (continuous derived fields): setup once per mesh, then per field
+    if case.name == "c2" and case.n_elements == 32768:
+        import torch
+
+        from paper_2312_09888_b200 import synth as _synth
+        from paper_2312_09888_b200.analysis import InsituAnalysis as _IA
+
+        gid = torch.from_numpy(_synth.lattice_ids((32, 32, 32), 0, 32768)).cuda()
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        ctx.mesh_set_global_ids(gid)
+        setup = _t.perf_counter() - t0
+        f = case.fields["temperature"].reshape(-1).clone()
+        ctx.dssum(f)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            ctx.dssum(f)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        npts = case.n_points
+        res["dssum"] = {"setup_ms": setup * 1e3, "ms": ms, "points": npts,
+                        "gb_per_s_field": 16 * npts / ms / 1e6,
+                        "note": "in-place average of one f64 field: read + write 8 B/pt, plus the sorted index"}
+        # the whole continuous step (gradient pass -> DSSUM of Q -> surface pass)
+        from dataclasses import replace as _rep
+
+        if pipe is not None:
+            ac, ad = _IA(_rep(pipe, continuous=True)), _IA(_rep(pipe, continuous=False))
+            for a_ in (ac, ad):
+                a_.execute(da, fetch_image=False)
+            out = {}
+            for key, a_ in (("continuous", ac), ("discontinuous", ad)):
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(reps):
+                    a_.execute(da, fetch_image=False)
+                e1.record()
+                torch.cuda.synchronize()
+                out[key] = e0.elapsed_time(e1) / reps
+            res["dssum"]["step_ms"] = out
     w = SemVtkWriter(ctx)
     arrays = names + ["Q"]
     w.encode(da, arrays, 0, 0, 0.0)
