@@ -213,6 +213,9 @@ struct nkb_ctx {
   std::map<std::vector<long long>, std::unique_ptr<StatsTables>> stats_cache;   // nkb_stats plans
   GsLocal gs;                                // DSSUM gather-scatter plan (nkb_mesh_set_global_ids)
   bool gs_ready = false;
+  cudaGraphExec_t graph_exec = nullptr;      // captured single-rank step (run_step)
+  std::string graph_key;
+  cudaStream_t cap_stream = nullptr;
   double* dq = nullptr;                      // continuous pipeline: DSSUM'd Q / |w| scratch
   double* dw = nullptr;
   int64_t dcap = 0;
@@ -313,11 +316,6 @@ static int ctx_check(nkb_ctx* ctx) {
   NKB_CUDA(cudaSetDevice(ctx->device));
   return NKB_OK;
 }
-#define NKB_TRY(expr)            \
-  do {                           \
-    int _rc = (expr);            \
-    if (_rc != NKB_OK) return _rc; \
-  } while (0)
 
 extern "C" {
 
@@ -391,6 +389,8 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   for (auto& kv : ctx->stats_cache)
     if (kv.second) stats_tables_free(*kv.second);
   gs_free(ctx->gs);
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   cudaFree(ctx->dq);
   cudaFree(ctx->dw);
   cudaFree(ctx->rgb_dev);
@@ -1260,8 +1260,11 @@ static int ensure_tri(nkb_ctx* ctx, int64_t cap, bool meta) {
   return NKB_OK;
 }
 
-static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
-                    cudaStream_t s, bool composite, bool ordered) {
+// Enqueue one step on stream s (no host synchronisation): memsets -> K1
+// (or count/scan/ordered emit) -> zbuf clear -> raster -> range words ->
+// composite -> resolve -> D2H of the report words.
+static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm, cudaStream_t s,
+                        bool composite, bool ordered, int* p2p_err, unsigned long long* tri_by_rank) {
   const bool timing = p->timing != 0;
   const int64_t npx = (int64_t)p->width * p->height;
   fp.tri = ctx->tri;
@@ -1386,12 +1389,69 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   if (!ordered)
     NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 8, ctx->region_count,
                              sizeof(unsigned long long) * ctx->n_regions, cudaMemcpyDeviceToHost, s));
+  if (p2p) {
+    NKB_CUDA(cudaMemcpyAsync(p2p_err, ctx->p2p.err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NKB_CUDA(cudaMemcpyAsync(tri_by_rank, ctx->p2p.flags + 2 * kMaxRanks, sizeof(unsigned long long) * kMaxRanks,
+                             cudaMemcpyDeviceToHost, s));
+  }
+  return NKB_OK;
+}
+
+// the launch parameters a captured step depends on (graph cache key)
+static std::string step_key(nkb_ctx* ctx, const nkb_pipeline* p, const FusedParams& fp, const Colormap& cm,
+                            bool ordered) {
+  std::string k;
+  auto add = [&](const void* d, size_t n) { k.append(reinterpret_cast<const char*>(d), n); };
+  add(p, sizeof(*p));
+  add(&fp, sizeof(fp));
+  add(&cm, sizeof(cm));
+  const void* ptrs[] = {ctx->tri, ctx->meta, ctx->zbuf, ctx->rgba, ctx->depth, ctx->counters, ctx->region_count,
+                        ctx->elem_count, ctx->elem_offset, ctx->range_dev, ctx->h_counters};
+  add(ptrs, sizeof(ptrs));
+  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0};
+  add(v, sizeof(v));
+  return k;
+}
+
+static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
+                    cudaStream_t s, bool composite, bool ordered) {
   int p2p_err = 0;
   unsigned long long tri_by_rank[kMaxRanks] = {};
-  if (p2p) {
-    NKB_CUDA(cudaMemcpyAsync(&p2p_err, ctx->p2p.err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    NKB_CUDA(cudaMemcpyAsync(tri_by_rank, ctx->p2p.flags + 2 * kMaxRanks, sizeof(tri_by_rank),
-                             cudaMemcpyDeviceToHost, s));
+  const bool p2p = composite && ctx->p2p.ready;
+  // Single-rank steps replay a CUDA graph of the whole launch sequence (one
+  // launch instead of ~10), re-captured whenever a parameter changes.
+  static const bool graphs = !(getenv("NKB_GRAPHS") && strcmp(getenv("NKB_GRAPHS"), "0") == 0);
+  // (per-stage timing keeps the eager path: its events bracket the stages)
+  if (graphs && !composite && fp.prof == nullptr && !p->timing) {
+    if (ordered && ctx->elem_cap < ctx->E) {       // (allocation happens outside the capture)
+      cudaFree(ctx->elem_count);
+      cudaFree(ctx->elem_offset);
+      ctx->elem_count = nullptr;
+      ctx->elem_offset = nullptr;
+      NKB_CUDA(cudaMalloc(&ctx->elem_count, sizeof(int) * ctx->E));
+      NKB_CUDA(cudaMalloc(&ctx->elem_offset, sizeof(long long) * ctx->E));
+      ctx->elem_cap = ctx->E;
+    }
+    NKB_TRY(launch_fused_prepare());
+    const std::string key = step_key(ctx, p, fp, cm, ordered);
+    if (!ctx->graph_exec || key != ctx->graph_key) {
+      if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+      ctx->graph_exec = nullptr;
+      if (!ctx->cap_stream) NKB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+      NKB_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+      const int rc = enqueue_step(ctx, p, fp, cm, ctx->cap_stream, composite, ordered, &p2p_err, tri_by_rank);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
+      NKB_TRY(rc);
+      NKB_CUDA(ce);
+      const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      NKB_CUDA(ie);
+      ctx->graph_key = key;
+    }
+    NKB_CUDA(cudaGraphLaunch(ctx->graph_exec, s));
+  } else {
+    NKB_TRY(enqueue_step(ctx, p, fp, cm, s, composite, ordered, &p2p_err, tri_by_rank));
   }
   NKB_CUDA(cudaStreamSynchronize(s));
   if (p2p) {

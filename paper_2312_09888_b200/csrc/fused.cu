@@ -832,6 +832,22 @@ static size_t fused_smem_bytes(int nin) {
   return (size_t)(kRing * nin + kNumD + 4) * kArr * sizeof(double) + 2 * kNN;
 }
 
+// one-time kernel attributes (outside any stream capture)
+int launch_fused_prepare() {
+  static bool done = false;
+  if (done) return NKB_OK;
+  const int mx = (int)fused_smem_bytes(kMaxIn);
+  NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  int dev = 0;
+  NKB_CUDA(cudaGetDevice(&dev));
+  NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  done = true;
+  return NKB_OK;
+}
+
 int launch_fused(const FusedParams& p, cudaStream_t s) {
   if (p.n_elements <= 0) return NKB_OK;
   const bool cached = p.geo != nullptr && p.need_grad;
@@ -859,18 +875,7 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   if (nin > kMaxIn) return fail(NKB_EINVAL, "too many staged fields for one pass (coordinates, velocity and "
                                             "scalars exceed 8)");
   const size_t shm = fused_smem_bytes(nin);
-  static bool attr_set = false;
-  if (!attr_set) {
-    const int mx = (int)fused_smem_bytes(kMaxIn);
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    int dev = 0;
-    NKB_CUDA(cudaGetDevice(&dev));
-    NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    attr_set = true;
-  }
+  NKB_TRY(launch_fused_prepare());
   const int grid = fused_grid(p.n_elements);
   const unsigned gx = (unsigned)grid;
   if (p.prof) {

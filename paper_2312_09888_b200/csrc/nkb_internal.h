@@ -15,6 +15,14 @@ namespace nkb {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 
+#ifndef NKB_TRY
+#define NKB_TRY(expr)            \
+  do {                           \
+    int _rc = (expr);            \
+    if (_rc != NKB_OK) return _rc; \
+  } while (0)
+#endif
+
 #define NKB_CUDA(call)                                                              \
   do {                                                                              \
     cudaError_t _e = (call);                                                        \
@@ -145,6 +153,7 @@ struct ResolveParams {
 int set_dmat_constant(const double* dmat);
 int fused_grid(int64_t n_elements);       // CTAs (= triangle regions) of launch_fused
 int launch_fused(const FusedParams& p, cudaStream_t s);
+int launch_fused_prepare();
 int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* geo, cudaStream_t s);
 int launch_compact(const float4* tri, const unsigned long long* meta, const unsigned long long* region_count,
                    int n_regions, int64_t region_cap, float4* out_tri, unsigned long long* out_meta,
