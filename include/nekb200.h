@@ -158,6 +158,13 @@ int nkb_mesh_set_global_ids(nkb_ctx* ctx, const int64_t* gid, void* stream);
  *   ((P_r0 + P_r1) + ...) / count,  P_r = sum of rank r's copies in
  * increasing local index order (ranks in increasing order).  Collective. */
 int nkb_dssum(nkb_ctx* ctx, double* field, void* stream);
+/* In transit (the paper's staging mode, reference transport.py:358-376):
+ * collective N:1 gather of every rank's mesh and registered fields to `root`
+ * over NCCL send/recv (GPU-direct, no host copy), concatenated in rank order
+ * (partitions must be contiguous and share one field schema).  Afterwards
+ * root's context describes the assembled mesh (library-owned buffers, valid
+ * until the next gather) and root can run nkb_execute on it alone. */
+int nkb_transit_gather(nkb_ctx* ctx, int root, void* stream);
 int nkb_mesh_modified(nkb_ctx* ctx);
 int nkb_set_geometry_cache(nkb_ctx* ctx, int enable);
 /* register (or re-point) a device-resident point field, borrowed.

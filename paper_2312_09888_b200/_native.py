@@ -126,6 +126,7 @@ _SIGS = {
     "nkb_encode_be": ([_vp, C.c_char_p, _vp, _i64, C.POINTER(C.c_int64), _vp], C.c_int),
     "nkb_mesh_set_global_ids": ([_vp, _vp, _vp], C.c_int),
     "nkb_dssum": ([_vp, _vp, _vp], C.c_int),
+    "nkb_transit_gather": ([_vp, C.c_int, _vp], C.c_int),
     "nkb_triangles_device": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)], C.c_int),
     "nkb_nccl_unique_id": ([_vp], C.c_int),
     "nkb_comm_init": ([_vp, _vp, C.c_int, C.c_int], C.c_int),

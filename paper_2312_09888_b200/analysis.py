@@ -184,19 +184,22 @@ class InsituAnalysis:
     def __init__(self, pipeline: Pipeline | dict[str, str]):
         self.pipeline = pipeline if isinstance(pipeline, Pipeline) else pipeline_from_params(pipeline)
         self._view: tuple[float, ...] | None = None
-        self._bounds_key = None
         self.executions = 0
 
     def view_for(self, data_adaptor) -> tuple[float, ...]:
+        """The camera: fixed by the pipeline, or fitted once to the global
+        mesh bounds on the first execute (nkb_mesh_bounds is collective, so
+        every rank makes the same calls; reset_view() refits, on all ranks)."""
         p = self.pipeline
         if p.view is not None:
             return tuple(p.view)
-        key = (id(data_adaptor._block), p.width, p.height, p.view_dir)
-        if self._view is None or key != self._bounds_key:
+        if self._view is None:
             b = data_adaptor.ctx.bounds()
             self._view = ortho_view(b, p.width, p.height, *p.view_dir)
-            self._bounds_key = key
         return self._view
+
+    def reset_view(self) -> None:
+        self._view = None
 
     def execute(self, data_adaptor, fetch_image: bool = True, depth: bool = False) -> ExecuteResult:
         view = self.view_for(data_adaptor)

@@ -35,6 +35,8 @@ _ATTRS_BY_KIND: dict[str, frozenset[str]] = {
     "render": frozenset({"dir", "width", "height", "field", "vmin", "vmax"}),
     "insitu": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
                          "velocity", "composite", "continuous"}),
+    "transit": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
+                          "velocity", "endpoint"}),
     "stats": frozenset({"path"}),
     "checkpoint": frozenset({"dir", "format", "arrays"}),
     "null": frozenset(),

@@ -89,6 +89,11 @@ class Context:
         """In-place direct stiffness average of a device point field."""
         N.call("nkb_dssum", self.handle, device_ptr(field), stream or None)
 
+    def transit_gather(self, root: int = 0, stream: int = 0) -> None:
+        """N:1 GPU-direct staging: gather every rank's mesh + fields to `root`
+        (collective); root's context then holds the assembled mesh."""
+        N.call("nkb_transit_gather", self.handle, int(root), stream or None)
+
     def mesh_modified(self) -> None:
         """Coordinates were edited in place (moving mesh): drop the geometry cache."""
         N.call("nkb_mesh_modified", self.handle)

@@ -213,6 +213,9 @@ struct nkb_ctx {
   std::map<std::vector<long long>, std::unique_ptr<StatsTables>> stats_cache;   // nkb_stats plans
   GsLocal gs;                                // DSSUM gather-scatter plan (nkb_mesh_set_global_ids)
   bool gs_ready = false;
+  // in transit staging (nkb_transit_gather): the assembled mesh on the endpoint
+  double* tr_buf = nullptr;
+  int64_t tr_cap = 0;                        // doubles
   cudaGraphExec_t graph_exec = nullptr;      // captured single-rank step (run_step)
   std::string graph_key;
   cudaStream_t cap_stream = nullptr;
@@ -389,6 +392,7 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   for (auto& kv : ctx->stats_cache)
     if (kv.second) stats_tables_free(*kv.second);
   gs_free(ctx->gs);
+  cudaFree(ctx->tr_buf);
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   cudaFree(ctx->dq);
@@ -750,6 +754,93 @@ int nkb_mesh_set_global_ids(nkb_ctx* ctx, const int64_t* gid, void* stream) {
   for (int q = 0; q < R; ++q) rp[q] = g.rbuf + g.noff[q];
   NKB_CUDA(cudaMemcpy(g.rptr, rp.data(), sizeof(double*) * R, cudaMemcpyHostToDevice));
   ctx->gs_ready = true;
+  return NKB_OK;
+}
+
+// ---- in transit: N:1 GPU-direct staging of SEM partitions ---------------------
+
+static unsigned long long fnv1a(const std::string& t, unsigned long long h = 1469598103934665603ULL) {
+  for (unsigned char c : t) h = (h ^ c) * 1099511628211ULL;
+  return h;
+}
+
+int nkb_transit_gather(nkb_ctx* ctx, int root, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->x) return fail(NKB_ESTATE, "transit before mesh_set");
+  if (!ctx->comm || ctx->nranks < 2) return fail(NKB_ESTATE, "transit needs a communicator with >= 2 ranks");
+  const int R = ctx->nranks, me = ctx->rank;
+  if (root < 0 || root >= R) return fail(NKB_EINVAL, "root out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  // schema check + partition sizes: (E, element offset, #fields, hash of names/components)
+  std::string sig;
+  for (auto& f : ctx->fields) sig += f.name + ":" + std::to_string(f.ncomp) + ";";
+  const long long mine[4] = {(long long)ctx->E, (long long)ctx->elem_off, (long long)ctx->fields.size(),
+                             (long long)(fnv1a(sig) & 0x7fffffffffffffffULL)};
+  long long* d = nullptr;
+  NKB_CUDA(cudaMalloc(&d, sizeof(long long) * 4 * (R + 1)));
+  NKB_CUDA(cudaMemcpy(d + 4 * R, mine, sizeof(mine), cudaMemcpyHostToDevice));
+  NKB_NCCL(g_nccl.AllGather(d + 4 * R, d, 4, ncclInt64, ctx->comm, s));
+  std::vector<long long> all(4 * R);
+  NKB_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(long long) * 4 * R, cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d);
+  std::vector<long long> lo(R + 1, 0);
+  for (int q = 0; q < R; ++q) {
+    if (all[4 * q + 2] != mine[2] || all[4 * q + 3] != mine[3])
+      return fail(NKB_EINVAL, "transit: ranks carry different field schemas");
+    if (q > 0 && all[4 * q + 1] != all[4 * (q - 1) + 1] + all[4 * (q - 1)])
+      return fail(NKB_EINVAL, "transit: partitions are not contiguous in rank order");
+    lo[q + 1] = lo[q] + all[4 * q];
+  }
+  const int64_t Et = lo[R], nt = Et * kNN;
+  // arrays in order: x, y, z, then every component of every field (SoA)
+  std::vector<std::pair<const double*, int64_t>> arrs;   // (local base, stride unused)
+  arrs.push_back({ctx->x, 0});
+  arrs.push_back({ctx->y, 0});
+  arrs.push_back({ctx->z, 0});
+  for (auto& f : ctx->fields)
+    for (int c = 0; c < f.ncomp; ++c) arrs.push_back({f.base + (int64_t)c * f.comp_stride, 0});
+  const int na = (int)arrs.size();
+  const int64_t nloc = ctx->E * kNN;
+  if (me == root && ctx->tr_cap < (int64_t)na * nt) {
+    cudaFree(ctx->tr_buf);
+    ctx->tr_buf = nullptr;
+    ctx->tr_cap = 0;
+    NKB_CUDA(cudaMalloc(&ctx->tr_buf, sizeof(double) * std::max<int64_t>((int64_t)na * nt, 1)));
+    ctx->tr_cap = (int64_t)na * nt;
+  }
+  NKB_NCCL(g_nccl.GroupStart());
+  for (int a = 0; a < na; ++a) {
+    if (me == root) {
+      double* dst = ctx->tr_buf + (int64_t)a * nt;
+      for (int q = 0; q < R; ++q) {
+        const int64_t cnt = all[4 * q] * kNN;
+        if (cnt == 0) continue;
+        if (q == root)
+          NKB_CUDA(cudaMemcpyAsync(dst + lo[q] * kNN, arrs[a].first, sizeof(double) * cnt, cudaMemcpyDeviceToDevice, s));
+        else
+          NKB_NCCL(g_nccl.Recv(dst + lo[q] * kNN, (size_t)cnt, ncclFloat64, q, ctx->comm, s));
+      }
+    } else if (nloc > 0) {
+      NKB_NCCL(g_nccl.Send(arrs[a].first, (size_t)nloc, ncclFloat64, root, ctx->comm, s));
+    }
+  }
+  NKB_NCCL(g_nccl.GroupEnd());
+  NKB_CUDA(cudaStreamSynchronize(s));
+  if (me != root) return NKB_OK;
+  // the endpoint's context now describes the assembled mesh (producer order)
+  std::vector<Field> nf;
+  int a = 3;
+  for (auto& f : ctx->fields) {
+    Field g = f;
+    g.base = ctx->tr_buf + (int64_t)a * nt;
+    g.comp_stride = nt;
+    a += f.ncomp;
+    nf.push_back(g);
+  }
+  const double* tb = ctx->tr_buf;
+  NKB_TRY(nkb_mesh_set(ctx, Et, kN, tb, tb + nt, tb + 2 * nt, 0, Et));
+  ctx->fields = nf;
   return NKB_OK;
 }
 

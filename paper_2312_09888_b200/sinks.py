@@ -20,6 +20,8 @@ bytes written, ``finalize()`` flushes.  Registered kinds:
   in the reference's exact STRUCTURED_POINTS layout; SEM snapshots as an
   UNSTRUCTURED_GRID of the sub-hex mesh with the snapshot's fields plus any
   AddArray arrays (``arrays="Q,vorticity:mag"``), encoded on the GPU (vtk.py).
+* ``transit`` -- the in transit mode: SEM partitions staged GPU-to-GPU to
+  an endpoint rank (NCCL), analysed there on the assembled mesh.
 * ``null`` -- counts invocations (:354-363).
 """
 from __future__ import annotations
@@ -243,6 +245,54 @@ def _device_len(d) -> int:
     return int(np.prod(shape)) if len(shape) else 1
 
 
+class TransitSink:
+    """In transit analysis (the paper's staging mode; reference transport.py
+    N:1 endpoint, :358-376): every rank's SEM partition is staged to the
+    endpoint GPU over NCCL send/recv (nkb_transit_gather, no host copy), and
+    the endpoint runs the in situ pipeline on the assembled mesh alone and
+    writes the image.  Same attributes as ``insitu`` plus ``endpoint``."""
+
+    def __init__(self, params: dict[str, str], comm=None):
+        from dataclasses import replace
+
+        self.dir = Path(params.get("dir", "transit_out"))
+        self.pipeline = replace(pipeline_from_params(params), composite=False)
+        self.endpoint = int(params.get("endpoint", 0))
+        self.comm = comm
+        self.velocity = params.get("velocity", "velocity")
+        self.analysis = InsituAnalysis(self.pipeline)
+        self.adaptor: SemDataAdaptor | None = None
+        self.last = None
+        if comm is None or comm.rank == self.endpoint:
+            self.dir.mkdir(parents=True, exist_ok=True)
+            _probe_writable(self.dir)
+
+    def consume(self, s) -> int:
+        if self.adaptor is None:
+            ctx = self.comm.ctx if self.comm is not None else default_context()
+            self.adaptor = SemDataAdaptor(ctx, velocity=self.velocity)
+            if self.comm is not None and self.comm.rank == self.endpoint:
+                # the endpoint alternates between its partition and the
+                # assembled mesh: recomputing J^-1 is cheaper than re-caching it
+                ctx.set_geometry_cache(False)
+        self.adaptor.initialize(s)
+        ctx = self.adaptor.ctx
+        view = self.analysis.view_for(self.adaptor)            # collective (global bounds)
+        if self.comm is not None and ctx.nranks > 1:
+            ctx.transit_gather(self.endpoint)
+            if ctx.rank != self.endpoint:
+                return 0
+        self.last = ctx.execute(self.pipeline.native(view))
+        ppm = ctx.image_ppm()
+        fname = f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}.ppm"
+        with open(self.dir / fname, "wb") as f:
+            f.write(ppm)
+        return len(ppm)
+
+    def finalize(self):
+        pass
+
+
 class StatsSink:
     """Appends step,time,field,min,max,mean rows (sinks.py:366-393).
 
@@ -373,6 +423,7 @@ class NullSink:
 _SINK_TYPES = {
     "render": RenderSink,
     "insitu": InsituSink,
+    "transit": TransitSink,
     "stats": StatsSink,
     "checkpoint": CheckpointSink,
     "null": NullSink,

@@ -197,3 +197,55 @@ def test_dssum_across_ranks_matches_oracle(tmp_path, size):
     exp = O.dssum(gid, glob, lo)
     got = np.concatenate([np.load(tmp_path / f"dssum{size}_{r}.npy") for r in range(size)])
     assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+
+
+def _transit_worker(rank, size, port, out_dir):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    try:
+        from paper_2312_09888_b200 import synth
+        from paper_2312_09888_b200.bridge import initialize, parse_config
+        from paper_2312_09888_b200.comm import Communicator
+        from paper_2312_09888_b200.context import Context
+        from paper_2312_09888_b200.data_model import POINT, FieldArray, SemBlock, Snapshot
+
+        nel = (4, 4, 6)
+        E = nel[0] * nel[1] * nel[2]
+        e0, e1 = synth.partition(E, rank, size)
+        c = synth.box(e0, e1, nel=nel)
+        ctx = Context(rank)
+        comm = Communicator.from_torch(ctx)
+        kind = "transit" if size > 1 else "insitu"
+        doc = (f'<sensei><analysis type="{kind}" frequency="1" dir="{out_dir}/{kind}{size}" '
+               f'iso="Q=0.5;temperature=0.6" slice="0.3,1,0.2,0.9" field="temperature" '
+               f'width="{W}" height="{H}" view="30,40"/></sensei>')
+        br = initialize(parse_config(doc), comm=comm if size > 1 else None)
+        fields = tuple(FieldArray(k, POINT, v.shape[0], v.ravel(), comp_stride=c.n_points) for k, v in c.fields.items())
+        blk = SemBlock(c.n_elements, c.x, c.y, c.z, fields=fields, element_offset=e0, n_elements_global=E)
+        for step in range(3):
+            reps = br.update(Snapshot(0.1 * step, step, rank, (blk,)))
+            assert all(r.error is None for r in reps), reps
+        dist.barrier()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size", [2, 4])
+def test_transit_endpoint_image_equals_single_gpu(tmp_path, size):
+    """In transit: partitions staged GPU-to-GPU to the endpoint, analysed there
+    on the assembled mesh -- the PPM equals the one-GPU in situ image byte for
+    byte, every step."""
+    if _ngpus() < size:
+        pytest.skip(f"needs {size} GPUs")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_transit_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
+    mp.spawn(_transit_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    for step in range(3):
+        name = f"step{step:06d}_temperature.ppm"
+        a = (tmp_path / "insitu1" / name).read_bytes()
+        b = (tmp_path / f"transit{size}" / name).read_bytes()
+        assert a == b
