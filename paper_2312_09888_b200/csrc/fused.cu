@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 4 * kArr);   // 512 case bits
   __shared__ McScratch mc;
   __shared__ double s_mn[kThreads / 32], s_mx[kThreads / 32];
+  __shared__ unsigned s_band, s_bor;                   // AND / OR of the element's case bits
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -520,6 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     const int prev_emits = __syncthreads_or(cls_any);
     tick(0);
     cls_any = 0;
+    if (tid == 0) {                                    // read by everyone before the barrier above
+      s_band = ~0u;
+      s_bor = 0u;
+    }
     const double* S_in = S_ring + slot * nin * kArr;
     if (it + 1 < n_it) prefetch(e + G, (int)((it + 1) % kRing));
     cp_async_commit();
@@ -622,6 +627,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
         bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
       }
       bits_out[n] = (unsigned char)bits;
+      {
+        // per-warp AND / OR of the case bits: an element whose nodes all sit
+        // on one side of every surface emits nothing and skips classification
+        const unsigned wa = __reduce_and_sync(0xffffffffu, bits), wo = __reduce_or_sync(0xffffffffu, bits);
+        if (lane == 0) {
+          atomicAnd(&s_band, wa);
+          atomicOr(&s_bor, wo);
+        }
+      }
       if (p.color_src >= 0) {
         const int src = p.color_src;
         const double c = (src == SRC_Q)      ? vq
@@ -639,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     if (kCached && tid == 0 && it + 1 < n_it)          // S_geo consumed: fetch element it+1
       bulk_load(S_geo, p.geo + (e + G) * 9 * kNN, kGeoBytes, &s_geo_bar);
     if (p.n_surf == 0) continue;
+    if ((s_bor & ~s_band) == 0) continue;               // no surface crosses this element
 
     // ---- classify: one sub-hex per thread (all warps) ----
     if (tid < kNC) {
