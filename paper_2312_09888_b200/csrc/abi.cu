@@ -87,12 +87,8 @@ static int load_nccl() {
       return ::nkb::fail(NKB_ENCCL, std::string(#call) + ": " + g_nccl.GetErrorString(_r)); \
   } while (0)
 
-// ordered encoding of doubles (monotone as unsigned 64-bit)
-static inline unsigned long long enc_ordered_h(double d) {
-  unsigned long long b;
-  memcpy(&b, &d, 8);
-  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
-}
+// inverse of the kernels' ordered encoding of doubles (monotone as unsigned
+// 64-bit: sign set -> flip all bits, else set the sign bit)
 static inline double dec_ordered_h(unsigned long long u) {
   unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
   double d;

@@ -148,9 +148,6 @@ constexpr int kMaxTriPerElem = kNC * NKB_MC_MAX_TRI * NKB_MAX_SURFACES;   // 686
 // even-odd 8-point derivatives of three staged fields along one pencil
 // (oracle deriv8): e_m = v_m + v_{7-m}, o_m = v_m - v_{7-m},
 // out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 DFMAs
-// I0/NI: compute only rows i in [I0, I0+NI) (and their mirrors 7-i), so two
-// threads can share one pencil (the geometry-cached variant)
-template <int I0 = 0, int NI = 4>
 __device__ __forceinline__ void pencil3(const double* s0, const double* s1, const double* s2, double* d0,
                                         double* d1, double* d2, const int* off) {
   double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
@@ -167,7 +164,7 @@ __device__ __forceinline__ void pencil3(const double* s0, const double* s1, cons
     o2[m] = __dsub_rn(a2, b2);
   }
 #pragma unroll
-  for (int i = I0; i < I0 + NI; ++i) {
+  for (int i = 0; i < 4; ++i) {
     const double ce = c_Ae[i][0], co = c_Ao[i][0];
     double E0 = __dmul_rn(ce, e0[0]), E1 = __dmul_rn(ce, e1[0]), E2 = __dmul_rn(ce, e2[0]);
     double O0 = __dmul_rn(co, o0[0]), O1 = __dmul_rn(co, o1[0]), O2 = __dmul_rn(co, o2[0]);
