@@ -481,6 +481,12 @@ def cpu_baseline(case, pipe, view, a, reps: int = 2) -> dict:
                       f"{cores} threads", "ms_per_step": best * 1e3}
 
 
+def synth_elements(config: str, world: int) -> int:
+    from paper_2312_09888_b200 import synth
+
+    return synth.CONFIG_ELEMENTS[config] * (world if config in ("c2", "c3") else 1)
+
+
 def run_reference(a):
     rank, world, _ = _env_rank()
     if rank != 0:
@@ -512,7 +518,10 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{a.config} (bounded CPU sample)", "image": f"{a.width}x{a.width}"},
+        "config": {"workload": WORKLOADS[a.config].format(
+                       E=synth_elements(a.config, world), N=world),
+                   "image": f"{a.width}x{a.width}",
+                   "cpu_sample": f"{e_sample} elements per step (bounded; throughput is per point)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
