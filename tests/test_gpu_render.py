@@ -150,3 +150,30 @@ def test_image_ppm_equals_write_ppm_bytes(tmp_path, wh):
     ppm = bytes(ctx.image_ppm())
     assert len(ppm) == n and ppm == (tmp_path / "a.ppm").read_bytes()
     ctx.close()
+
+
+def test_gpu_colormap_equals_np_interp_on_2m_samples(ctx):
+    """SURVEY.md §8c pin: the GPU colormap (structured renderer, exact grid
+    sampling with vmin=0, vmax=1 so t = value) against the reference's own
+    formula -- np.interp per channel then floor(v + 0.5) (sinks.py:201-209)
+    -- on 2,097,152 samples including the anchors, clipping and exact halves."""
+    from paper_2312_09888_b200.device import DeviceArray
+
+    ni, nj = 16384, 128
+    rng = np.random.default_rng(123)
+    t = rng.uniform(-0.2, 1.2, ni * nj)
+    halves = (np.arange(0, 196) + 0.5 - 59) / 392.0
+    special = np.array([0.0, 0.5, 1.0, -0.0, 0.25, 0.75, np.nextafter(0.5, 0), np.nextafter(0.5, 1), 1e-300])
+    t[:special.size] = special
+    t[special.size:special.size + halves.size] = halves
+    grid = t.reshape(nj, ni)                         # row j = y index (x fastest)
+    d = DeviceArray.empty(ctx, (t.size,), np.float64)
+    d.upload(np.ascontiguousarray(grid).ravel())
+    rgb = DeviceArray.empty(ctx, (ni * nj * 3,), np.uint8)
+    ctx.render_structured([(d, ni)], nj, 1, 0, ni, nj, 0.0, 1.0, rgb)
+    img = rgb.to_host().reshape(nj, ni, 3)[::-1]     # row 0 = top = largest y
+    tc = np.clip(grid, 0.0, 1.0)
+    exp = np.empty((nj, ni, 3), np.uint8)
+    for ch, col in enumerate(((59, 255, 180), (76, 255, 4), (192, 255, 38))):
+        exp[..., ch] = np.floor(np.interp(tc, [0.0, 0.5, 1.0], col) + 0.5).astype(np.uint8)
+    assert np.array_equal(img, exp), int((img != exp).any(-1).sum())
