@@ -333,6 +333,7 @@ def run_ours(a):
             "workload": WORKLOADS[a.config].format(E=case.n_elements_global, N=world),
             "elements_per_gpu": case.n_elements, "gll_points_per_gpu": npts,
             "gll_points_total": npts * world,
+            **({"gll_points_unique": 185193} if a.config == "c1" else {}),
             "surfaces": case.params.get("iso", "") + (";slice " + case.params["slice"] if "slice" in case.params else ""),
             "color": case.params.get("field"), "image": f"{a.width}x{a.width}",
             "l2": f"inputs {npts * bpp / 1e9:.2f} GB/GPU >> 126 MB L2 (no flush needed)",
@@ -344,7 +345,8 @@ def run_ours(a):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": "fused_kernel",
                      "kernel_ms": fused, "alg_bytes_per_launch": alg_bytes, "peak_source": peak_kind,
-                     "bytes_per_point": bpp, "triangles": ntri},
+                     "bytes_per_point": bpp, "triangles": ntri,
+                     "frac_of_nominal_8tbs": achieved / 8000.0},
         "fused_uncached": uncached,
         "stages_ms": dict(zip(("fused", "raster", "composite", "resolve"),
                               (round(statistics.mean(x), 4) for x in zip(*stages)))),
