@@ -11,25 +11,11 @@
 #include <math.h>
 
 #include "nkb_internal.h"
+#include "raster_dev.cuh"
 
 namespace nkb {
 
 namespace {
-
-constexpr double kGuard = 32768.0;   // |screen coordinate| bound in pixels
-
-__device__ __forceinline__ void xform(const double* V, double x, double y, double z, double& sx,
-                                      double& sy, double& sz) {
-  sx = __dadd_rn(__fma_rn(V[2], z, __fma_rn(V[1], y, __dmul_rn(V[0], x))), V[3]);
-  sy = __dadd_rn(__fma_rn(V[6], z, __fma_rn(V[5], y, __dmul_rn(V[4], x))), V[7]);
-  sz = __dadd_rn(__fma_rn(V[10], z, __fma_rn(V[9], y, __dmul_rn(V[8], x))), V[11]);
-}
-
-__device__ __forceinline__ long long floordiv(long long a, long long b) {  // b > 0
-  long long q = a / b;
-  if ((a % b != 0) && (a < 0)) --q;
-  return q;
-}
 
 __device__ __forceinline__ double dec_ordered(unsigned long long u) {
   unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
@@ -75,70 +61,7 @@ __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
   const int W = p.width, H = p.height;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntri;
        t += (long long)gridDim.x * blockDim.x) {
-    long long X[3], Y[3];
-    double Z[3], C[3];
-    bool ok = true;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const float4 v = tri[3 * t + q];
-      double sx, sy, sz;
-      xform(p.view, (double)v.x, (double)v.y, (double)v.z, sx, sy, sz);
-      if (!(fabs(sx) <= kGuard && fabs(sy) <= kGuard && sz == sz && v.w == v.w)) ok = false;
-      X[q] = __double2ll_rn(__dmul_rn(sx, 256.0));
-      Y[q] = __double2ll_rn(__dmul_rn(sy, 256.0));
-      Z[q] = sz;
-      C[q] = (double)v.w;
-    }
-    if (!ok) continue;
-    long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
-    if (area == 0) continue;
-    if (area < 0) {
-      long long tx = X[1]; X[1] = X[2]; X[2] = tx;
-      long long ty = Y[1]; Y[1] = Y[2]; Y[2] = ty;
-      double tz = Z[1]; Z[1] = Z[2]; Z[2] = tz;
-      double tc = C[1]; C[1] = C[2]; C[2] = tc;
-      area = -area;
-    }
-    const long long xmin = min(X[0], min(X[1], X[2])), xmax = max(X[0], max(X[1], X[2]));
-    const long long ymin = min(Y[0], min(Y[1], Y[2])), ymax = max(Y[0], max(Y[1], Y[2]));
-    long long px0 = -floordiv(-(xmin - 128), 256), px1 = floordiv(xmax - 128, 256);
-    long long py0 = -floordiv(-(ymin - 128), 256), py1 = floordiv(ymax - 128, 256);
-    if (px0 < 0) px0 = 0;
-    if (py0 < 0) py0 = 0;
-    if (px1 > W - 1) px1 = W - 1;
-    if (py1 > H - 1) py1 = H - 1;
-    // edge (a->b) opposite vertex i: w_i(P) = (Xb-Xa)(Py-Ya) - (Yb-Ya)(Px-Xa)
-    const int ea[3] = {1, 2, 0}, eb[3] = {2, 0, 1};
-    long long bias[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const long long dy = Y[eb[i]] - Y[ea[i]], dx = X[eb[i]] - X[ea[i]];
-      bias[i] = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : -1;   // inclusive (top-left) edges
-    }
-    const double dA = (double)area;
-    for (long long py = py0; py <= py1; ++py) {
-      const long long cy = py * 256 + 128;
-      for (long long px = px0; px <= px1; ++px) {
-        const long long cx = px * 256 + 128;
-        long long w[3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-          w[i] = (X[eb[i]] - X[ea[i]]) * (cy - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx - X[ea[i]]);
-        if (w[0] + bias[0] < 0 || w[1] + bias[1] < 0 || w[2] + bias[2] < 0) continue;
-        double d = __ddiv_rn(__fma_rn((double)w[2], Z[2],
-                                      __fma_rn((double)w[1], Z[1], __dmul_rn((double)w[0], Z[0]))),
-                             dA);
-        if (!(d >= 0.0 && d <= 1.0)) continue;
-        d = __dadd_rn(d, 0.0);
-        const double c = __ddiv_rn(__fma_rn((double)w[2], C[2],
-                                            __fma_rn((double)w[1], C[1], __dmul_rn((double)w[0], C[0]))),
-                                   dA);
-        const unsigned long long key =
-            ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
-            (unsigned long long)__float_as_uint(__double2float_rn(c));
-        atomicMin(p.zbuf + py * W + px, key);
-      }
-    }
+    rdev::raster_triangle(p.view, W, H, tri + 3 * t, p.zbuf);
   }
 }
 
