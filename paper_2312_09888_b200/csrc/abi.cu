@@ -605,7 +605,15 @@ static int resolve_src(nkb_ctx* ctx, const char* name, FusedParams& fp, int* src
   return NKB_OK;
 }
 
+// per-segment slopes of np.interp, computed once on the host with the same
+// IEEE operations the kernels used per pixel (-ffp-contract=off): bit-identical
+static void colormap_slopes(Colormap& cm) {
+  for (int j = 0; j + 1 < cm.n; ++j)
+    for (int ch = 0; ch < 3; ++ch) cm.slope[j][ch] = (cm.rgb[j + 1][ch] - cm.rgb[j][ch]) / (cm.t[j + 1] - cm.t[j]);
+}
+
 static int build_colormap(const nkb_pipeline* p, Colormap& cm) {
+  memset(&cm, 0, sizeof(cm));
   if (p->n_anchors == 0) {  // DEFAULT_COLORMAP (sinks.py:213)
     cm.n = 3;
     const double t[3] = {0.0, 0.5, 1.0};
@@ -614,6 +622,7 @@ static int build_colormap(const nkb_pipeline* p, Colormap& cm) {
       cm.t[i] = t[i];
       for (int ch = 0; ch < 3; ++ch) cm.rgb[i][ch] = c[i][ch];
     }
+    colormap_slopes(cm);
     return NKB_OK;
   }
   if (p->n_anchors < 2 || p->n_anchors > NKB_MAX_ANCHORS)
@@ -629,6 +638,7 @@ static int build_colormap(const nkb_pipeline* p, Colormap& cm) {
     cm.t[i] = p->anchor_t[i];
     for (int ch = 0; ch < 3; ++ch) cm.rgb[i][ch] = (double)p->anchor_rgb[i][ch];
   }
+  colormap_slopes(cm);
   return NKB_OK;
 }
 

@@ -112,6 +112,7 @@ struct Colormap {
   int n;
   double t[NKB_MAX_ANCHORS];
   double rgb[NKB_MAX_ANCHORS][3];
+  double slope[NKB_MAX_ANCHORS][3];   // (rgb[j+1]-rgb[j]) / (t[j+1]-t[j]), IEEE on the host
 };
 
 // ---- P2P sort-last composite (composite.cu) ----------------------------------

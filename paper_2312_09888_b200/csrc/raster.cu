@@ -36,8 +36,7 @@ __device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double
     if (t == cm.t[j]) {
       v = cm.rgb[j][ch];
     } else {
-      const double slope = __ddiv_rn(__dsub_rn(cm.rgb[j + 1][ch], cm.rgb[j][ch]),
-                                     __dsub_rn(cm.t[j + 1], cm.t[j]));
+      const double slope = cm.slope[j][ch];      // host-precomputed, same IEEE division
       v = __dadd_rn(__dmul_rn(slope, __dsub_rn(t, cm.t[j])), cm.rgb[j][ch]);
     }
   }
