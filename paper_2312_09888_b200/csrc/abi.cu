@@ -82,10 +82,19 @@ static void p2p_release(nkb_ctx* ctx) {
   cudaFree(ctx->p2p.keys[1]);
   cudaFree(ctx->p2p.flags);
   cudaFree(ctx->p2p.err);
+  cudaFree(ctx->p2p.dev_epoch);
+  cudaFreeHost(ctx->p2p.h_res);
   ctx->p2p.keys[0] = ctx->p2p.keys[1] = nullptr;
   ctx->p2p.flags = nullptr;
   ctx->p2p.err = nullptr;
+  ctx->p2p.dev_epoch = nullptr;
+  ctx->p2p.h_res = nullptr;
   ctx->p2p.ready = false;
+  for (int k = 0; k < 2; ++k) {                       // captured steps reference these buffers
+    if (ctx->graph_exec[k]) cudaGraphExecDestroy(ctx->graph_exec[k]);
+    ctx->graph_exec[k] = nullptr;
+    ctx->graph_key[k].clear();
+  }
 }
 
 // collective: every rank calls it with the same image size.  Allocates the two
@@ -105,6 +114,9 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
   NKB_CUDA(cudaMemset(P.flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)));
   NKB_CUDA(cudaMalloc(&P.err, sizeof(int)));
   NKB_CUDA(cudaMemset(P.err, 0, sizeof(int)));
+  NKB_CUDA(cudaMalloc(&P.dev_epoch, sizeof(unsigned long long)));
+  NKB_CUDA(cudaMemset(P.dev_epoch, 0, sizeof(unsigned long long)));
+  NKB_CUDA(cudaMallocHost(&P.h_res, (1 + kMaxRanks) * sizeof(unsigned long long)));
   constexpr int kH = 5;
   cudaIpcMemHandle_t mine[kH];
   void* ptrs[kH] = {P.keys[0], P.keys[1], P.flags, ctx->rgba, ctx->depth};
@@ -230,7 +242,8 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
     if (kv.second) stats_tables_free(*kv.second);
   gs_free(ctx->gs);
   cudaFree(ctx->tr_buf);
-  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  for (int k = 0; k < 2; ++k)
+    if (ctx->graph_exec[k]) cudaGraphExecDestroy(ctx->graph_exec[k]);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   cudaFree(ctx->dq);
   cudaFree(ctx->dw);
@@ -680,7 +693,7 @@ static int ensure_tri(nkb_ctx* ctx, int64_t cap, bool meta) {
 // (or count/scan/ordered emit) -> zbuf clear -> raster -> range words ->
 // composite -> resolve -> D2H of the report words.
 static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm, cudaStream_t s,
-                        bool composite, bool ordered, int* p2p_err, unsigned long long* tri_by_rank) {
+                        bool composite, bool ordered, unsigned long long ep) {
   const bool timing = p->timing != 0;
   const int64_t npx = (int64_t)p->width * p->height;
   fp.tri = ctx->tri;
@@ -722,10 +735,8 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   const bool p2p = composite && ctx->p2p.ready;
   unsigned long long* zbuf = ctx->zbuf;
   P2PParams pp;
-  unsigned long long ep = 0;
   if (p2p) {
     auto& P = ctx->p2p;
-    ep = ++P.epoch;
     memset(&pp, 0, sizeof(pp));
     pp.rank = ctx->rank;
     pp.nranks = ctx->nranks;
@@ -745,9 +756,11 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     pp.root_depth = P.root_depth;
     pp.range_out = ctx->range_dev;
     pp.err = P.err;
+    pp.dev_epoch = P.dev_epoch;
     zbuf = P.keys[ep & 1];
+    NKB_TRY(launch_p2p_epoch(pp, s));                // device epoch := ep
     // every peer has finished reading this key buffer (epoch ep-2) before it is cleared
-    if (ep > 2) NKB_TRY(launch_p2p_wait(pp, 1, ep - 2, s));
+    NKB_TRY(launch_p2p_wait(pp, 1, 2, s));
   }
   NKB_TRY(launch_zbuf_clear(zbuf, npx, s));
   RasterParams rp;
@@ -770,10 +783,10 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[2], s));
   if (p2p) {
     // fused sort-last composite + resolve over NVLink peer memory
-    NKB_TRY(launch_p2p_signal(pp, 0, ep, nullptr, s));
-    NKB_TRY(launch_p2p_composite(pp, ep, s));
-    NKB_TRY(launch_p2p_signal(pp, 1, ep, ctx->counters, s));
-    if (ctx->rank == 0) NKB_TRY(launch_p2p_wait(pp, 1, ep, s));
+    NKB_TRY(launch_p2p_signal(pp, 0, nullptr, s));
+    NKB_TRY(launch_p2p_composite(pp, s));
+    NKB_TRY(launch_p2p_signal(pp, 1, ctx->counters, s));
+    if (ctx->rank == 0) NKB_TRY(launch_p2p_wait(pp, 1, 0, s));
   } else if (composite) {
     NKB_NCCL(g_nccl.GroupStart());
     NKB_NCCL(g_nccl.Reduce(ctx->zbuf, ctx->zbuf, (size_t)npx + 2, ncclUint64, ncclMin, 0, ctx->comm, s));
@@ -806,9 +819,9 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 8, ctx->region_count,
                              sizeof(unsigned long long) * ctx->n_regions, cudaMemcpyDeviceToHost, s));
   if (p2p) {
-    NKB_CUDA(cudaMemcpyAsync(p2p_err, ctx->p2p.err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    NKB_CUDA(cudaMemcpyAsync(tri_by_rank, ctx->p2p.flags + 2 * kMaxRanks, sizeof(unsigned long long) * kMaxRanks,
-                             cudaMemcpyDeviceToHost, s));
+    NKB_CUDA(cudaMemcpyAsync(ctx->p2p.h_res, ctx->p2p.err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NKB_CUDA(cudaMemcpyAsync(ctx->p2p.h_res + 1, ctx->p2p.flags + 2 * kMaxRanks,
+                             sizeof(unsigned long long) * kMaxRanks, cudaMemcpyDeviceToHost, s));
   }
   return NKB_OK;
 }
@@ -831,14 +844,16 @@ static std::string step_key(nkb_ctx* ctx, const nkb_pipeline* p, const FusedPara
 
 static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
                     cudaStream_t s, bool composite, bool ordered) {
-  int p2p_err = 0;
-  unsigned long long tri_by_rank[kMaxRanks] = {};
   const bool p2p = composite && ctx->p2p.ready;
-  // Single-rank steps replay a CUDA graph of the whole launch sequence (one
-  // launch instead of ~10), re-captured whenever a parameter changes.
+  const unsigned long long ep = p2p ? ++ctx->p2p.epoch : 0;   // the device counter follows in-stream
+  // Steps replay a CUDA graph of the whole launch sequence (one launch
+  // instead of ~10-14), re-captured whenever a parameter changes.  With the
+  // P2P composite the epoch lives on the device and only the key-buffer
+  // parity alternates, so two graphs cover every step; the NCCL composite
+  // path stays eager.
   static const bool graphs = !(getenv("NKB_GRAPHS") && strcmp(getenv("NKB_GRAPHS"), "0") == 0);
   // (per-stage timing keeps the eager path: its events bracket the stages)
-  if (graphs && !composite && fp.prof == nullptr && !p->timing) {
+  if (graphs && (!composite || p2p) && fp.prof == nullptr && !p->timing) {
     if (ordered && ctx->elem_cap < ctx->E) {       // (allocation happens outside the capture)
       cudaFree(ctx->elem_count);
       cudaFree(ctx->elem_offset);
@@ -849,31 +864,38 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
       ctx->elem_cap = ctx->E;
     }
     NKB_TRY(launch_fused_prepare());
-    const std::string key = step_key(ctx, p, fp, cm, ordered);
-    if (!ctx->graph_exec || key != ctx->graph_key) {
-      if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
-      ctx->graph_exec = nullptr;
+    const int slot = (int)(ep & 1);
+    std::string key = step_key(ctx, p, fp, cm, ordered);
+    if (p2p) {
+      const void* pk[] = {ctx->p2p.keys[0], ctx->p2p.keys[1], ctx->p2p.flags, ctx->p2p.dev_epoch, ctx->p2p.h_res};
+      key.append(reinterpret_cast<const char*>(pk), sizeof(pk));
+      key.push_back((char)slot);
+    }
+    if (!ctx->graph_exec[slot] || key != ctx->graph_key[slot]) {
+      if (ctx->graph_exec[slot]) cudaGraphExecDestroy(ctx->graph_exec[slot]);
+      ctx->graph_exec[slot] = nullptr;
       if (!ctx->cap_stream) NKB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
       NKB_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
-      const int rc = enqueue_step(ctx, p, fp, cm, ctx->cap_stream, composite, ordered, &p2p_err, tri_by_rank);
+      const int rc = enqueue_step(ctx, p, fp, cm, ctx->cap_stream, composite, ordered, ep);
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
       NKB_TRY(rc);
       NKB_CUDA(ce);
-      const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec, g, 0);
+      const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec[slot], g, 0);
       cudaGraphDestroy(g);
       NKB_CUDA(ie);
-      ctx->graph_key = key;
+      ctx->graph_key[slot] = key;
     }
-    NKB_CUDA(cudaGraphLaunch(ctx->graph_exec, s));
+    NKB_CUDA(cudaGraphLaunch(ctx->graph_exec[slot], s));
   } else {
-    NKB_TRY(enqueue_step(ctx, p, fp, cm, s, composite, ordered, &p2p_err, tri_by_rank));
+    NKB_TRY(enqueue_step(ctx, p, fp, cm, s, composite, ordered, ep));
   }
   NKB_CUDA(cudaStreamSynchronize(s));
   if (p2p) {
-    if (p2p_err) return fail(NKB_ENCCL, "P2P composite: timed out waiting for a peer rank");
+    if (*reinterpret_cast<const int*>(ctx->p2p.h_res))
+      return fail(NKB_ENCCL, "P2P composite: timed out waiting for a peer rank");
     unsigned long long tot = 0;
-    for (int q = 0; q < ctx->nranks; ++q) tot += tri_by_rank[q];
+    for (int q = 0; q < ctx->nranks; ++q) tot += ctx->p2p.h_res[1 + q];
     ctx->h_counters[3] = tot;   // meaningful on rank 0 (every rank reports to every rank)
   }
   ctx->last_fast = !ordered;

@@ -87,8 +87,11 @@ __device__ int wait_flags(const unsigned long long* flags, int first, int n, uns
   return 0;
 }
 
-__global__ void signal_kernel(P2PParams p, int which, unsigned long long epoch, const unsigned long long* count) {
+__global__ void epoch_kernel(P2PParams p) { *p.dev_epoch += 1ULL; }
+
+__global__ void signal_kernel(P2PParams p, int which, const unsigned long long* count) {
   // which 0: "keys ready", 1: "done reading peers' keys" (+ this rank's triangle count)
+  const unsigned long long epoch = *p.dev_epoch;
   const int q = threadIdx.x;
   if (q < p.nranks) {
     if (count) p.peer_flags[q][2 * kMaxRanks + p.rank] = *count;
@@ -97,11 +100,14 @@ __global__ void signal_kernel(P2PParams p, int which, unsigned long long epoch, 
   }
 }
 
-__global__ void wait_kernel(P2PParams p, int which, unsigned long long target) {
-  if (threadIdx.x == 0) wait_flags(p.flags, which * kMaxRanks, p.nranks, target, p.err);
+// wait until every rank reached (this step's epoch - back)
+__global__ void wait_kernel(P2PParams p, int which, unsigned long long back) {
+  const unsigned long long ep = *p.dev_epoch;
+  if (threadIdx.x == 0 && ep > back) wait_flags(p.flags, which * kMaxRanks, p.nranks, ep - back, p.err);
 }
 
-__global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p, unsigned long long epoch) {
+__global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
+  const unsigned long long epoch = *p.dev_epoch;
   __shared__ int s_ok;
   __shared__ double s_lo, s_hi;
   if (threadIdx.x == 0) {
@@ -152,25 +158,30 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p, unsigne
 
 }  // namespace
 
-int launch_p2p_signal(const P2PParams& p, int which, unsigned long long epoch, const unsigned long long* count,
-                      cudaStream_t s) {
-  signal_kernel<<<1, 32, 0, s>>>(p, which, epoch, count);
+int launch_p2p_epoch(const P2PParams& p, cudaStream_t s) {
+  epoch_kernel<<<1, 1, 0, s>>>(p);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
 
-int launch_p2p_wait(const P2PParams& p, int which, unsigned long long target, cudaStream_t s) {
-  wait_kernel<<<1, 32, 0, s>>>(p, which, target);
+int launch_p2p_signal(const P2PParams& p, int which, const unsigned long long* count, cudaStream_t s) {
+  signal_kernel<<<1, 32, 0, s>>>(p, which, count);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
 
-int launch_p2p_composite(const P2PParams& p, unsigned long long epoch, cudaStream_t s) {
+int launch_p2p_wait(const P2PParams& p, int which, unsigned long long back, cudaStream_t s) {
+  wait_kernel<<<1, 32, 0, s>>>(p, which, back);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_p2p_composite(const P2PParams& p, cudaStream_t s) {
   const long long band = (long long)p.width * ((long long)p.height / p.nranks + 1);
   long long blocks = (band + 255) / 256;
   if (blocks > 148 * 4) blocks = 148 * 4;
   if (blocks < 1) blocks = 1;
-  p2p_composite_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, epoch);
+  p2p_composite_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

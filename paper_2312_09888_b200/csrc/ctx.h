@@ -138,8 +138,8 @@ struct nkb_ctx {
   // in transit staging (nkb_transit_gather): the assembled mesh on the endpoint
   double* tr_buf = nullptr;
   int64_t tr_cap = 0;                        // doubles
-  cudaGraphExec_t graph_exec = nullptr;      // captured single-rank step (run_step)
-  std::string graph_key;
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};   // captured steps (by key-buffer parity)
+  std::string graph_key[2];
   cudaStream_t cap_stream = nullptr;
   double* dq = nullptr;                      // continuous pipeline: DSSUM'd Q / |w| scratch
   double* dw = nullptr;
@@ -156,7 +156,9 @@ struct nkb_ctx {
     unsigned long long* peer_flags[kMaxRanks] = {};
     unsigned char* root_rgba = nullptr;
     float* root_depth = nullptr;
-    unsigned long long epoch = 0;
+    unsigned long long epoch = 0;            // host copy of the step epoch
+    unsigned long long* dev_epoch = nullptr; // device counter read by the P2P kernels
+    unsigned long long* h_res = nullptr;     // pinned: [0] timeout flag, [1..] per-rank triangles
   } p2p;
 };
 

@@ -131,11 +131,14 @@ struct P2PParams {
   float* root_depth;
   double* range_out;                                  // local [2]
   int* err;                                           // local: 1 = peer timeout
+  unsigned long long* dev_epoch;                      // local: step epoch (device counter, graph-safe)
 };
-int launch_p2p_signal(const P2PParams& p, int which, unsigned long long epoch, const unsigned long long* count,
-                      cudaStream_t s);
-int launch_p2p_wait(const P2PParams& p, int which, unsigned long long target, cudaStream_t s);
-int launch_p2p_composite(const P2PParams& p, unsigned long long epoch, cudaStream_t s);
+// the epoch lives on the device, so a step's launches are identical every
+// step (CUDA-graph replayable); only the key-buffer parity alternates
+int launch_p2p_epoch(const P2PParams& p, cudaStream_t s);
+int launch_p2p_signal(const P2PParams& p, int which, const unsigned long long* count, cudaStream_t s);
+int launch_p2p_wait(const P2PParams& p, int which, unsigned long long back, cudaStream_t s);
+int launch_p2p_composite(const P2PParams& p, cudaStream_t s);
 
 struct ResolveParams {
   const unsigned long long* zbuf;
