@@ -154,12 +154,13 @@ def lib():
     """Load libnekb200.so (raises if it was not built -- there is no CPU fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("NKB_LIB", LIB_PATH)       # A/B of two builds of the same ABI
+        if not os.path.exists(path):
             raise NativeError(
-                f"{LIB_PATH} is missing; build it with `python -m paper_2312_09888_b200.build` "
+                f"{path} is missing; build it with `python -m paper_2312_09888_b200.build` "
                 "(the GPU path has no CPU fallback)"
             )
-        L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        L = C.CDLL(path, mode=C.RTLD_GLOBAL)
         for name, (argtypes, restype) in _SIGS.items():
             fn = getattr(L, name)
             fn.argtypes = argtypes
