@@ -68,7 +68,7 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
     const long long dy = Y[eb[i]] - Y[ea[i]], dx = X[eb[i]] - X[ea[i]];
     bias[i] = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : -1;   // inclusive (top-left) edges
   }
-  const double dA = (double)area;
+  const double inv = __drcp_rn((double)area);     // == 1.0 / area: one IEEE division per triangle
   for (long long py = py0; py <= py1; ++py) {
     const long long cy = py * 256 + 128;
     for (long long px = px0; px <= px1; ++px) {
@@ -78,14 +78,14 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
       for (int i = 0; i < 3; ++i)
         w[i] = (X[eb[i]] - X[ea[i]]) * (cy - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx - X[ea[i]]);
       if (w[0] + bias[0] < 0 || w[1] + bias[1] < 0 || w[2] + bias[2] < 0) continue;
-      double d = __ddiv_rn(__fma_rn((double)w[2], Z[2],
+      double d = __dmul_rn(__fma_rn((double)w[2], Z[2],
                                     __fma_rn((double)w[1], Z[1], __dmul_rn((double)w[0], Z[0]))),
-                           dA);
+                           inv);
       if (!(d >= 0.0 && d <= 1.0)) continue;
       d = __dadd_rn(d, 0.0);
-      const double c = __ddiv_rn(__fma_rn((double)w[2], C[2],
+      const double c = __dmul_rn(__fma_rn((double)w[2], C[2],
                                           __fma_rn((double)w[1], C[1], __dmul_rn((double)w[0], C[0]))),
-                                 dA);
+                                 inv);
       const unsigned long long key =
           ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
           (unsigned long long)__float_as_uint(__double2float_rn(c));
