@@ -111,6 +111,7 @@ def test_insitu_kind_and_attributes():
     ("<sensei><analysis", "malformed"),
     ("<other/>", "root element"),
     ('<sensei><analysis frequency="1"/></sensei>', "missing 'type'"),
+    ('<sensei><analysis type="stats" frequency="1"/></sensei>', "requires a 'path'"),
 ])
 def test_config_errors(doc, match):
     with pytest.raises(ConfigError, match=match):
@@ -287,3 +288,33 @@ def test_cylinder_mesh_is_curved_and_inside_unit_disk():
     r = np.hypot(c.x, c.y)
     assert r.max() <= 1.0 + 1e-12
     assert c.fields["temperature"].shape == (1, 64 * 512)
+
+
+def test_kinds_of_the_reference_and_the_sem_path():
+    """Every reference sink kind exists (render, stats, checkpoint, null;
+    reference sinks.py:405-410) plus insitu / transit; attributes are
+    filtered per kind like the reference's _KNOWN_ATTRS (bridge.py:34-39)."""
+    from paper_2312_09888_b200.bridge import KINDS
+    from paper_2312_09888_b200.sinks import _SINK_TYPES
+
+    for k in ("render", "stats", "checkpoint", "null", "insitu", "transit"):
+        assert k in KINDS and k in _SINK_TYPES
+    cfg = parse_config('<sensei><analysis type="stats" path="/tmp/x.csv" frequency="3" dir="d"/>'
+                       '<analysis type="checkpoint" dir="ck" format="ascii" arrays="Q" width="5"/>'
+                       '<analysis type="transit" endpoint="1" iso="Q=1" continuous="1"/></sensei>')
+    st, ck, tr = cfg.specs
+    assert st.params == {"path": "/tmp/x.csv"} and st.frequency == 3
+    assert ck.params == {"dir": "ck", "format": "ascii", "arrays": "Q"}
+    assert tr.params == {"endpoint": "1", "iso": "Q=1"}          # continuous is an insitu-only attribute
+
+
+def test_stats_and_checkpoint_sinks_construct_without_gpu(tmp_path):
+    """Constructing sinks needs no GPU (only consume does), and output
+    locations are probed like the reference's (_probe_writable)."""
+    from paper_2312_09888_b200.sinks import CheckpointSink, StatsSink
+
+    StatsSink({"path": str(tmp_path / "a" / "s.csv")})
+    assert (tmp_path / "a" / "s.csv").read_text() == "step,time,field,min,max,mean\n"
+    CheckpointSink({"dir": str(tmp_path / "ck")})
+    with pytest.raises(ValueError, match="ascii or binary"):
+        CheckpointSink({"dir": str(tmp_path / "ck"), "format": "hdf5"})
