@@ -25,6 +25,7 @@
 #include <math.h>
 
 #include "nkb_internal.h"
+#include "raster_dev.cuh"
 
 namespace nkb {
 
@@ -44,32 +45,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ double dec_ordered(unsigned long long u) {
-  unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
-  return __longlong_as_double((long long)b);
-}
-
-// same np.interp + floor(v + 0.5) rule as raster.cu resolve (sinks.py:201-209)
-__device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double t, int ch) {
-  if (t != t) return 0;
-  const int n = cm.n;
-  double v;
-  if (t >= cm.t[n - 1]) {
-    v = cm.rgb[n - 1][ch];
-  } else {
-    int j = 0;
-    for (int k = 1; k < n - 1; ++k)
-      if (t >= cm.t[k]) j = k;
-    if (t == cm.t[j]) {
-      v = cm.rgb[j][ch];
-    } else {
-      const double slope = cm.slope[j][ch];      // host-precomputed, same IEEE division
-      v = __dadd_rn(__dmul_rn(slope, __dsub_rn(t, cm.t[j])), cm.rgb[j][ch]);
-    }
-  }
-  return (unsigned char)floor(__dadd_rn(v, 0.5));
 }
 
 // wait until flags[first .. first+n) >= target (all peers); 0 = ok, 1 = timeout
@@ -120,8 +95,8 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
       wmax = min(wmax, z[p.npx + 1]);
     }
     double lo = p.vmin, hi = p.vmax;
-    if (!(lo == lo)) lo = (wmin == ~0ULL) ? 0.0 : dec_ordered(wmin);
-    if (!(hi == hi)) hi = (~wmax == 0ULL) ? 0.0 : dec_ordered(~wmax);
+    if (!(lo == lo)) lo = (wmin == ~0ULL) ? 0.0 : rdev::dec_ordered(wmin);
+    if (!(hi == hi)) hi = (~wmax == 0ULL) ? 0.0 : rdev::dec_ordered(~wmax);
     s_lo = lo;
     s_hi = hi;
     if (blockIdx.x == 0 && p.range_out) {
@@ -149,7 +124,7 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
       dep = __uint_as_float((unsigned)(key >> 32));
       double t = hi > lo ? __ddiv_rn(__dsub_rn(s, lo), span) : 0.0;
       t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
-      o = make_uchar4(cmap_channel(p.cmap, t, 0), cmap_channel(p.cmap, t, 1), cmap_channel(p.cmap, t, 2), 255);
+      o = make_uchar4(rdev::cmap_channel(p.cmap, t, 0), rdev::cmap_channel(p.cmap, t, 1), rdev::cmap_channel(p.cmap, t, 2), 255);
     }
     reinterpret_cast<uchar4*>(p.root_rgba)[i] = o;
     p.root_depth[i] = dep;

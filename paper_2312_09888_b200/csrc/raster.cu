@@ -17,32 +17,6 @@ namespace nkb {
 
 namespace {
 
-__device__ __forceinline__ double dec_ordered(unsigned long long u) {
-  unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
-  return __longlong_as_double((long long)b);
-}
-
-// np.interp on clipped t, then floor(v + 0.5) -> uint8 (sinks.py:201-209)
-__device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double t, int ch) {
-  if (t != t) return 0;
-  const int n = cm.n;
-  double v;
-  if (t >= cm.t[n - 1]) {
-    v = cm.rgb[n - 1][ch];
-  } else {
-    int j = 0;
-    for (int k = 1; k < n - 1; ++k)
-      if (t >= cm.t[k]) j = k;
-    if (t == cm.t[j]) {
-      v = cm.rgb[j][ch];
-    } else {
-      const double slope = cm.slope[j][ch];      // host-precomputed, same IEEE division
-      v = __dadd_rn(__dmul_rn(slope, __dsub_rn(t, cm.t[j])), cm.rgb[j][ch]);
-    }
-  }
-  return (unsigned char)floor(__dadd_rn(v, 0.5));
-}
-
 __device__ __forceinline__ double clip01(double t) { return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t); }
 
 __global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
@@ -74,8 +48,8 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
   double lo = p.vmin, hi = p.vmax;
   if (p.range_words) {
     const unsigned long long w0 = p.range_words[0], w1 = ~p.range_words[1];
-    if (!(lo == lo)) lo = (w0 == ~0ULL) ? 0.0 : dec_ordered(w0);
-    if (!(hi == hi)) hi = (w1 == 0ULL) ? 0.0 : dec_ordered(w1);
+    if (!(lo == lo)) lo = (w0 == ~0ULL) ? 0.0 : rdev::dec_ordered(w0);
+    if (!(hi == hi)) hi = (w1 == 0ULL) ? 0.0 : rdev::dec_ordered(w1);
   }
   const long long n = (long long)p.width * p.height;
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.range_out) {
@@ -95,8 +69,8 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
       const double s = (double)__uint_as_float((unsigned)(key & 0xffffffffULL));
       dep = __uint_as_float((unsigned)(key >> 32));
       const double t = clip01(hi > lo ? __ddiv_rn(__dsub_rn(s, lo), span) : 0.0);
-      o = make_uchar4(cmap_channel(p.cmap, t, 0), cmap_channel(p.cmap, t, 1),
-                      cmap_channel(p.cmap, t, 2), 255);
+      o = make_uchar4(rdev::cmap_channel(p.cmap, t, 0), rdev::cmap_channel(p.cmap, t, 1),
+                      rdev::cmap_channel(p.cmap, t, 2), 255);
     }
     reinterpret_cast<uchar4*>(p.rgba)[i] = o;
     if (p.depth) p.depth[i] = dep;
@@ -145,8 +119,8 @@ __global__ void __launch_bounds__(256) structured_minmax_kernel(const Structured
 
 __global__ void __launch_bounds__(256) structured_render_kernel(const StructuredParams p) {
   double lo = p.vmin, hi = p.vmax;
-  if (!(lo == lo)) lo = dec_ordered(p.minmax[0]);
-  if (!(hi == hi)) hi = dec_ordered(p.minmax[1]);
+  if (!(lo == lo)) lo = rdev::dec_ordered(p.minmax[0]);
+  if (!(hi == hi)) hi = rdev::dec_ordered(p.minmax[1]);
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.range_out) {
     p.range_out[0] = lo;
     p.range_out[1] = hi;
@@ -177,9 +151,9 @@ __global__ void __launch_bounds__(256) structured_render_kernel(const Structured
     s = __dadd_rn(s, __dmul_rn(__dmul_rn(t10, ay), omax));
     s = __dadd_rn(s, __dmul_rn(__dmul_rn(t11, ay), ax));
     const double t = clip01(s);
-    p.rgb[3 * i + 0] = cmap_channel(p.cmap, t, 0);
-    p.rgb[3 * i + 1] = cmap_channel(p.cmap, t, 1);
-    p.rgb[3 * i + 2] = cmap_channel(p.cmap, t, 2);
+    p.rgb[3 * i + 0] = rdev::cmap_channel(p.cmap, t, 0);
+    p.rgb[3 * i + 1] = rdev::cmap_channel(p.cmap, t, 1);
+    p.rgb[3 * i + 2] = rdev::cmap_channel(p.cmap, t, 2);
   }
 }
 

@@ -1,14 +1,48 @@
-// One triangle into the packed depth|scalar key buffer: the raster step of
-// K2 (raster.cu runs one thread per triangle).  16.8 fixed-point edge
-// functions with a top-left rule,
-// sampling at pixel centres, depth clipped to [0, 1], order-independent
-// atomicMin; oracle/sem_oracle.c restates it operation for operation.
+// Device helpers of the image kernels (raster.cu, composite.cu):
+//  * raster_triangle: one triangle into the packed depth|scalar key buffer
+//    (the raster step of K2, one thread per triangle) -- 16.8 fixed-point
+//    edge functions with a top-left rule, sampling at pixel centres, depth
+//    clipped to [0, 1], order-independent atomicMin;
+//  * dec_ordered / cmap_channel: the colour-range decoding and the colormap.
+// oracle/sem_oracle.c restates them operation for operation.
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
+
+#include "nkb_internal.h"
 
 namespace nkb {
 namespace rdev {
+
+// inverse of the order-preserving encoding of doubles used by the colour-range words
+__device__ __forceinline__ double dec_ordered(unsigned long long u) {
+  unsigned long long b = (u & 0x8000000000000000ULL) ? (u & 0x7fffffffffffffffULL) : ~u;
+  return __longlong_as_double((long long)b);
+}
+
+// np.interp on clipped t, then floor(v + 0.5) -> uint8 (sinks.py:201-209);
+// shared by K3 resolve, the structured renderer and the P2P composite
+__device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double t, int ch) {
+  if (t != t) return 0;
+  const int n = cm.n;
+  double v;
+  if (t >= cm.t[n - 1]) {
+    v = cm.rgb[n - 1][ch];
+  } else {
+    int j = 0;
+    for (int k = 1; k < n - 1; ++k)
+      if (t >= cm.t[k]) j = k;
+    if (t == cm.t[j]) {
+      v = cm.rgb[j][ch];
+    } else {
+      const double slope = cm.slope[j][ch];      // host-precomputed, same IEEE division
+      v = __dadd_rn(__dmul_rn(slope, __dsub_rn(t, cm.t[j])), cm.rgb[j][ch]);
+    }
+  }
+  return (unsigned char)floor(__dadd_rn(v, 0.5));
+}
+
 
 constexpr double kGuard = 32768.0;   // |screen coordinate| bound in pixels
 
