@@ -99,6 +99,9 @@ typedef struct {
     int          continuous;                       /* 1: DSSUM-average derived sources (Q, vorticity:mag)
                                                       before surfaces / colour (C0 across element faces);
                                                       needs nkb_mesh_set_global_ids */
+    /* perspective: w = persp . (x, y, z, 1) and (col, row, depth) = view * (x, y, z, 1) / w
+       (vertices with w <= 0 drop their triangle); all zero = orthographic (no division) */
+    double       persp[4];
 } nkb_pipeline;
 
 typedef struct {

@@ -168,9 +168,19 @@ def mc(cf: CaseFields, surfaces, color: str, cases: bool = False):
     return out + ((cs,) if cases else ())
 
 
-def raster(tri: np.ndarray, view, W: int, H: int, zbuf: np.ndarray | None = None) -> np.ndarray:
+def _view16(view, persp=None) -> np.ndarray:
+    """3x4 view rows + perspective row (zeros = orthographic), as orc_raster takes them."""
+    v = np.zeros(16)
+    a = np.asarray(view, dtype=np.float64).ravel()
+    v[:a.size] = a                                  # 12 values, or 16 with the perspective row
+    if persp is not None:
+        v[12:] = np.asarray(persp, dtype=np.float64)
+    return v
+
+
+def raster(tri: np.ndarray, view, W: int, H: int, zbuf: np.ndarray | None = None, persp=None) -> np.ndarray:
     t = np.ascontiguousarray(tri, dtype=np.float32)
-    V = np.ascontiguousarray(view, dtype=np.float64)
+    V = _view16(view, persp)
     if zbuf is None:
         zbuf = np.empty(W * H, np.uint64)
         lib().orc_zbuf_clear(_p(zbuf), W * H)
@@ -222,11 +232,11 @@ def render_structured(blocks, rows: int, comps: int, mode: int, W: int, H: int, 
 
 
 def pipeline_mt(cf: CaseFields, surfaces, color, view, W, H, nthreads: int, vmin=None, vmax=None,
-                anchors=DEFAULT_ANCHORS, bg=(0, 0, 0, 0)):
+                anchors=DEFAULT_ANCHORS, bg=(0, 0, 0, 0), persp=None):
     """Full step on `nthreads` CPU threads -> (rgba, depth, ntri, range)."""
     f = cf.native(surfaces, color)
     n, ts, rgb = _anchors(anchors)
-    V = np.ascontiguousarray(view, dtype=np.float64)
+    V = _view16(view, persp)
     out = np.empty((H, W, 4), np.uint8)
     dep = np.empty((H, W), np.float32)
     b = np.array(bg, np.uint8)

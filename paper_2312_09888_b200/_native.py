@@ -55,6 +55,7 @@ class NkbPipeline(C.Structure):
         ("composite", C.c_int),
         ("timing", C.c_int),
         ("continuous", C.c_int),
+        ("persp", C.c_double * 4),
     ]
 
 

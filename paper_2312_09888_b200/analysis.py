@@ -44,8 +44,10 @@ class Pipeline:
     color_field: str = "velocity:mag"
     width: int = 256
     height: int = 256
-    view: tuple[float, ...] | None = None     # 3x4 row-major; None -> auto (fit bounds)
+    view: tuple[float, ...] | None = None     # 3x4 row-major (+ perspective row: 16); None -> auto
     view_dir: tuple[float, float] = (0.0, 90.0)   # azimuth, elevation (deg) for auto
+    projection: str = "ortho"                 # auto camera: "ortho" or "perspective"
+    fov: float = 30.0                         # perspective: vertical field of view (deg)
     vmin: float | None = None
     vmax: float | None = None
     anchors: tuple = DEFAULT_ANCHORS
@@ -74,8 +76,12 @@ class Pipeline:
                 ns.normal[a] = float(s.normal[a])
         p.color_field = self.color_field.encode()
         p.width, p.height = int(self.width), int(self.height)
-        for i, v in enumerate(view):
-            p.view[i] = float(v)
+        if len(view) not in (12, 16):
+            raise ValueError("view must have 12 values (3x4) or 16 (3x4 + perspective row)")
+        for i in range(12):
+            p.view[i] = float(view[i])
+        for i in range(4):
+            p.persp[i] = float(view[12 + i]) if len(view) == 16 else 0.0
         p.vmin = math.nan if self.vmin is None else float(self.vmin)
         p.vmax = math.nan if self.vmax is None else float(self.vmax)
         if tuple(self.anchors) == DEFAULT_ANCHORS:
@@ -120,6 +126,37 @@ def ortho_view(bounds, width: int, height: int, azimuth: float = 0.0, elevation:
     row1 = np.concatenate([-s * up, [height / 2.0 + s * up.dot(c)]])
     row2 = np.concatenate([fwd / (2.0 * r), [0.5 - fwd.dot(c) / (2.0 * r)]])
     return tuple(float(v) for v in np.concatenate([row0, row1, row2]))
+
+
+def perspective_view(bounds, width: int, height: int, azimuth: float = 0.0, elevation: float = 90.0,
+                     fov: float = 30.0, margin: float = 1.05) -> tuple[float, ...]:
+    """16 values: the 3x4 rows and the w row of a pinhole camera that sees
+    the bounding sphere of `bounds` in a `fov`-degree cone from direction
+    (azimuth, elevation).  (col, row, depth) = rows . X / (w . X): depth is
+    0 on the near and 1 on the far side of the sphere, row 0 is the top."""
+    b = np.asarray(bounds, dtype=np.float64)
+    c = np.array([(b[0] + b[1]) / 2, (b[2] + b[3]) / 2, (b[4] + b[5]) / 2])
+    r = 0.5 * math.sqrt((b[1] - b[0]) ** 2 + (b[3] - b[2]) ** 2 + (b[5] - b[4]) ** 2)
+    r = max(r, 1e-300) * margin
+    half = math.radians(fov) / 2.0
+    az, el = math.radians(azimuth), math.radians(elevation)
+    d = np.array([math.cos(el) * math.cos(az), math.cos(el) * math.sin(az), math.sin(el)])
+    dist = r / math.sin(half)
+    eye = c + dist * d
+    fwd = -d
+    up0 = np.array([0.0, 1.0, 0.0]) if abs(d[2]) > 0.999 else np.array([0.0, 0.0, 1.0])
+    right = np.cross(fwd, up0)
+    right /= np.linalg.norm(right)
+    up = np.cross(right, fwd)
+    f = 0.5 * min(width, height) / math.tan(half)
+    near, far = dist - r, dist + r
+    A, B = far / (far - near), -near * far / (far - near)
+    # camera coordinates: xc = right.(X-eye), yc = up.(X-eye), zc = fwd.(X-eye) (> 0 in front)
+    rows = [f * right + 0.5 * width * fwd, -f * up + 0.5 * height * fwd, A * fwd]
+    offs = [-rows[0].dot(eye), -rows[1].dot(eye), -rows[2].dot(eye) + B]
+    wrow = np.concatenate([fwd, [-fwd.dot(eye)]])
+    out = np.concatenate([np.concatenate([rows[i], [offs[i]]]) for i in range(3)] + [wrow])
+    return tuple(float(v) for v in out)
 
 
 _AXES = {"x": (1.0, 0.0, 0.0), "y": (0.0, 1.0, 0.0), "z": (0.0, 0.0, 1.0)}
@@ -167,6 +204,8 @@ def pipeline_from_params(params: dict[str, str]) -> Pipeline:
         vmax=float(params["vmax"]) if "vmax" in params else None,
         composite=params.get("composite", "1") not in ("0", "false", "no"),
         continuous=params.get("continuous", "0") in ("1", "true", "yes"),
+        projection=params.get("projection", "ortho"),
+        fov=float(params.get("fov", 30.0)),
     )
 
 
@@ -195,7 +234,12 @@ class InsituAnalysis:
             return tuple(p.view)
         if self._view is None:
             b = data_adaptor.ctx.bounds()
-            self._view = ortho_view(b, p.width, p.height, *p.view_dir)
+            if p.projection == "perspective":
+                self._view = perspective_view(b, p.width, p.height, *p.view_dir, fov=p.fov)
+            elif p.projection == "ortho":
+                self._view = ortho_view(b, p.width, p.height, *p.view_dir)
+            else:
+                raise ValueError(f"projection must be 'ortho' or 'perspective', got {p.projection!r}")
         return self._view
 
     def reset_view(self) -> None:

@@ -34,9 +34,9 @@ log = logging.getLogger(__name__)
 _ATTRS_BY_KIND: dict[str, frozenset[str]] = {
     "render": frozenset({"dir", "width", "height", "field", "vmin", "vmax"}),
     "insitu": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
-                         "velocity", "composite", "continuous"}),
+                         "velocity", "composite", "continuous", "projection", "fov"}),
     "transit": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
-                          "velocity", "endpoint"}),
+                          "velocity", "endpoint", "projection", "fov"}),
     "stats": frozenset({"path"}),
     "checkpoint": frozenset({"dir", "format", "arrays"}),
     "null": frozenset(),

@@ -774,7 +774,8 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     rp.n_regions = ctx->n_regions;
     rp.region_cap = ctx->region_cap;
   }
-  memcpy(rp.view, p->view, sizeof(rp.view));
+  memcpy(rp.view, p->view, 12 * sizeof(double));
+  memcpy(rp.view + 12, p->persp, 4 * sizeof(double));
   rp.width = p->width;
   rp.height = p->height;
   rp.zbuf = zbuf;
@@ -986,6 +987,8 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     return fail(NKB_EINVAL, "n_surfaces must be in [0, 4]");
   for (int i = 0; i < 12; ++i)
     if (!isfinite(p->view[i])) return fail(NKB_EINVAL, "view matrix must be finite");
+  for (int i = 0; i < 4; ++i)
+    if (!isfinite(p->persp[i])) return fail(NKB_EINVAL, "perspective row must be finite");
   cudaStream_t s = (cudaStream_t)stream;
 
   FusedParams fp;

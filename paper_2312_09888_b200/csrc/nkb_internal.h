@@ -103,7 +103,7 @@ struct RasterParams {
   const unsigned long long* region_count;   // [n_regions] triangles in each region
   int n_regions;
   int64_t region_cap;               // region r = tri[r*region_cap, r*region_cap + count)
-  double view[12];
+  double view[16];                  // 3x4 view rows + perspective row (all zero: orthographic)
   int width, height;
   unsigned long long* zbuf;
 };

@@ -65,11 +65,21 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
   long long X[3], Y[3];
   double Z[3], C[3];
   bool ok = true;
+  const bool persp = view[12] != 0.0 || view[13] != 0.0 || view[14] != 0.0 || view[15] != 0.0;
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     const float4 v = tri[q];
     double sx, sy, sz;
     xform(view, (double)v.x, (double)v.y, (double)v.z, sx, sy, sz);
+    if (persp) {                                   // perspective divide (w > 0 in front)
+      const double* P = view + 12;
+      const double w = __dadd_rn(__fma_rn(P[2], (double)v.z, __fma_rn(P[1], (double)v.y, __dmul_rn(P[0], (double)v.x))),
+                                 P[3]);
+      if (!(w > 0.0)) ok = false;
+      sx = __ddiv_rn(sx, w);
+      sy = __ddiv_rn(sy, w);
+      sz = __ddiv_rn(sz, w);
+    }
     if (!(fabs(sx) <= kGuard && fabs(sy) <= kGuard && sz == sz && v.w == v.w)) ok = false;
     X[q] = __double2ll_rn(__dmul_rn(sx, 256.0));
     Y[q] = __double2ll_rn(__dmul_rn(sy, 256.0));

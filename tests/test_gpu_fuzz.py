@@ -35,13 +35,15 @@ def scenarios(draw):
     color = draw(st.sampled_from(["temperature", "Q", "vorticity:mag", "velocity:mag"]))
     w, h = draw(st.integers(1, 96)), draw(st.integers(1, 96))
     az, el = draw(st.floats(-180, 180)), draw(st.floats(-80, 80))
-    return nel, seed, kinds, color, w, h, az, el
+    proj = draw(st.sampled_from(["ortho", "perspective"]))
+    fov = draw(st.floats(5.0, 120.0))
+    return nel, seed, kinds, color, w, h, az, el, proj, fov
 
 
 @settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck))
 @given(scenarios())
 def test_random_pipelines_bit_exact(sc):
-    nel, seed, kinds, color, w, h, az, el = sc
+    nel, seed, kinds, color, w, h, az, el, proj, fov = sc
     case = synth.box(nel=nel, seed=seed)
     rng = np.random.default_rng(seed)
     surfaces, orc = [], []
@@ -67,7 +69,7 @@ def test_random_pipelines_bit_exact(sc):
                    for k, v in case.fields.items())
     da.initialize(Snapshot(0.0, 0, 0, (SemBlock(case.n_elements, case.x, case.y, case.z, fields=fields),)))
     pipe = Pipeline(surfaces=tuple(surfaces), color_field=color, width=w, height=h, view_dir=(az, el),
-                    emit_meta=True)
+                    emit_meta=True, projection=proj, fov=fov)
     res = InsituAnalysis(pipe).execute(da, depth=True)
     cf = O.CaseFields(case.x, case.y, case.z, case.fields)
     tri, meta, (cmin, cmax) = O.mc(cf, orc, color)

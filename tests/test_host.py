@@ -318,3 +318,28 @@ def test_stats_and_checkpoint_sinks_construct_without_gpu(tmp_path):
     CheckpointSink({"dir": str(tmp_path / "ck")})
     with pytest.raises(ValueError, match="ascii or binary"):
         CheckpointSink({"dir": str(tmp_path / "ck"), "format": "hdf5"})
+
+
+def test_perspective_view_maps_sphere_into_image():
+    """The pinhole camera puts the bounds' centre at the image centre with a
+    depth in (0, 1), the nearest / farthest points of the bounding sphere at
+    depth ~0 / ~1, and keeps +z up for an elevation of 0."""
+    import math
+
+    from paper_2312_09888_b200.analysis import perspective_view
+
+    b = (0.0, 2.0, -1.0, 1.0, 0.0, 1.0)
+    v = np.array(perspective_view(b, 200, 100, azimuth=30.0, elevation=0.0, fov=40.0, margin=1.0))
+    V, P = v[:12].reshape(3, 4), v[12:]
+
+    def proj(x):
+        h = np.append(x, 1.0)
+        return V @ h / (P @ h)
+
+    c = np.array([1.0, 0.0, 0.5])
+    sx, sy, sz = proj(c)
+    assert abs(sx - 100) < 1e-9 and abs(sy - 50) < 1e-9 and 0 < sz < 1
+    r = 0.5 * math.sqrt(4 + 4 + 1)
+    d = np.array([math.cos(math.radians(30)), math.sin(math.radians(30)), 0.0])
+    assert abs(proj(c + r * d)[2]) < 1e-12 and abs(proj(c - r * d)[2] - 1.0) < 1e-12
+    assert proj(c + [0, 0, 0.4])[1] < sy                       # higher z -> smaller row (up)
