@@ -177,3 +177,14 @@ def test_gpu_colormap_equals_np_interp_on_2m_samples(ctx):
     for ch, col in enumerate(((59, 255, 180), (76, 255, 4), (192, 255, 38))):
         exp[..., ch] = np.floor(np.interp(tc, [0.0, 0.5, 1.0], col) + 0.5).astype(np.uint8)
     assert np.array_equal(img, exp), int((img != exp).any(-1).sum())
+
+
+def test_device_memory_flat_over_many_steps():
+    """insitu + stats + checkpoint sinks for 60 steps: no per-step device
+    allocations leak (tools/soak.py runs the long version)."""
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, "tools/soak.py", "60"], capture_output=True, text=True,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.returncode == 0 and "soak ok" in r.stdout, r.stdout + r.stderr
