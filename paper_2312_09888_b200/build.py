@@ -74,6 +74,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
         run([cc, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-cudart", "static"])
+    # the plain-C usage example (examples/insitu_c_api.c), linked against the library
+    ex_src = os.path.join(ROOT, "examples", "insitu_c_api.c")
+    ex_bin = os.path.join(LIBDIR, "insitu_c_api")
+    if os.path.exists(ex_src) and (force or _stale(ex_bin, [ex_src, LIB, os.path.join(ROOT, "include", "nekb200.h")])):
+        run([shutil.which("gcc") or "gcc", "-O2", "-std=c11", "-I", os.path.join(ROOT, "include"), ex_src,
+             "-o", ex_bin, "-L", LIBDIR, "-lnekb200", "-Wl,-rpath,$ORIGIN", "-lm"])
     return LIB
 
 
