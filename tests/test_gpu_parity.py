@@ -327,3 +327,34 @@ def test_errors_map_to_reference_exceptions(ctx):
         an.execute(da)
     with pytest.raises(ValueError, match="order"):
         ctx.mesh_set(1, 0, 0, 0, order=5)
+
+
+def test_abi_error_paths(ctx):
+    """Argument and state errors of the newer entry points map to the
+    reference's exception vocabulary (ValueError / RuntimeError)."""
+    import ctypes as C
+
+    from paper_2312_09888_b200 import _native as N
+    from paper_2312_09888_b200.device import DeviceArray
+
+    case = synth.box(nel=(1, 1, 1))
+    da = SemDataAdaptor(ctx)
+    da.initialize(_snapshot(case))
+    d = DeviceArray.empty(ctx, (8,), np.float64)
+    with pytest.raises(ValueError, match="segment shape"):
+        ctx.stats([(d.ptr, 4, 0, 4)])
+    with pytest.raises(ValueError, match="comp_stride"):
+        ctx.stats([(d.ptr, 4, 2, 3)])
+    n = C.c_int64()
+    with pytest.raises(ValueError, match="too small"):
+        N.call("nkb_encode_be", ctx.handle, b"POINTS", d.ptr, 8, C.byref(n), None)
+    with pytest.raises(ValueError, match="no field named"):
+        N.call("nkb_encode_be", ctx.handle, b"pressure", None, 0, C.byref(n), None)
+    with pytest.raises(RuntimeError, match="communicator"):
+        ctx.transit_gather(0)
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="temperature",
+                    view=tuple([1.0] * 12) + (0.0, 0.0, float("nan"), 1.0))
+    with pytest.raises(ValueError, match="perspective row"):
+        InsituAnalysis(pipe).execute(da)
+    with pytest.raises(ValueError, match="12 values"):
+        InsituAnalysis(Pipeline(view=(1.0,) * 13)).execute(da)
