@@ -114,6 +114,8 @@ typedef struct {
     int     reran;                /* 1 if the triangle buffer grew and the step re-ran */
     int     geometry_cached;      /* 1 if the step used the geometry cache */
     float   ms_geometry;          /* time spent (re)building the cache this step (when timing) */
+    int     surface_pass;         /* surface pass that ran: 0 = K1 fused (velocity gradient),
+                                     1 = K1s stream (no gradient; NKB_STREAM=0 forces K1) */
 } nkb_report;
 
 typedef struct {

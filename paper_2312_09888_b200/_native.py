@@ -73,6 +73,7 @@ class NkbReport(C.Structure):
         ("reran", C.c_int),
         ("geometry_cached", C.c_int),
         ("ms_geometry", C.c_float),
+        ("surface_pass", C.c_int),
     ]
 
 

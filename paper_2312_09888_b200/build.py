@@ -20,7 +20,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libnekb200.so")
-SOURCES = ["abi.cu", "abi_collective.cu", "fused.cu", "raster.cu", "composite.cu", "mesh_export.cu", "stats.cu", "dssum.cu", "gll.cpp"]
+SOURCES = ["abi.cu", "abi_collective.cu", "fused.cu", "stream.cu", "raster.cu", "composite.cu", "mesh_export.cu", "stats.cu", "dssum.cu", "gll.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -27,6 +27,7 @@ class Report:
     reran: bool
     geometry_cached: bool = False
     ms_geometry: float = 0.0
+    surface_pass: int = 0          # 0: K1 fused (gradients), 1: K1s stream (no gradient)
 
     @classmethod
     def from_native(cls, r: N.NkbReport) -> "Report":
@@ -35,7 +36,7 @@ class Report:
             (float(r.range[0]), float(r.range[1])),
             (float(r.data_range[0]), float(r.data_range[1])),
             float(r.ms_fused), float(r.ms_raster), float(r.ms_composite), float(r.ms_resolve),
-            bool(r.reran), bool(r.geometry_cached), float(r.ms_geometry),
+            bool(r.reran), bool(r.geometry_cached), float(r.ms_geometry), int(r.surface_pass),
         )
 
 

@@ -838,7 +838,7 @@ static std::string step_key(nkb_ctx* ctx, const nkb_pipeline* p, const FusedPara
   const void* ptrs[] = {ctx->tri, ctx->meta, ctx->zbuf, ctx->rgba, ctx->depth, ctx->counters, ctx->region_count,
                         ctx->elem_count, ctx->elem_offset, ctx->range_dev, ctx->h_counters};
   add(ptrs, sizeof(ptrs));
-  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0};
+  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0, surface_pass_of(fp)};
   add(v, sizeof(v));
   return k;
 }
@@ -1085,6 +1085,7 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     out->data_range[1] = ctx->h_counters[2] == 0ULL ? NAN : dec_ordered_h(ctx->h_counters[2]);
     out->reran = reran;
     out->geometry_cached = ctx->geo_used ? 1 : 0;
+    out->surface_pass = surface_pass_of(fp);
     if (p->timing) {
       if (ctx->geo_built) cudaEventElapsedTime(&out->ms_geometry, ctx->ev[5], ctx->ev[0]);
       cudaEventElapsedTime(&out->ms_fused, ctx->ev[0], ctx->ev[1]);

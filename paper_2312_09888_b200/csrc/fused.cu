@@ -42,10 +42,12 @@
 // an explicit fma()).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #define NKB_MC_NO_HOST_TABLES
 #include "mc_tables.h"
 #include "nkb_internal.h"
+#include "sem_dev.cuh"
 
 namespace nkb {
 
@@ -73,6 +75,8 @@ int set_dmat_constant(const double* dmat) {
 
 namespace {
 
+using namespace dev;
+
 constexpr int kThreads = 512;
 constexpr int kPencilThreads = 384;   // 2 groups x 3 dirs x 64 pencils
 constexpr int kMcThreads = kThreads - kPencilThreads;   // 128
@@ -90,15 +94,6 @@ __device__ __forceinline__ int sw(int i, int j, int k) {
 }
 __device__ __forceinline__ int sw_node(int n) { return sw(n & 7, (n >> 3) & 7, n >> 6); }
 
-// VTK_HEXAHEDRON corner v -> lattice offset (matches NKB_MC_VERT_OFF_DATA)
-__device__ __forceinline__ int voff_i(int v) { return (v ^ (v >> 1)) & 1; }
-__device__ __forceinline__ int voff_j(int v) { return (v >> 1) & 1; }
-__device__ __forceinline__ int voff_k(int v) { return v >> 2; }
-
-__device__ __forceinline__ unsigned long long enc_ordered(double d) {
-  unsigned long long b = (unsigned long long)__double_as_longlong(d);
-  return (b & 0x8000000000000000ULL) ? ~b : (b | 0x8000000000000000ULL);
-}
 
 __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -132,15 +127,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 }
 // barrier among the 4 MC warps only (id 1; id 0 is __syncthreads)
 __device__ __forceinline__ void mc_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kMcThreads) : "memory"); }
-
-__device__ __forceinline__ double mag3(double a, double b, double c) {
-  // reference ':mag' = sqrt(sum(v**2)) summed left to right (sinks.py:240-241)
-  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
-}
-
-__device__ __forceinline__ double plane_dist(const double* n, double x, double y, double z) {
-  return __fma_rn(n[2], z, __fma_rn(n[1], y, __dmul_rn(n[0], x)));
-}
 
 
 constexpr int kMaxTriPerElem = kNC * NKB_MC_MAX_TRI * NKB_MAX_SURFACES;   // 6860
@@ -233,12 +219,6 @@ struct McScratch {
   signed char t_tri[256][3 * NKB_MC_MAX_TRI];
   unsigned char t_edge[12][2];
 };
-
-// case byte of surface s from the 8 corner bit-bytes packed in w (byte v =
-// bits of corner v): gather bit s of every byte into one byte (bit v)
-__device__ __forceinline__ unsigned case_of(unsigned long long w, int s) {
-  return (unsigned)((((w >> s) & 0x0101010101010101ULL) * 0x0102040810204080ULL) >> 56);
-}
 
 }  // namespace
 
@@ -853,11 +833,21 @@ int launch_fused_prepare() {
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  NKB_TRY(launch_stream_prepare());
   int dev = 0;
   NKB_CUDA(cudaGetDevice(&dev));
   NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   done = true;
   return NKB_OK;
+}
+
+// which pass runs the surfaces of `p`: 1 = the barrier-free warp-per-element
+// pass (stream.cu) for pipelines without a velocity gradient, 0 = K1.
+// NKB_STREAM=0 forces K1 (A/B runs); the phase profile is K1's.
+int surface_pass_of(const FusedParams& p) {
+  const char* v = getenv("NKB_STREAM");
+  const bool on = v == nullptr || v[0] != '0';
+  return (on && p.prof == nullptr && stream_eligible(p)) ? 1 : 0;
 }
 
 int launch_fused(const FusedParams& p, cudaStream_t s) {
@@ -890,6 +880,7 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   NKB_TRY(launch_fused_prepare());
   const int grid = fused_grid(p.n_elements);
   const unsigned gx = (unsigned)grid;
+  if (surface_pass_of(p) == 1) return launch_stream(p, grid, s);
   if (p.prof) {
     if (cached) fused_kernel<true, true><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
     else fused_kernel<false, true><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);

@@ -158,6 +158,12 @@ int set_dmat_constant(const double* dmat);
 int fused_grid(int64_t n_elements);       // CTAs (= triangle regions) of launch_fused
 int launch_fused(const FusedParams& p, cudaStream_t s);
 int launch_fused_prepare();
+// K1s (stream.cu): pipelines without a velocity gradient (no exports, fields
+// 16-byte aligned); launch_fused dispatches to it when surface_pass_of == 1
+bool stream_eligible(const FusedParams& p);
+int surface_pass_of(const FusedParams& p);
+int launch_stream(const FusedParams& p, int grid, cudaStream_t s);
+int launch_stream_prepare();
 int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* geo, cudaStream_t s);
 int launch_compact(const float4* tri, const unsigned long long* meta, const unsigned long long* region_count,
                    int n_regions, int64_t region_cap, float4* out_tri, unsigned long long* out_meta,

@@ -358,3 +358,45 @@ def test_abi_error_paths(ctx):
         InsituAnalysis(pipe).execute(da)
     with pytest.raises(ValueError, match="12 values"):
         InsituAnalysis(Pipeline(view=(1.0,) * 13)).execute(da)
+
+
+NOGRAD_PIPES = {
+    "umag_iso_umag_colour": Pipeline(surfaces=(Surface("iso", "velocity:mag", 0.6),
+                                               Surface("slice", value=0.5, normal=(0, 0, 1))),
+                                     color_field="velocity:mag"),
+    "scalar_iso_two_slices": Pipeline(surfaces=(Surface("iso", "temperature", 0.4),
+                                                Surface("slice", value=0.9, normal=(0.3, 1.0, 0.2)),
+                                                Surface("slice", value=1.0, normal=(1, 0, 0))),
+                                      color_field="temperature", width=120, height=90),
+    "four_no_grad": Pipeline(surfaces=(Surface("iso", "temperature", 0.2), Surface("iso", "temperature", 0.7),
+                                       Surface("iso", "velocity:mag", 0.5),
+                                       Surface("slice", value=0.7, normal=(1, 1, 1))),
+                             color_field="temperature"),
+}
+
+
+@pytest.mark.parametrize("name", list(NOGRAD_PIPES))
+def test_stream_pass_matches_fused_pass_and_oracle(ctx, name, monkeypatch):
+    """Pipelines without a velocity gradient run the warp-per-element pass
+    (stream.cu, report.surface_pass == 1); NKB_STREAM=0 forces K1.  Both
+    give the oracle's triangles (ordered: same list and case words; fast:
+    same multiset) and identical images."""
+    case = synth.box(nel=(4, 3, 3))
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("NKB_STREAM", mode)
+        pipe = Pipeline(**{**NOGRAD_PIPES[name].__dict__, "emit_meta": True})
+        _, res = _run(ctx, case, pipe)
+        assert res.report.surface_pass == int(mode)
+        _check_against_oracle(ctx, case, pipe, res)
+        _, fast = _run(ctx, case, NOGRAD_PIPES[name])
+        assert fast.report.surface_pass == int(mode)
+        out[mode] = (_rows(ctx.triangles()), fast.rgba.copy(), fast.report.range)
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
+
+
+def test_gradient_pipelines_use_fused_pass(ctx):
+    case = synth.box(nel=(2, 2, 2))
+    _, res = _run(ctx, case, BOX_PIPES["q_iso"])
+    assert res.report.surface_pass == 0

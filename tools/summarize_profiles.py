@@ -1,7 +1,11 @@
 """Summarise gpurun_out/<tag>_* ncu outputs into profiles/ (committed).
 
     python tools/summarize_profiles.py r01
+    python tools/summarize_profiles.py s2_c4 --launches gpurun_out/s2/c4_launches.csv \
+        --rep gpurun_out/s2/c4_stream.ncu-rep --kernel stream_kernel --config c4 \
+        --label "C4 (1,048,576 elements, 537M GLL points)"
 """
+import argparse
 import csv
 import json
 import os
@@ -12,8 +16,8 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def launches(tag):
-    path = os.path.join(ROOT, "gpurun_out", f"{tag}_launches.csv")
+def launches(tag, path=None):
+    path = path or os.path.join(ROOT, "gpurun_out", f"{tag}_launches.csv")
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     h = rows[0]
     iN, iV, iM = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
@@ -36,8 +40,8 @@ def launches(tag):
     return "\n".join(lines) + "\n"
 
 
-def full(tag):
-    rep = os.path.join(ROOT, "gpurun_out", f"{tag}_fused.ncu-rep")
+def full(tag, rep=None):
+    rep = rep or os.path.join(ROOT, "gpurun_out", f"{tag}_fused.ncu-rep")
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h, units, vals = rows[0], rows[1], rows[2]
@@ -56,16 +60,19 @@ def full(tag):
     return out
 
 
-def main(tag):
+def main(tag, launches_csv=None, rep=None, kernel="fused_kernel", config="c2",
+         label="C2 (32768 elements, 16.8M GLL points)"):
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    txt = launches(tag)
+    txt = launches(tag, launches_csv)
     open(os.path.join(ROOT, "profiles", f"{tag}_launches.txt"), "w").write(txt)
     print(txt)
-    m = full(tag)
-    lines = [f"# ncu --set full, fused_kernel, C2 (32768 elements, 16.8M GLL points), tag {tag}"]
+    rep = rep or os.path.join(ROOT, "gpurun_out", f"{tag}_fused.ncu-rep")
+    m = full(tag, rep)
+    short = kernel.replace("_kernel", "")
+    lines = [f"# ncu --set full, {kernel}, {label}, tag {tag}"]
     for k, (v, u) in m.items():
         lines.append(f"{k:70s} {v} {u}")
-    open(os.path.join(ROOT, "profiles", f"{tag}_fused_full.txt"), "w").write("\n".join(lines) + "\n")
+    open(os.path.join(ROOT, "profiles", f"{tag}_{short}_full.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
     def num(k):
@@ -74,15 +81,14 @@ def main(tag):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         return f * scale
     # per-source-line stall samples of the same capture (where the warps wait)
-    rep = os.path.join(ROOT, "gpurun_out", f"{tag}_fused.ncu-rep")
     page = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                           capture_output=True, text=True).stdout
     tmp = os.path.join(ROOT, "gpurun_out", f"{tag}_source.csv")
     open(tmp, "w").write(page)
     top = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), tmp, "40"],
                          capture_output=True, text=True).stdout
-    open(os.path.join(ROOT, "profiles", f"{tag}_fused_lines.txt"), "w").write(
-        f"# fused_kernel stall samples / instructions by CUDA source line (ncu source page), tag {tag}\n" + top)
+    open(os.path.join(ROOT, "profiles", f"{tag}_{short}_lines.txt"), "w").write(
+        f"# {kernel} stall samples / instructions by CUDA source line (ncu source page), tag {tag}\n" + top)
     bj = os.path.join(ROOT, "gpurun_out", f"{tag}_bench.json")
     if os.path.exists(bj):
         js = [ln for ln in open(bj).read().splitlines() if ln.startswith("{")]
@@ -90,10 +96,18 @@ def main(tag):
             open(os.path.join(ROOT, "profiles", f"{tag}_bench.json"), "w").write(js[-1] + "\n")
     if "dram__bytes_read.sum" in m:
         traffic = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
-        json.dump({"dram_bytes_per_launch": traffic, "source": f"profiles/{tag}_fused_full.txt"},
-                  open(os.path.join(ROOT, "profiles", "traffic_c2.json"), "w"), indent=1)
+        json.dump({"dram_bytes_per_launch": traffic, "source": f"profiles/{tag}_{short}_full.txt"},
+                  open(os.path.join(ROOT, "profiles", f"traffic_{config}.json"), "w"), indent=1)
         print("traffic", traffic)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    ap = argparse.ArgumentParser()
+    ap.add_argument("tag", nargs="?", default="r01")
+    ap.add_argument("--launches", default=None)
+    ap.add_argument("--rep", default=None)
+    ap.add_argument("--kernel", default="fused_kernel")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--label", default="C2 (32768 elements, 16.8M GLL points)")
+    a = ap.parse_args()
+    main(a.tag, a.launches, a.rep, a.kernel, a.config, a.label)
