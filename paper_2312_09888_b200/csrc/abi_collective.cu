@@ -37,6 +37,8 @@ void stats_tables_free(StatsTables& T) {
   cudaFree(T.d_nodes);
   cudaFree(T.d_levels);
   cudaFree(T.d_out);
+  cudaFreeHost(T.h_out);
+  T.h_out = nullptr;
   T.d_chunks = nullptr;
   T.d_shapes = nullptr;
   T.d_leaves = nullptr;
@@ -340,6 +342,13 @@ int nkb_dssum(nkb_ctx* ctx, double* field, void* stream) {
 
 // ---- field statistics (stats sink) --------------------------------------------
 
+static double dec_ordered_stats(unsigned long long e) {
+  const unsigned long long b = (e & 0x8000000000000000ULL) ? (e & ~0x8000000000000000ULL) : ~e;
+  double d;
+  memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
 static void stats_bind(const StatsTables& T, StatsParams& P) {
   P.chunks = T.d_chunks;
   P.n_chunks = T.n_dev;
@@ -348,7 +357,7 @@ static void stats_bind(const StatsTables& T, StatsParams& P) {
   P.nodes = T.d_nodes;
   P.level_start = T.d_levels;
   P.out_sum = T.d_out;
-  P.out_mm = T.d_out + std::max(T.n_dev, 1);
+  P.out_mm = reinterpret_cast<unsigned long long*>(T.d_out + T.n_dev);
 }
 
 // upload chunk list + shape tables; returns the kernel parameters
@@ -378,7 +387,8 @@ static int stats_upload(StatsTables& T, const std::vector<StatChunk>& chunks, St
   NKB_CUDA(cudaMalloc(&T.d_leaves, sizeof(int2) * std::max<size_t>(lv.size(), 1)));
   NKB_CUDA(cudaMalloc(&T.d_nodes, sizeof(int2) * nd.size()));
   NKB_CUDA(cudaMalloc(&T.d_levels, sizeof(int) * ls.size()));
-  NKB_CUDA(cudaMalloc(&T.d_out, sizeof(double) * 4 * std::max(n, 1)));
+  NKB_CUDA(cudaMalloc(&T.d_out, sizeof(double) * (n + 3)));
+  NKB_CUDA(cudaMallocHost(&T.h_out, sizeof(double) * (n + 3)));
   if (n) NKB_CUDA(cudaMemcpy(T.d_chunks, chunks.data(), sizeof(StatChunk) * n, cudaMemcpyHostToDevice));
   if (!shp.empty()) NKB_CUDA(cudaMemcpy(T.d_shapes, shp.data(), sizeof(StatShape) * shp.size(), cudaMemcpyHostToDevice));
   if (!lv.empty()) NKB_CUDA(cudaMemcpy(T.d_leaves, lv.data(), sizeof(int2) * lv.size(), cudaMemcpyHostToDevice));
@@ -475,29 +485,27 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
   std::vector<double> sums(nc, 0.0);
   double mn = INFINITY, mx = -INFINITY;
   bool nan = false;
+  // one launch over `chunks`: hs = chunk sums, hm = {min, max, NaN flag} of all their values
   auto run = [&](StatsTables& TT, const std::vector<StatChunk>& chunks, bool upload, StatsParams& Q,
                  std::vector<double>& hs, std::vector<double>& hm) -> int {
     if (upload) NKB_TRY(stats_upload(TT, chunks, Q));
     else stats_bind(TT, Q);
-    NKB_TRY(launch_pairwise_chunks(Q, s));
     const int m = (int)chunks.size();
-    hs.resize(m);
-    hm.resize(3 * (size_t)m);
-    if (m) {
-      NKB_CUDA(cudaMemcpyAsync(hs.data(), Q.out_sum, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
-      NKB_CUDA(cudaMemcpyAsync(hm.data(), Q.out_mm, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
-    }
+    NKB_CUDA(cudaMemsetAsync(Q.out_mm, 0xff, sizeof(unsigned long long), s));       // enc(min) <- max
+    NKB_CUDA(cudaMemsetAsync(Q.out_mm + 1, 0, 2 * sizeof(unsigned long long), s));  // enc(max), NaN <- 0
+    NKB_TRY(launch_pairwise_chunks(Q, s));
+    NKB_CUDA(cudaMemcpyAsync(TT.h_out, TT.d_out, sizeof(double) * (m + 3), cudaMemcpyDeviceToHost, s));
     NKB_CUDA(cudaStreamSynchronize(s));
+    hs.assign(TT.h_out, TT.h_out + m);
+    unsigned long long w[3];
+    memcpy(w, TT.h_out + m, sizeof(w));
+    hm = {w[0] == ~0ULL ? INFINITY : dec_ordered_stats(w[0]), w[1] == 0ULL ? -INFINITY : dec_ordered_stats(w[1]),
+          w[2] ? 1.0 : 0.0};
     return NKB_OK;
   };
   std::vector<double> hs, hm;
   NKB_TRY(run(T, T.mine, fresh, P, hs, hm));
-  double lmn = INFINITY, lmx = -INFINITY, lnan = 0.0;
-  for (size_t k = 0; k < T.mine.size(); ++k) {
-    lmn = fmin(lmn, hm[3 * k]);
-    lmx = fmax(lmx, hm[3 * k + 1]);
-    if (hm[3 * k + 2] != 0.0) lnan = 1.0;
-  }
+  const double lmn = hm[0], lmx = hm[1], lnan = hm[2];
   if (!coll) {
     for (size_t k = 0; k < T.mine.size(); ++k) sums[T.mine_idx[k]] = hs[k];
     mn = lmn;
@@ -570,15 +578,14 @@ int nkb_stats(nkb_ctx* ctx, const nkb_segment* segs, int nseg, int collective, d
       cudaFree(dv);
       stats_tables_free(TB);
       NKB_TRY(rc);
-      for (size_t k = 0; k < boundary.size(); ++k) {
-        sums[boundary[k]] = bs[k];
-        mn = fmin(mn, bm[3 * k]);
-        mx = fmax(mx, bm[3 * k + 1]);
-        if (bm[3 * k + 2] != 0.0) nan = true;
-      }
+      for (size_t k = 0; k < boundary.size(); ++k) sums[boundary[k]] = bs[k];
+      mn = fmin(mn, bm[0]);
+      mx = fmax(mx, bm[1]);
+      if (bm[2] != 0.0) nan = true;
     }
   }
-  const double total = 0.0 + pairwise_combine(N, lo, sums);      // np.add.reduce: identity + pairwise
+  if (T.comb.empty()) pairwise_combine_program(N, lo, T.comb);
+  const double total = 0.0 + pairwise_combine(T.comb, sums);     // np.add.reduce: identity + pairwise
   out[0] = nan ? NAN : mn;
   out[1] = nan ? NAN : mx;
   out[2] = total / (double)N;                                    // np.mean: sum / count

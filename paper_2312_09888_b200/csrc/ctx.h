@@ -64,7 +64,9 @@ struct StatsTables {
   int2* d_leaves = nullptr;
   int2* d_nodes = nullptr;
   int* d_levels = nullptr;
-  double* d_out = nullptr;                     // sums [n] + mm [3n]
+  double* d_out = nullptr;                     // sums [n] + 3 reduced words (min, max, NaN)
+  double* h_out = nullptr;                     // pinned copy of d_out
+  std::vector<int> comb;                       // postfix program of the tree above the chunks
   int n_dev = 0;
 };
 

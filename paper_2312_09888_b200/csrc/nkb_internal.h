@@ -203,7 +203,7 @@ struct StatsParams {
   const int2* nodes;                     // children as slots of the value array
   const int* level_start;
   double* out_sum;                       // [n_chunks]
-  double* out_mm;                        // [n_chunks][3]: min, max, nan flag
+  unsigned long long* out_mm;            // [3]: enc(min) (atomicMin), enc(max) (atomicMax), NaN flag
 };
 struct PlanChunk {
   long long off, n;
@@ -215,7 +215,8 @@ struct StatShapeHost {
   int n_levels = 0;
 };
 void pairwise_plan(long long n, const std::vector<long long>& rank_lo, std::vector<PlanChunk>& out);
-double pairwise_combine(long long n, const std::vector<long long>& rank_lo, const std::vector<double>& chunk_sums);
+void pairwise_combine_program(long long n, const std::vector<long long>& rank_lo, std::vector<int>& prog);
+double pairwise_combine(const std::vector<int>& prog, const std::vector<double>& chunk_sums);
 void pairwise_shape(long long n, StatShapeHost& sh);
 int launch_pairwise_chunks(const StatsParams& p, cudaStream_t s);
 int launch_stat_windows(const StatsParams& p, double* out, cudaStream_t s);
