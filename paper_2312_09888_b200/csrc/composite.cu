@@ -109,11 +109,7 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
   const double lo = s_lo, hi = s_hi, span = __dsub_rn(hi, lo);
   const long long r0 = (long long)p.height * p.rank / p.nranks, r1 = (long long)p.height * (p.rank + 1) / p.nranks;
   const long long i0 = r0 * p.width, i1 = r1 * p.width;
-  for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < i1;
-       i += (long long)gridDim.x * blockDim.x) {
-    unsigned long long key = ~0ULL;
-#pragma unroll 4
-    for (int q = 0; q < p.nranks; ++q) key = min(key, p.peer_keys[q][i]);
+  auto resolve = [&](unsigned long long key, long long i) {
     uchar4 o;
     float dep;
     if (key == ~0ULL) {
@@ -128,6 +124,34 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
     }
     reinterpret_cast<uchar4*>(p.root_rgba)[i] = o;
     p.root_depth[i] = dep;
+  };
+  // pairs of pixels: one 16-byte load per peer, all peers' loads in flight
+  // before the min (remote NVLink loads are latency-bound, not bandwidth-bound)
+  const long long j0 = (i0 + 1) >> 1, j1 = i1 >> 1;   // whole pairs [2*j0, 2*j1)
+  const long long stride = (long long)gridDim.x * blockDim.x, t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long j = j0 + t; j < j1; j += stride) {
+    ulonglong2 v[kMaxRanks];
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q)
+      if (q < p.nranks) v[q] = reinterpret_cast<const ulonglong2*>(p.peer_keys[q])[j];
+    unsigned long long a = ~0ULL, b = ~0ULL;
+#pragma unroll
+    for (int q = 0; q < kMaxRanks; ++q)
+      if (q < p.nranks) {
+        a = min(a, v[q].x);
+        b = min(b, v[q].y);
+      }
+    resolve(a, 2 * j);
+    resolve(b, 2 * j + 1);
+  }
+  // an odd pixel at either end of the band
+  if (t < 2) {
+    const long long i = t == 0 ? i0 : i1 - 1;
+    if ((t == 0 && (i0 & 1) && i0 < i1) || (t == 1 && (i1 & 1) && i1 - 1 >= i0)) {
+      unsigned long long key = ~0ULL;
+      for (int q = 0; q < p.nranks; ++q) key = min(key, p.peer_keys[q][i]);
+      resolve(key, i);
+    }
   }
 }
 
@@ -153,8 +177,8 @@ int launch_p2p_wait(const P2PParams& p, int which, unsigned long long back, cuda
 
 int launch_p2p_composite(const P2PParams& p, cudaStream_t s) {
   const long long band = (long long)p.width * ((long long)p.height / p.nranks + 1);
-  long long blocks = (band + 255) / 256;
-  if (blocks > 148 * 4) blocks = 148 * 4;
+  long long blocks = (band / 2 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
   p2p_composite_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
   NKB_CUDA(cudaGetLastError());

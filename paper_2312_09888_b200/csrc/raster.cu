@@ -25,47 +25,16 @@ __global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
     z[i] = ~0ULL;
 }
 
-// One thread per triangle; blockIdx.y = triangle region (the count lives on
-// the device).  A thread walks the pixels of a small triangle itself; a
-// triangle whose box exceeds kBigBox pixels is set up once and walked by its
-// whole warp (lanes over pixels), so a few large triangles (coarse meshes,
-// close cameras) no longer serialise one thread.  Per-pixel arithmetic and
-// the atomicMin are the same either way, so the keys are identical.
-constexpr int kBigBox = 16;
-
+// one thread per triangle; blockIdx.y = triangle region (the count lives on the device)
 __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
-  __shared__ rdev::TriSetup s_big[256 / 32];
   const int r = blockIdx.y;
   long long ntri = (long long)p.region_count[r];
   if (ntri > p.region_cap) ntri = p.region_cap;
   const float4* tri = p.tri + 3 * (long long)r * p.region_cap;
   const int W = p.width, H = p.height;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long t0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); t0 < ntri; t0 += stride) {
-    const long long t = t0 + lane;                 // warp-uniform loop: every lane reaches the ballot
-    rdev::TriSetup T;
-    const bool ok = t < ntri && rdev::tri_setup(p.view, W, H, tri + 3 * t, T);
-    const long long box = ok ? (long long)(T.px1 - T.px0 + 1) * (T.py1 - T.py0 + 1) : 0;
-    const bool big = ok && T.px1 >= T.px0 && T.py1 >= T.py0 && box > kBigBox;
-    if (ok && !big)
-      for (int py = T.py0; py <= T.py1; ++py)
-        for (int px = T.px0; px <= T.px1; ++px) rdev::tri_pixel(T, px, py, W, p.zbuf);
-    unsigned m = __ballot_sync(0xffffffffu, big);
-    while (m) {
-      const int leader = __ffs(m) - 1;
-      m &= m - 1;
-      if (lane == leader) s_big[warp] = T;
-      __syncwarp();
-      const rdev::TriSetup& B = s_big[warp];
-      const int bw = B.px1 - B.px0 + 1;
-      const long long np = (long long)bw * (B.py1 - B.py0 + 1);
-      for (long long i = lane; i < np; i += 32) {
-        const int py = B.py0 + (int)(i / bw);
-        rdev::tri_pixel(B, B.px0 + (int)(i - (long long)(py - B.py0) * bw), py, W, p.zbuf);
-      }
-      __syncwarp();
-    }
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntri;
+       t += (long long)gridDim.x * blockDim.x) {
+    rdev::raster_triangle(p.view, W, H, tri + 3 * t, p.zbuf);
   }
 }
 

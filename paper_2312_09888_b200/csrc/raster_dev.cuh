@@ -1,8 +1,8 @@
 // Device helpers of the image kernels (raster.cu, composite.cu):
-//  * tri_setup / tri_pixel: one triangle into the packed depth|scalar key
-//    buffer (K2) -- 16.8 fixed-point edge functions with a top-left rule,
-//    sampling at pixel centres, depth clipped to [0, 1], order-independent
-//    atomicMin;
+//  * raster_triangle: one triangle into the packed depth|scalar key buffer
+//    (the raster step of K2, one thread per triangle) -- 16.8 fixed-point
+//    edge functions with a top-left rule, sampling at pixel centres, depth
+//    clipped to [0, 1], order-independent atomicMin;
 //  * dec_ordered / cmap_channel: the colour-range decoding and the colormap.
 // oracle/sem_oracle.c restates them operation for operation.
 #pragma once
@@ -60,19 +60,10 @@ __device__ __forceinline__ long long floordiv(long long a, long long b) {  // b 
 }
 
 
-// A triangle after setup: 16.8 fixed-point vertices (counter-clockwise),
-// depth and colour scalar per vertex, the top-left biases, 1/area and the
-// pixel bounding box clipped to the image.
-struct TriSetup {
+__device__ __forceinline__ void raster_triangle(const double* view, int W, int H, const float4* tri,
+                                                unsigned long long* zbuf) {
   long long X[3], Y[3];
   double Z[3], C[3];
-  long long bias[3];
-  double inv;
-  int px0, px1, py0, py1;
-};
-
-// false: culled (behind the camera, outside the guard band, NaN, zero area)
-__device__ __forceinline__ bool tri_setup(const double* view, int W, int H, const float4* tri, TriSetup& T) {
   bool ok = true;
   const bool persp = view[12] != 0.0 || view[13] != 0.0 || view[14] != 0.0 || view[15] != 0.0;
 #pragma unroll
@@ -90,64 +81,61 @@ __device__ __forceinline__ bool tri_setup(const double* view, int W, int H, cons
       sz = __ddiv_rn(sz, w);
     }
     if (!(fabs(sx) <= kGuard && fabs(sy) <= kGuard && sz == sz && v.w == v.w)) ok = false;
-    T.X[q] = __double2ll_rn(__dmul_rn(sx, 256.0));
-    T.Y[q] = __double2ll_rn(__dmul_rn(sy, 256.0));
-    T.Z[q] = sz;
-    T.C[q] = (double)v.w;
+    X[q] = __double2ll_rn(__dmul_rn(sx, 256.0));
+    Y[q] = __double2ll_rn(__dmul_rn(sy, 256.0));
+    Z[q] = sz;
+    C[q] = (double)v.w;
   }
-  if (!ok) return false;
-  long long area = (T.X[1] - T.X[0]) * (T.Y[2] - T.Y[0]) - (T.Y[1] - T.Y[0]) * (T.X[2] - T.X[0]);
-  if (area == 0) return false;
+  if (!ok) return;
+  long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
+  if (area == 0) return;
   if (area < 0) {
-    long long tx = T.X[1]; T.X[1] = T.X[2]; T.X[2] = tx;
-    long long ty = T.Y[1]; T.Y[1] = T.Y[2]; T.Y[2] = ty;
-    double tz = T.Z[1]; T.Z[1] = T.Z[2]; T.Z[2] = tz;
-    double tc = T.C[1]; T.C[1] = T.C[2]; T.C[2] = tc;
+    long long tx = X[1]; X[1] = X[2]; X[2] = tx;
+    long long ty = Y[1]; Y[1] = Y[2]; Y[2] = ty;
+    double tz = Z[1]; Z[1] = Z[2]; Z[2] = tz;
+    double tc = C[1]; C[1] = C[2]; C[2] = tc;
     area = -area;
   }
-  const long long xmin = min(T.X[0], min(T.X[1], T.X[2])), xmax = max(T.X[0], max(T.X[1], T.X[2]));
-  const long long ymin = min(T.Y[0], min(T.Y[1], T.Y[2])), ymax = max(T.Y[0], max(T.Y[1], T.Y[2]));
+  const long long xmin = min(X[0], min(X[1], X[2])), xmax = max(X[0], max(X[1], X[2]));
+  const long long ymin = min(Y[0], min(Y[1], Y[2])), ymax = max(Y[0], max(Y[1], Y[2]));
   long long px0 = -floordiv(-(xmin - 128), 256), px1 = floordiv(xmax - 128, 256);
   long long py0 = -floordiv(-(ymin - 128), 256), py1 = floordiv(ymax - 128, 256);
   if (px0 < 0) px0 = 0;
   if (py0 < 0) py0 = 0;
   if (px1 > W - 1) px1 = W - 1;
   if (py1 > H - 1) py1 = H - 1;
-  T.px0 = (int)px0;
-  T.px1 = (int)px1;
-  T.py0 = (int)py0;
-  T.py1 = (int)py1;
   // edge (a->b) opposite vertex i: w_i(P) = (Xb-Xa)(Py-Ya) - (Yb-Ya)(Px-Xa)
+  const int ea[3] = {1, 2, 0}, eb[3] = {2, 0, 1};
+  long long bias[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const int ea = (i + 1) % 3, eb = (i + 2) % 3;
-    const long long dy = T.Y[eb] - T.Y[ea], dx = T.X[eb] - T.X[ea];
-    T.bias[i] = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : -1;   // inclusive (top-left) edges
+    const long long dy = Y[eb[i]] - Y[ea[i]], dx = X[eb[i]] - X[ea[i]];
+    bias[i] = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : -1;   // inclusive (top-left) edges
   }
-  T.inv = __drcp_rn((double)area);                // == 1.0 / area: one IEEE division per triangle
-  return true;
-}
-
-// pixel (px, py) of a set-up triangle: sample at the pixel centre, depth and
-// colour from the barycentric weights, order-independent atomicMin of the key
-__device__ __forceinline__ void tri_pixel(const TriSetup& T, int px, int py, int W, unsigned long long* zbuf) {
-  const long long cy = (long long)py * 256 + 128, cx = (long long)px * 256 + 128;
-  long long w[3];
+  const double inv = __drcp_rn((double)area);     // == 1.0 / area: one IEEE division per triangle
+  for (long long py = py0; py <= py1; ++py) {
+    const long long cy = py * 256 + 128;
+    for (long long px = px0; px <= px1; ++px) {
+      const long long cx = px * 256 + 128;
+      long long w[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const int ea = (i + 1) % 3, eb = (i + 2) % 3;
-    w[i] = (T.X[eb] - T.X[ea]) * (cy - T.Y[ea]) - (T.Y[eb] - T.Y[ea]) * (cx - T.X[ea]);
+      for (int i = 0; i < 3; ++i)
+        w[i] = (X[eb[i]] - X[ea[i]]) * (cy - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx - X[ea[i]]);
+      if (w[0] + bias[0] < 0 || w[1] + bias[1] < 0 || w[2] + bias[2] < 0) continue;
+      double d = __dmul_rn(__fma_rn((double)w[2], Z[2],
+                                    __fma_rn((double)w[1], Z[1], __dmul_rn((double)w[0], Z[0]))),
+                           inv);
+      if (!(d >= 0.0 && d <= 1.0)) continue;
+      d = __dadd_rn(d, 0.0);
+      const double c = __dmul_rn(__fma_rn((double)w[2], C[2],
+                                          __fma_rn((double)w[1], C[1], __dmul_rn((double)w[0], C[0]))),
+                                 inv);
+      const unsigned long long key =
+          ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
+          (unsigned long long)__float_as_uint(__double2float_rn(c));
+      atomicMin(zbuf + py * W + px, key);
+    }
   }
-  if (w[0] + T.bias[0] < 0 || w[1] + T.bias[1] < 0 || w[2] + T.bias[2] < 0) return;
-  double d = __dmul_rn(__fma_rn((double)w[2], T.Z[2], __fma_rn((double)w[1], T.Z[1], __dmul_rn((double)w[0], T.Z[0]))),
-                       T.inv);
-  if (!(d >= 0.0 && d <= 1.0)) return;
-  d = __dadd_rn(d, 0.0);
-  const double c = __dmul_rn(__fma_rn((double)w[2], T.C[2], __fma_rn((double)w[1], T.C[1], __dmul_rn((double)w[0], T.C[0]))),
-                             T.inv);
-  const unsigned long long key = ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
-                                 (unsigned long long)__float_as_uint(__double2float_rn(c));
-  atomicMin(zbuf + (long long)py * W + px, key);
 }
 
 }  // namespace rdev

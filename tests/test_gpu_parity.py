@@ -400,3 +400,16 @@ def test_gradient_pipelines_use_fused_pass(ctx):
     case = synth.box(nel=(2, 2, 2))
     _, res = _run(ctx, case, BOX_PIPES["q_iso"])
     assert res.report.surface_pass == 0
+
+
+def test_large_triangles_raster_bit_exact(ctx):
+    """A coarse mesh drawn big: triangles span hundreds of pixels (long
+    per-thread pixel walks in K2, many atomicMin collisions between
+    overlapping triangles); image and depth equal the oracle's."""
+    case = synth.box(nel=(2, 2, 2))
+    pipe = Pipeline(surfaces=(Surface("iso", "temperature", 0.45), Surface("slice", value=0.8, normal=(1, 0.2, 0))),
+                    color_field="temperature", width=640, height=480, emit_meta=True)
+    _, res = _run(ctx, case, pipe)
+    tri = ctx.triangles()
+    assert len(tri) > 0
+    _check_against_oracle(ctx, case, pipe, res)
