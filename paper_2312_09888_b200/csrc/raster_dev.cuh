@@ -133,10 +133,7 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
       const unsigned long long key =
           ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
           (unsigned long long)__float_as_uint(__double2float_rn(c));
-      // early depth test: the stored key only decreases, so skipping a key that
-      // is not below the current value gives the same result with fewer atomics
-      unsigned long long* zp = zbuf + py * W + px;
-      if (key < *(volatile unsigned long long*)zp) atomicMin(zp, key);
+      atomicMin(zbuf + py * W + px, key);
     }
   }
 }
