@@ -356,7 +356,11 @@ def run_ours(a):
                               (round(statistics.mean(x), 4) for x in zip(*stages)))),
         "fused_ms_per_rank": per_rank_fused,
         "triangles_per_rank": per_rank_tri,
-        "gpu_launches": 5 * a.steps,
+        # libnekb200 kernels per step on rank 0: K1|K1s, zbuf clear, K2, range words, K3
+        # (1 GPU or the NCCL composite, whose reduce kernels are NCCL's); the P2P
+        # composite adds epoch, two waits, two signals and the composite kernel
+        # and drops K3 (resolved inside the composite)
+        "gpu_launches": (5 if world == 1 or os.environ.get("NKB_COMPOSITE") == "nccl" else 10) * a.steps,
         "clocks": clk,
     }
     if world == 1:
