@@ -699,7 +699,7 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   fp.tri = ctx->tri;
   fp.meta = p->emit_meta ? ctx->meta : nullptr;
   fp.tri_cap = ctx->tri_cap;
-  ctx->n_regions = fused_grid(ctx->E);
+  ctx->n_regions = fused_grid_for(fp, ctx->E);
   ctx->region_cap = ctx->tri_cap / ctx->n_regions;
   fp.region_cap = ctx->region_cap;
   fp.region_count = ctx->region_count;

@@ -820,6 +820,364 @@ int launch_geometry(const double* x, const double* y, const double* z, int64_t E
   return NKB_OK;
 }
 
+
+// ---- K1g: the cached-geometry gradient pass, two independent CTAs per SM ----
+// K1 runs one 512-thread CTA per SM whose phases (pencils | node | classify |
+// emit) are serialised by CTA-wide barriers; its phase profile shows the SM
+// waiting at them.  K1g runs TWO 256-thread CTAs per SM, each owning one
+// element at a time start to finish, so one CTA's barrier waits and load
+// latency are covered by the other CTA's work:
+//   - inputs double-buffered (cp.async, 8 B per node, the swizzled layout of K1);
+//   - the cached J^-1 is read per node straight from global memory (coalesced),
+//     pulled toward L2 one element ahead by a bulk prefetch, instead of staged;
+//   - u,v,w pencils on 192 threads (pencil3 of K1), then 2 nodes per thread,
+//     then classification (2 sub-hexes per thread), one block scan of packed
+//     (triangle, active-cell) counts, and emission with one task per triangle
+//     vertex over all 256 threads -- all inside the element's iteration.
+// Every value is computed by K1's device functions in K1's order, so the
+// results are bit-identical to K1 and to the oracle.
+constexpr int kG2Threads = 256;
+constexpr int kG2PerSM = 2;
+constexpr int kG2MaxIn = 7;                 // 2 CTAs/SM of (2*nin + 11) * 4 KB shared memory
+
+struct G2Scratch {
+  unsigned char t_ntri[256];
+  signed char t_tri[256][3 * NKB_MC_MAX_TRI];
+  unsigned char t_edge[12][2];
+  unsigned act_cases[kNC];
+  unsigned short act_cell[kNC];
+  unsigned short act_off[kNC];
+  int wsum[kG2Threads / 32];
+  unsigned long long base;
+  unsigned band, bor;
+};
+
+__device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const FusedParams p, int nin, int slot_sc,
+                                                                     int slot_vel, int slot_xyz) {
+  extern __shared__ __align__(16) double smem[];
+  double* S_ring = smem;                               // 2 * nin * 512
+  double* S_dv = S_ring + 2 * nin * kArr;              // 9 * 512 u,v,w derivatives
+  double* S_q = S_dv + 9 * kArr;                       // Q, |w| (swizzled)
+  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 2 * kArr);   // 512 case bits, node order
+  __shared__ G2Scratch mc;
+  __shared__ double s_mn[kG2Threads / 32], s_mx[kG2Threads / 32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long E = p.n_elements;
+  const long long G = gridDim.x;
+  const long long n_it = (E > blockIdx.x) ? (E - blockIdx.x + G - 1) / G : 0;
+  double cmin = INFINITY, cmax = -INFINITY;
+  unsigned long long cta_fill = 0;
+  constexpr unsigned kGeoBytes = 9u * kNN * sizeof(double);
+
+  for (int i = tid; i < 256; i += kG2Threads) mc.t_ntri[i] = g_mc_ntri[i];
+  for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kG2Threads) (&mc.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
+  if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
+
+  const int q0 = sw_node(tid), q1 = sw_node(tid + kG2Threads);
+  auto prefetch = [&](long long e, int b) {
+    double* dst = S_ring + b * nin * kArr;
+    const long long g0 = e * (long long)kNN + tid;
+#pragma unroll
+    for (int f = 0; f < kG2MaxIn; ++f) {
+      if (f < nin) {
+        const double* src = p.in_ptr[f] + g0;
+        double* d = dst + f * kArr;
+        cp_async8(d + q0, src);
+        cp_async8(d + q1, src + kG2Threads);
+      }
+    }
+  };
+  if (n_it > 0) {
+    prefetch(blockIdx.x, 0);
+    if (tid == 0) l2_prefetch(p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes);
+  }
+  cp_async_commit();
+
+  int off[kNP];                                        // pencil offsets (threads < 192)
+  pencil_offsets(tid >> 6 < 3 ? tid >> 6 : 0, tid & 7, (tid >> 3) & 7, off);
+
+  for (long long it = 0; it < n_it; ++it) {
+    const long long e = blockIdx.x + it * G;
+    const int b = (int)(it & 1);
+    cp_async_wait_all();
+    if (tid == 0) {
+      mc.band = ~0u;
+      mc.bor = 0u;
+    }
+    __syncthreads();                                   // element `it` staged; iteration it-1 finished
+    if (it + 1 < n_it) {
+      prefetch(e + G, b ^ 1);
+      if (tid == 0) l2_prefetch(p.geo + (e + G) * 9 * kNN, kGeoBytes);
+    }
+    cp_async_commit();
+    const double* S_in = S_ring + b * nin * kArr;
+
+    // ---- u,v,w pencils: thread = (dir, pencil), 3 fields share offsets ----
+    if (tid < 192) {
+      const double* su = S_in + slot_vel * kArr;
+      double* d0 = S_dv + (tid >> 6) * kArr;
+      pencil3(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
+    }
+    __syncthreads();
+
+    // ---- node phase: nodes tid and tid + 256 ----
+    const long long g0 = e * (long long)kNN;
+    unsigned wand = ~0u, wor = 0u;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int n = tid + kG2Threads * h;
+      const int q = h ? q1 : q0;
+      double J[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) J[c] = __ldg(p.geo + (e * 9 + c) * kNN + n);
+      double U[9];
+#pragma unroll
+      for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
+      double A[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb)
+          A[3 * a + bb] = __fma_rn(U[3 * a + 2], J[6 + bb],
+                                   __fma_rn(U[3 * a + 1], J[3 + bb], __dmul_rn(U[3 * a + 0], J[0 + bb])));
+      const double offd = __fma_rn(A[5], A[7], __fma_rn(A[2], A[6], __dmul_rn(A[1], A[3])));
+      const double dia = __fma_rn(A[8], A[8], __fma_rn(A[4], A[4], __dmul_rn(A[0], A[0])));
+      const double vq = -__fma_rn(0.5, dia, offd);
+      const double om0 = __dsub_rn(A[7], A[5]);
+      const double om1 = __dsub_rn(A[2], A[6]);
+      const double om2 = __dsub_rn(A[3], A[1]);
+      double vw = 0.0, vu = 0.0;
+      S_q[q] = vq;
+      if (p.need_wmag) {
+        vw = mag3(om0, om1, om2);
+        S_q[kArr + q] = vw;
+      }
+      if (p.q_out) p.q_out[g0 + n] = vq;
+      if (p.wmag_out) p.wmag_out[g0 + n] = vw;
+      if (p.vort_out) {
+        p.vort_out[3 * (g0 + n) + 0] = om0;
+        p.vort_out[3 * (g0 + n) + 1] = om1;
+        p.vort_out[3 * (g0 + n) + 2] = om2;
+      }
+      if (p.need_umag)
+        vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
+      unsigned bits = 0;
+#pragma unroll
+      for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
+        if (s >= p.n_surf) break;
+        const int src = p.surf_src[s];
+        double val;
+        if (src >= SRC_PLANE)
+          val = plane_dist(p.surf_n[s], S_in[slot_xyz * kArr + q], S_in[(slot_xyz + 1) * kArr + q],
+                           S_in[(slot_xyz + 2) * kArr + q]);
+        else if (src == SRC_Q) val = vq;
+        else if (src == SRC_WMAG) val = vw;
+        else if (src == SRC_UMAG) val = vu;
+        else val = S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+        bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+      }
+      S_bits[n] = (unsigned char)bits;
+      wand &= bits;
+      wor |= bits;
+      if (p.color_src >= 0) {
+        const int src = p.color_src;
+        const double c = (src == SRC_Q)      ? vq
+                         : (src == SRC_WMAG) ? vw
+                         : (src == SRC_UMAG) ? vu
+                                             : S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+        cmin = fmin(cmin, c);
+        cmax = fmax(cmax, c);
+      }
+    }
+    {
+      const unsigned wa = __reduce_and_sync(0xffffffffu, wand), wo = __reduce_or_sync(0xffffffffu, wor);
+      if (lane == 0) {
+        atomicAnd(&mc.band, wa);
+        atomicOr(&mc.bor, wo);
+      }
+    }
+    __syncthreads();                                   // case bits, Q, |w| of element `it` ready
+    if (p.n_surf == 0) continue;
+    if ((mc.bor & ~mc.band) == 0) {                    // no surface crosses this element
+      if (p.mode == FUSED_COUNT && tid == 0) p.elem_count[e] = 0;
+      continue;
+    }
+
+    // ---- classify: sub-hexes 2t, 2t+1; one block scan of (triangles, active cells) ----
+    unsigned pk[2] = {0u, 0u};
+    int nt[2] = {0, 0};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = 2 * tid + u;
+      if (c < kNC) {
+        const unsigned long long w =
+            corner_bytes(reinterpret_cast<const unsigned long long*>(S_bits), c % kN, (c / kN) % kN, c / (kN * kN));
+#pragma unroll
+        for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
+          if (s >= p.n_surf) break;
+          const unsigned cs = case_of(w, s);
+          pk[u] |= cs << (8 * s);
+          nt[u] += mc.t_ntri[cs];
+        }
+      }
+    }
+    const int mine = ((nt[0] + nt[1]) << 10) | ((nt[0] > 0) + (nt[1] > 0));
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) mc.wsum[warp] = incl;
+    __syncthreads();
+    int before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kG2Threads / 32; ++w) {
+      const int v = mc.wsum[w];
+      before += (w < warp) ? v : 0;
+      all += v;
+    }
+    const int excl = before + incl - mine;
+    int tri_off = excl >> 10, act = excl & 1023;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (nt[u] > 0) {
+        mc.act_cell[act] = (unsigned short)(2 * tid + u);
+        mc.act_cases[act] = pk[u];
+        mc.act_off[act] = (unsigned short)tri_off;
+        ++act;
+        tri_off += nt[u];
+      }
+    const int total = all >> 10, n_act = all & 1023;
+    if (tid == 0) {
+      unsigned long long base = 0;
+      if (p.mode == FUSED_FAST) {
+        base = (unsigned long long)blockIdx.x * (unsigned long long)p.region_cap + cta_fill;
+      } else if (p.mode == FUSED_COUNT) {
+        p.elem_count[e] = total;
+      } else {
+        base = (unsigned long long)p.elem_offset[e];
+      }
+      mc.base = base;
+    }
+    cta_fill += (unsigned long long)total;             // every thread keeps the same count
+    __syncthreads();
+    if (p.mode == FUSED_COUNT || total == 0) continue;
+
+    // ---- emit: one thread per active cell, (surface, table) order ----
+    const bool xyz_staged = slot_xyz >= 0;
+    const double* Sx = xyz_staged ? S_in + slot_xyz * kArr : p.x + g0;
+    const double* Sy = xyz_staged ? S_in + (slot_xyz + 1) * kArr : p.y + g0;
+    const double* Sz = xyz_staged ? S_in + (slot_xyz + 2) * kArr : p.z + g0;
+    const double* Su = S_in + slot_vel * kArr;
+    auto value_at = [&](int src, int s, int q) -> double {
+      if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
+      if (src == SRC_Q) return S_q[q];
+      if (src == SRC_WMAG) return S_q[kArr + q];
+      if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
+      return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+    };
+    // one task per triangle VERTEX over all 256 threads: triangle tt's cell
+    // by binary search of the active cells' offsets, then its (surface,
+    // table row) by walking the cell's case bytes
+    const unsigned long long base = mc.base;
+    for (int task = tid; task < 3 * total; task += kG2Threads) {
+      const int tt = task / 3, r = task - 3 * (task / 3);
+      int lo = 0, hi = n_act - 1;                      // last active cell with act_off <= tt
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((int)mc.act_off[mid] <= tt) lo = mid;
+        else hi = mid - 1;
+      }
+      const int c = mc.act_cell[lo];
+      const unsigned packed = mc.act_cases[lo];
+      int li = tt - (int)mc.act_off[lo], s = 0;
+      unsigned cs = packed & 0xffu;
+      for (;;) {
+        const int nt = mc.t_ntri[cs];
+        if (li < nt) break;
+        li -= nt;
+        ++s;
+        cs = (packed >> (8 * s)) & 0xffu;
+      }
+      const int k = li;
+      const long long out = (long long)base + tt;
+      const bool over = p.mode == FUSED_FAST ? (out - (long long)blockIdx.x * p.region_cap >= p.region_cap)
+                                             : (out >= p.tri_cap);
+      if (over) continue;                              // counted, not written; the host grows and re-runs
+      const int ca = c % kN, cb = (c / kN) % kN, ck = c / (kN * kN);
+      const int src = p.surf_src[s];
+      const double iso = p.surf_iso[s];
+      const int ed = mc.t_tri[cs][3 * k + r];
+      const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
+      const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
+      const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
+      const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
+      const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
+      const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
+      const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
+      const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
+      const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
+      const double xa = Sx[pa], ya = Sy[pa], za = Sz[pa];
+      const double xb = Sx[pb], yb = Sy[pb], zb = Sz[pb];
+      float4 v;
+      v.x = __double2float_rn(__fma_rn(tv, __dsub_rn(xb, xa), xa));
+      v.y = __double2float_rn(__fma_rn(tv, __dsub_rn(yb, ya), ya));
+      v.z = __double2float_rn(__fma_rn(tv, __dsub_rn(zb, za), za));
+      v.w = __double2float_rn(__fma_rn(tv, __dsub_rn(clb, cla), cla));
+      p.tri[3 * out + r] = v;
+      if (p.meta && r == 0)
+        p.meta[out] = ((unsigned long long)e << 32) | ((unsigned long long)c << 16) |
+                      ((unsigned long long)s << 12) | ((unsigned long long)k << 8) | cs;
+    }
+  }
+
+  if (p.mode == FUSED_FAST && p.region_count != nullptr && tid == 0) {
+    p.region_count[blockIdx.x] = cta_fill;
+    if (cta_fill) atomicAdd(&p.counters[0], cta_fill);
+  }
+  if (p.color_src >= 0 && p.mode != FUSED_ORDERED) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+      cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    }
+    if (lane == 0) {
+      s_mn[warp] = cmin;
+      s_mx[warp] = cmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double mn = s_mn[0], mx = s_mx[0];
+      for (int w = 1; w < kG2Threads / 32; ++w) {
+        mn = fmin(mn, s_mn[w]);
+        mx = fmax(mx, s_mx[w]);
+      }
+      if (mn <= mx) {
+        atomicMin(&p.counters[1], enc_ordered(mn));
+        atomicMax(&p.counters[2], enc_ordered(mx));
+      }
+    }
+  }
+}
+
+static size_t fused2_smem_bytes(int nin) { return (size_t)(2 * nin + 11) * kArr * sizeof(double) + kNN; }
+
+static bool fused2_on(const FusedParams& p) {
+  const char* v = getenv("NKB_FUSED2");               // A/B: NKB_FUSED2=0 forces K1
+  if (v && v[0] == '0') return false;
+  if (!(p.geo != nullptr && p.need_grad) || p.prof != nullptr) return false;
+  bool has_plane = false;
+  for (int i = 0; i < p.n_surf; ++i) has_plane |= p.surf_src[i] >= SRC_PLANE;
+  const int nin = (has_plane ? 3 : 0) + (p.need_vel ? 3 : 0) + p.n_scalars;
+  return nin <= kG2MaxIn;
+}
+
 static size_t fused_smem_bytes(int nin) {
   return (size_t)(kRing * nin + kNumD + 4) * kArr * sizeof(double) + 2 * kNN;
 }
@@ -834,6 +1192,8 @@ int launch_fused_prepare() {
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_TRY(launch_stream_prepare());
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused2_smem_bytes(kG2MaxIn)));
   int dev = 0;
   NKB_CUDA(cudaGetDevice(&dev));
   NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -847,7 +1207,16 @@ int launch_fused_prepare() {
 int surface_pass_of(const FusedParams& p) {
   const char* v = getenv("NKB_STREAM");
   const bool on = v == nullptr || v[0] != '0';
-  return (on && p.prof == nullptr && stream_eligible(p)) ? 1 : 0;
+  if (on && p.prof == nullptr && stream_eligible(p)) return 1;
+  return fused2_on(p) ? 2 : 0;
+}
+
+// triangle regions (CTAs) of the pass that runs `p`
+int fused_grid_for(const FusedParams& p, int64_t n_elements) {
+  const int g = fused_grid(n_elements);                 // min(E, SMs)
+  if (surface_pass_of(p) != 2) return g;
+  const int64_t g2 = (int64_t)kG2PerSM * g_num_sms;
+  return (int)(n_elements < g2 ? (n_elements < 1 ? 1 : n_elements) : g2);
 }
 
 int launch_fused(const FusedParams& p, cudaStream_t s) {
@@ -880,7 +1249,14 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   NKB_TRY(launch_fused_prepare());
   const int grid = fused_grid(p.n_elements);
   const unsigned gx = (unsigned)grid;
-  if (surface_pass_of(p) == 1) return launch_stream(p, grid, s);
+  const int pass = surface_pass_of(p);
+  if (pass == 1) return launch_stream(p, grid, s);
+  if (pass == 2) {
+    fused2_kernel<<<(unsigned)fused_grid_for(p, p.n_elements), kG2Threads, fused2_smem_bytes(nin), s>>>(
+        q, nin, slot_sc, slot_vel, slot_xyz);
+    NKB_CUDA(cudaGetLastError());
+    return NKB_OK;
+  }
   if (p.prof) {
     if (cached) fused_kernel<true, true><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);
     else fused_kernel<false, true><<<gx, kThreads, shm, s>>>(q, nin, slot_sc, slot_vel, slot_xyz);

@@ -397,9 +397,34 @@ def test_stream_pass_matches_fused_pass_and_oracle(ctx, name, monkeypatch):
 
 
 def test_gradient_pipelines_use_fused_pass(ctx):
+    """Gradient pipelines run K1 (uncached geometry) or K1g (cached geometry,
+    two CTAs per SM, report.surface_pass == 2; NKB_FUSED2=0 forces K1)."""
     case = synth.box(nel=(2, 2, 2))
+    ctx.set_geometry_cache(False)
     _, res = _run(ctx, case, BOX_PIPES["q_iso"])
     assert res.report.surface_pass == 0
+    ctx.set_geometry_cache(True)
+    _, res = _run(ctx, case, BOX_PIPES["q_iso"])
+    assert res.report.surface_pass == 2
+
+
+@pytest.mark.parametrize("name", ["q_iso", "three_surfaces", "colour_wmag", "four_surfaces"])
+def test_two_cta_gradient_pass_matches_k1_and_oracle(ctx, name, monkeypatch):
+    """K1g (two 256-thread CTAs per SM) against K1 and the oracle: ordered
+    triangles and case words, fast-path multisets, images and ranges."""
+    case = synth.box(nel=(5, 4, 3))
+    ctx.set_geometry_cache(True)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("NKB_FUSED2", mode)
+        pipe = Pipeline(**{**BOX_PIPES[name].__dict__, "emit_meta": True})
+        _, res = _run(ctx, case, pipe)
+        assert res.report.surface_pass == (2 if mode == "1" else 0)
+        _check_against_oracle(ctx, case, pipe, res)
+        _, fast = _run(ctx, case, BOX_PIPES[name])
+        out[mode] = (_rows(ctx.triangles()), fast.rgba.copy(), fast.report.range)
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
 
 
 def test_large_triangles_raster_bit_exact(ctx):
