@@ -827,7 +827,8 @@ int launch_geometry(const double* x, const double* y, const double* z, int64_t E
 // waiting at them.  K1g runs TWO 256-thread CTAs per SM, each owning one
 // element at a time start to finish, so one CTA's barrier waits and load
 // latency are covered by the other CTA's work:
-//   - inputs double-buffered (cp.async, 8 B per node, the swizzled layout of K1);
+//   - inputs double-buffered (cp.async, 8 B per node, the swizzled layout of
+//     K1), issued by warps 6-7 while warps 0-5 run the pencils;
 //   - the cached J^-1 is read per node straight from global memory (coalesced),
 //     pulled toward L2 one element ahead by a bulk prefetch, instead of staged;
 //   - u,v,w pencils on 192 threads (pencil3 of K1), then 2 nodes per thread,
@@ -879,21 +880,26 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
   if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
 
   const int q0 = sw_node(tid), q1 = sw_node(tid + kG2Threads);
+  // staging of the next element by warps 6-7 (idle during the u,v,w pencils):
+  // 64 threads x 8 nodes per field, coalesced 8-byte cp.async
+  int qs[8];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) qs[h] = sw_node((tid & 63) + 64 * h);
   auto prefetch = [&](long long e, int b) {
     double* dst = S_ring + b * nin * kArr;
-    const long long g0 = e * (long long)kNN + tid;
+    const long long g0 = e * (long long)kNN + (tid & 63);
 #pragma unroll
     for (int f = 0; f < kG2MaxIn; ++f) {
       if (f < nin) {
         const double* src = p.in_ptr[f] + g0;
         double* d = dst + f * kArr;
-        cp_async8(d + q0, src);
-        cp_async8(d + q1, src + kG2Threads);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) cp_async8(d + qs[h], src + 64 * h);
       }
     }
   };
   if (n_it > 0) {
-    prefetch(blockIdx.x, 0);
+    if (tid >= 192) prefetch(blockIdx.x, 0);
     if (tid == 0) l2_prefetch(p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes);
   }
   cp_async_commit();
@@ -911,7 +917,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     }
     __syncthreads();                                   // element `it` staged; iteration it-1 finished
     if (it + 1 < n_it) {
-      prefetch(e + G, b ^ 1);
+      if (tid >= 192) prefetch(e + G, b ^ 1);
       if (tid == 0) l2_prefetch(p.geo + (e + G) * 9 * kNN, kGeoBytes);
     }
     cp_async_commit();
@@ -928,7 +934,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     // ---- node phase: nodes tid and tid + 256 ----
     const long long g0 = e * (long long)kNN;
     unsigned wand = ~0u, wor = 0u;
-#pragma unroll 1
+#pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int n = tid + kG2Threads * h;
       const int q = h ? q1 : q0;
