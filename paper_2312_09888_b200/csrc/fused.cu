@@ -923,6 +923,11 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     cp_async_commit();
     const double* S_in = S_ring + b * nin * kArr;
 
+    // J^-1 of my first node: loads in flight across the pencil phase
+    double J0[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) J0[c] = __ldg(p.geo + (e * 9 + c) * kNN + tid);
+
     // ---- u,v,w pencils: thread = (dir, pencil), 3 fields share offsets ----
     if (tid < 192) {
       const double* su = S_in + slot_vel * kArr;
@@ -940,7 +945,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       const int q = h ? q1 : q0;
       double J[9];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) J[c] = __ldg(p.geo + (e * 9 + c) * kNN + n);
+      for (int c = 0; c < 9; ++c) J[c] = h ? __ldg(p.geo + (e * 9 + c) * kNN + n) : J0[c];
       double U[9];
 #pragma unroll
       for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
