@@ -1,6 +1,6 @@
 #!/bin/bash
 # Run on the GPU box (via gpurun): plain bench, then the ncu launch list of the
-# same command, then one --set full capture of the fused kernel.  Outputs in
+# same command, then one --set full capture of the surface pass (K1g fused2_kernel for C2).  Outputs in
 # gpurun_out/; summarise locally with tools/summarize_profiles.py.
 set -u
 TAG=${1:-r01}
@@ -14,6 +14,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 echo "launch list rc=$?"
 PROBE="python tools/gpu_probe.py c2 --reps 2 --device-gen --geo on"
 $PROBE > gpurun_out/${TAG}_probe.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 1 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:fused -s 1 -c 1 \
     -f -o gpurun_out/${TAG}_fused $PROBE > gpurun_out/${TAG}_full.log 2>&1
 echo "full capture rc=$?"
