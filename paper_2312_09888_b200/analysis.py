@@ -223,6 +223,7 @@ class InsituAnalysis:
     def __init__(self, pipeline: Pipeline | dict[str, str]):
         self.pipeline = pipeline if isinstance(pipeline, Pipeline) else pipeline_from_params(pipeline)
         self._view: tuple[float, ...] | None = None
+        self._native = None                 # (pipeline, view, NkbPipeline): marshalled once, reused per step
         self.executions = 0
 
     def view_for(self, data_adaptor) -> tuple[float, ...]:
@@ -248,7 +249,9 @@ class InsituAnalysis:
     def execute(self, data_adaptor, fetch_image: bool = True, depth: bool = False) -> ExecuteResult:
         view = self.view_for(data_adaptor)
         ctx = data_adaptor.ctx
-        rep = ctx.execute(self.pipeline.native(view))
+        if self._native is None or self._native[0] is not self.pipeline or self._native[1] != view:
+            self._native = (self.pipeline, view, self.pipeline.native(view))
+        rep = ctx.execute(self._native[2])
         self.executions += 1
         res = ExecuteResult(rep, view=view)
         root = (ctx.nranks == 1) or (not self.pipeline.composite) or ctx.rank == 0

@@ -2,9 +2,10 @@
 # 1-GPU bench lines for every config, 2/4-GPU weak scaling of C2, C4 on 4
 # GPUs, and the reference arm.  Outputs: gpurun_out/<tag>/*.json
 set -u
-TAG=${1:-r04}
+TAG=${1:-r06}
 D=gpurun_out/$TAG
 mkdir -p $D
+timeout 1500 python -m pytest tests/test_gpu_multi.py tests/test_gpu_stats.py tests/test_gpu_dssum.py -q -x > $D/pytest_multi.log 2>&1; echo "pytest multi rc=$?"; tail -1 $D/pytest_multi.log
 for c in c1 c2 c3 c4; do
   python bench.py --config $c --steps 20 --warmup 5 > $D/${c}_1.json 2> $D/${c}_1.err; echo "$c n=1 rc=$?"
 done
@@ -14,4 +15,6 @@ for n in 2 4; do
 done
 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29600 \
   bench.py --gpus 4 --steps 10 --warmup 3 --config c4 --e2e-max-gb 4 > $D/c4_4.json 2> $D/c4_4.err; echo "c4 n=4 rc=$?"
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29700 \
+  bench.py --gpus 4 --steps 10 --warmup 3 --config c3 --e2e-max-gb 4 > $D/c3_4.json 2> $D/c3_4.err; echo "c3 n=4 rc=$?"
 python bench.py --impl reference --steps 3 --warmup 3 > $D/ref_1.json 2> $D/ref_1.err; echo "ref rc=$?"
