@@ -73,6 +73,7 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device = device
+        self.interval = float(os.environ.get("NKB_CLOCK_SAMPLE_MS", "2")) / 1e3   # NVML poll period
         self.samples: list[tuple[float, int]] = []
         self.max_mhz = None
         self._stop = threading.Event()
@@ -104,7 +105,7 @@ class ClockSampler:
                 self.samples.append((float(mhz), int(rs)))
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(self.interval)
 
     def stop(self) -> dict:
         if self._nv is None:
