@@ -115,7 +115,8 @@ typedef struct {
     int     geometry_cached;      /* 1 if the step used the geometry cache */
     float   ms_geometry;          /* time spent (re)building the cache this step (when timing) */
     int     surface_pass;         /* surface pass that ran: 0 = K1 fused (velocity gradient),
-                                     1 = K1s stream (no gradient; NKB_STREAM=0 forces K1) */
+                                     1 = K1s stream (no gradient; NKB_STREAM=0 forces K1),
+                                     2 = K1g two-CTA gradient pass (geometry cache; NKB_FUSED2=0 forces K1) */
 } nkb_report;
 
 typedef struct {

@@ -27,7 +27,7 @@ class Report:
     reran: bool
     geometry_cached: bool = False
     ms_geometry: float = 0.0
-    surface_pass: int = 0          # 0: K1 fused (gradients), 1: K1s stream (no gradient)
+    surface_pass: int = 0          # 0: K1 fused, 1: K1s stream (no gradient), 2: K1g (cached geometry)
 
     @classmethod
     def from_native(cls, r: N.NkbReport) -> "Report":
