@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
       dep = __uint_as_float((unsigned)(key >> 32));
       double t = hi > lo ? __ddiv_rn(__dsub_rn(s, lo), span) : 0.0;
       t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
-      o = make_uchar4(rdev::cmap_channel(p.cmap, t, 0), rdev::cmap_channel(p.cmap, t, 1), rdev::cmap_channel(p.cmap, t, 2), 255);
+      o = rdev::cmap_rgba(p.cmap, t);
     }
     reinterpret_cast<uchar4*>(p.root_rgba)[i] = o;
     p.root_depth[i] = dep;

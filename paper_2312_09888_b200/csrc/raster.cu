@@ -69,8 +69,7 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
       const double s = (double)__uint_as_float((unsigned)(key & 0xffffffffULL));
       dep = __uint_as_float((unsigned)(key >> 32));
       const double t = clip01(hi > lo ? __ddiv_rn(__dsub_rn(s, lo), span) : 0.0);
-      o = make_uchar4(rdev::cmap_channel(p.cmap, t, 0), rdev::cmap_channel(p.cmap, t, 1),
-                      rdev::cmap_channel(p.cmap, t, 2), 255);
+      o = rdev::cmap_rgba(p.cmap, t);
     }
     reinterpret_cast<uchar4*>(p.rgba)[i] = o;
     if (p.depth) p.depth[i] = dep;
@@ -151,9 +150,10 @@ __global__ void __launch_bounds__(256) structured_render_kernel(const Structured
     s = __dadd_rn(s, __dmul_rn(__dmul_rn(t10, ay), omax));
     s = __dadd_rn(s, __dmul_rn(__dmul_rn(t11, ay), ax));
     const double t = clip01(s);
-    p.rgb[3 * i + 0] = rdev::cmap_channel(p.cmap, t, 0);
-    p.rgb[3 * i + 1] = rdev::cmap_channel(p.cmap, t, 1);
-    p.rgb[3 * i + 2] = rdev::cmap_channel(p.cmap, t, 2);
+    const uchar4 o = rdev::cmap_rgba(p.cmap, t);
+    p.rgb[3 * i + 0] = o.x;
+    p.rgb[3 * i + 1] = o.y;
+    p.rgb[3 * i + 2] = o.z;
   }
 }
 

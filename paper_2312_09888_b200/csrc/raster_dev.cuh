@@ -44,6 +44,31 @@ __device__ __forceinline__ unsigned char cmap_channel(const Colormap& cm, double
 }
 
 
+// all three channels with one anchor search (the per-channel arithmetic of
+// cmap_channel, unchanged)
+__device__ __forceinline__ uchar4 cmap_rgba(const Colormap& cm, double t) {
+  if (t != t) return make_uchar4(0, 0, 0, 255);
+  const int n = cm.n;
+  unsigned char o[3];
+  if (t >= cm.t[n - 1]) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) o[ch] = (unsigned char)floor(__dadd_rn(cm.rgb[n - 1][ch], 0.5));
+  } else {
+    int j = 0;
+    for (int k = 1; k < n - 1; ++k)
+      if (t >= cm.t[k]) j = k;
+    const double tj = cm.t[j];
+    const bool at = t == tj;
+    const double dt = __dsub_rn(t, tj);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const double v = at ? cm.rgb[j][ch] : __dadd_rn(__dmul_rn(cm.slope[j][ch], dt), cm.rgb[j][ch]);
+      o[ch] = (unsigned char)floor(__dadd_rn(v, 0.5));
+    }
+  }
+  return make_uchar4(o[0], o[1], o[2], 255);
+}
+
 constexpr double kGuard = 32768.0;   // |screen coordinate| bound in pixels
 
 __device__ __forceinline__ void xform(const double* V, double x, double y, double z, double& sx,
