@@ -25,15 +25,19 @@ __global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
     z[i] = ~0ULL;
 }
 
-// one thread per triangle; blockIdx.y = triangle region (the count lives on the device)
+// one thread per triangle; blockIdx.y = triangle region (the count lives on
+// the device).  The region's warps take 32 consecutive triangles each
+// (coalesced reads) and are dealt round-robin over the region's blocks, so a
+// region with few triangles still spreads over several SMs.
 __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
   const int r = blockIdx.y;
   long long ntri = (long long)p.region_count[r];
   if (ntri > p.region_cap) ntri = p.region_cap;
   const float4* tri = p.tri + 3 * (long long)r * p.region_cap;
   const int W = p.width, H = p.height;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntri;
-       t += (long long)gridDim.x * blockDim.x) {
+  const long long gw = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;   // region-local warp
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long t = gw * 32 + (threadIdx.x & 31); t < ntri; t += nw * 32) {
     rdev::raster_triangle(p.view, W, H, tri + 3 * t, p.zbuf);
   }
 }

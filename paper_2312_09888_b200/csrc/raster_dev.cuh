@@ -138,28 +138,42 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
     bias[i] = (dy > 0 || (dy == 0 && dx < 0)) ? 0 : -1;   // inclusive (top-left) edges
   }
   const double inv = __drcp_rn((double)area);     // == 1.0 / area: one IEEE division per triangle
-  for (long long py = py0; py <= py1; ++py) {
-    const long long cy = py * 256 + 128;
-    for (long long px = px0; px <= px1; ++px) {
-      const long long cx = px * 256 + 128;
-      long long w[3];
+  // edge functions stepped incrementally: w_i(cx + 256) = w_i(cx) - 256 (Yb - Ya),
+  // w_i(cy + 256) = w_i(cy) + 256 (Xb - Xa) -- exact int64, the same values as
+  // evaluating w_i at every pixel centre
+  long long dwx[3], dwy[3], wrow[3];
+  {
+    const long long cy0 = py0 * 256 + 128, cx0 = px0 * 256 + 128;
 #pragma unroll
-      for (int i = 0; i < 3; ++i)
-        w[i] = (X[eb[i]] - X[ea[i]]) * (cy - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx - X[ea[i]]);
-      if (w[0] + bias[0] < 0 || w[1] + bias[1] < 0 || w[2] + bias[2] < 0) continue;
-      double d = __dmul_rn(__fma_rn((double)w[2], Z[2],
-                                    __fma_rn((double)w[1], Z[1], __dmul_rn((double)w[0], Z[0]))),
-                           inv);
-      if (!(d >= 0.0 && d <= 1.0)) continue;
-      d = __dadd_rn(d, 0.0);
-      const double c = __dmul_rn(__fma_rn((double)w[2], C[2],
-                                          __fma_rn((double)w[1], C[1], __dmul_rn((double)w[0], C[0]))),
-                                 inv);
-      const unsigned long long key =
-          ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
-          (unsigned long long)__float_as_uint(__double2float_rn(c));
-      atomicMin(zbuf + py * W + px, key);
+    for (int i = 0; i < 3; ++i) {
+      dwx[i] = -(Y[eb[i]] - Y[ea[i]]) * 256;
+      dwy[i] = (X[eb[i]] - X[ea[i]]) * 256;
+      wrow[i] = (X[eb[i]] - X[ea[i]]) * (cy0 - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx0 - X[ea[i]]);
     }
+  }
+  for (long long py = py0; py <= py1; ++py) {
+    long long w[3] = {wrow[0], wrow[1], wrow[2]};
+    for (long long px = px0; px <= px1; ++px) {
+      if (w[0] + bias[0] >= 0 && w[1] + bias[1] >= 0 && w[2] + bias[2] >= 0) {
+        double d = __dmul_rn(__fma_rn((double)w[2], Z[2],
+                                      __fma_rn((double)w[1], Z[1], __dmul_rn((double)w[0], Z[0]))),
+                             inv);
+        if (d >= 0.0 && d <= 1.0) {
+          d = __dadd_rn(d, 0.0);
+          const double c = __dmul_rn(__fma_rn((double)w[2], C[2],
+                                              __fma_rn((double)w[1], C[1], __dmul_rn((double)w[0], C[0]))),
+                                     inv);
+          const unsigned long long key =
+              ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
+              (unsigned long long)__float_as_uint(__double2float_rn(c));
+          atomicMin(zbuf + py * W + px, key);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) w[i] += dwx[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) wrow[i] += dwy[i];
   }
 }
 
