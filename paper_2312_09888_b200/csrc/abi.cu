@@ -785,8 +785,11 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   if (p2p) {
     // fused sort-last composite + resolve over NVLink peer memory
     NKB_TRY(launch_p2p_signal(pp, 0, nullptr, s));
+    if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[6], s));
     NKB_TRY(launch_p2p_composite(pp, s));
+    if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[7], s));
     NKB_TRY(launch_p2p_signal(pp, 1, ctx->counters, s));
+    if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[8], s));
     if (ctx->rank == 0) NKB_TRY(launch_p2p_wait(pp, 1, 0, s));
   } else if (composite) {
     NKB_NCCL(g_nccl.GroupStart());
@@ -1091,6 +1094,15 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
       cudaEventElapsedTime(&out->ms_fused, ctx->ev[0], ctx->ev[1]);
       cudaEventElapsedTime(&out->ms_raster, ctx->ev[1], ctx->ev[2]);
       cudaEventElapsedTime(&out->ms_composite, ctx->ev[2], ctx->ev[3]);
+      if (ctx->p2p.ready && p->composite && ctx->nranks > 1 && getenv("NKB_TIMING_DETAIL")) {
+        float a = 0, b = 0, c = 0, d = 0;              // signal(ready) | composite (incl. peer wait) | signal(done) | done wait
+        cudaEventElapsedTime(&a, ctx->ev[2], ctx->ev[6]);
+        cudaEventElapsedTime(&b, ctx->ev[6], ctx->ev[7]);
+        cudaEventElapsedTime(&c, ctx->ev[7], ctx->ev[8]);
+        cudaEventElapsedTime(&d, ctx->ev[8], ctx->ev[3]);
+        fprintf(stderr, "[nkb composite rank %d] signal %.4f composite %.4f signal %.4f wait %.4f ms\n", ctx->rank, a,
+                b, c, d);
+      }
       cudaEventElapsedTime(&out->ms_resolve, ctx->ev[3], ctx->ev[4]);
     }
   }

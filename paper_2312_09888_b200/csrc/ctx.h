@@ -125,7 +125,7 @@ struct nkb_ctx {
   // comm
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[9] = {};                   // stage events; 6-8: P2P composite detail (timing)
   // geometry cache: 9 SoA arrays of d(r,s,t)/d(x,y,z) (fused.cu geometry_kernel)
   bool geo_enabled = true;
   bool geo_valid = false;
