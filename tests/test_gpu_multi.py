@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _image(rank, size, out_dir, steps=3):
+def _image(rank, size, out_dir, steps=3, cuts=None):
     import torch.distributed as dist
 
     from paper_2312_09888_b200 import synth
@@ -34,7 +34,7 @@ def _image(rank, size, out_dir, steps=3):
 
     nel = (4, 4, 6)
     E = nel[0] * nel[1] * nel[2]
-    e0, e1 = synth.partition(E, rank, size)
+    e0, e1 = synth.partition(E, rank, size) if cuts is None else (cuts[rank], cuts[rank + 1])
     c = synth.box(e0, e1, nel=nel)
     ctx = Context(rank)
     comm = Communicator.from_torch(ctx)
@@ -53,13 +53,13 @@ def _image(rank, size, out_dir, steps=3):
     comm.close()
 
 
-def _worker(rank, size, port, out_dir, mode="p2p"):
+def _worker(rank, size, port, out_dir, mode="p2p", cuts=None):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank), NKB_COMPOSITE=mode)
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
-        _image(rank, size, out_dir)
+        _image(rank, size, out_dir, cuts=cuts)
     finally:
         dist.destroy_process_group()
 
@@ -82,6 +82,24 @@ def test_composite_equals_single_gpu(tmp_path, size, mode):
     mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
     mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), mode), nprocs=size, join=True)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / f"g{size}.npz")
+    assert int(a["n"]) == int(b["n"])
+    assert np.array_equal(a["rng"], b["rng"])
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
+
+
+def test_composite_ragged_partitions_p2p(tmp_path):
+    """Ragged partitions with an empty rank in the middle (E = 0 on rank 1):
+    the P2P composite over 3 ranks still reproduces the one-GPU image bit for
+    bit (the empty rank contributes an all-background key buffer)."""
+    if _ngpus() < 3:
+        pytest.skip("needs 3 GPUs")
+    import torch.multiprocessing as mp
+
+    E = 4 * 4 * 6
+    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), "p2p"), nprocs=1, join=True)
+    mp.spawn(_worker, args=(3, _free_port(), str(tmp_path), "p2p", (0, 17, 17, E)), nprocs=3, join=True)
+    a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g3.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
     assert np.array_equal(a["rgba"], b["rgba"])
