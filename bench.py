@@ -307,7 +307,10 @@ def run_ours(a):
         hblk = SemBlock(case.n_elements, host["x"], host["y"], host["z"], fields=hfields, element_offset=case.e0,
                         n_elements_global=case.n_elements_global)
         tmpdir = tempfile.mkdtemp(prefix="nkb_e2e_")
-        params = {**case.params, "width": str(a.width), "height": str(a.width), "dir": tmpdir}
+        # the PPM write of step i overlaps step i+1's H2D (writer thread); the
+        # last write is waited for inside the timed region (sink.flush)
+        params = {**case.params, "width": str(a.width), "height": str(a.width), "dir": tmpdir,
+                  "async_write": "0" if a.e2e_sync_write else "1"}
         sink = InsituSink(params, comm=comm)
         e2e_steps = max(3, min(a.steps, 10))
         step = 0
@@ -319,12 +322,16 @@ def run_ours(a):
         for _ in range(e2e_steps):
             sink.consume(Snapshot(0.0, step, rank, (hblk,)))
             step += 1
+        sink.flush()
         e1.record(stream)
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+        sink.finalize()
         e2e = {"value": world * npts / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(sink.adaptor.h2d_bytes), "d2h_bytes_per_step": int(a.width * a.width * 4 + 48),
-               "path": "InsituSink.consume(host pinned snapshot) -> H2D -> execute -> D2H RGBA -> PPM"}
+               "path": "InsituSink.consume(host pinned snapshot) -> H2D -> execute -> D2H RGBA -> PPM"
+                       + (" (written synchronously)" if a.e2e_sync_write else
+                          " (written on a writer thread, overlapping the next step's H2D; last write waited for)")}
     else:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": int(host_bytes), "d2h_bytes_per_step": 0,
                "skipped": f"partition needs {host_bytes / 1e9:.1f} GB of pinned host memory (> --e2e-max-gb)"}
@@ -549,6 +556,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-max-gb", type=float, default=12.0)
+    ap.add_argument("--e2e-sync-write", action="store_true", help="write each PPM inside consume() (no writer thread)")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3

@@ -213,6 +213,14 @@ class InsituSink:
         self.adaptor: SemDataAdaptor | None = None   # created on first consume (needs the GPU)
         self.analysis = InsituAnalysis(self.pipeline)
         self.last = None
+        # async_write=1: the PPM write of step i runs on a writer thread while
+        # step i+1's fields cross PCIe; consume() waits for the previous write
+        # before the library's pinned PPM buffer is reused, and flush() /
+        # finalize() wait for the last one.  Default 0: the file is complete
+        # when consume() returns, as in the reference (sinks.py:346-351).
+        self.async_write = params.get("async_write", "0").strip().lower() in ("1", "true", "yes", "on")
+        self._writer = None
+        self._pending = None
         root = comm is None or comm.rank == 0
         if root:
             self.dir.mkdir(parents=True, exist_ok=True)
@@ -228,16 +236,39 @@ class InsituSink:
         self.last = res
         if not ((ctx.nranks == 1) or (not self.pipeline.composite) or ctx.rank == 0):
             return 0
+        self.flush()                  # the previous write still reads the pinned PPM buffer
         # header + RGB packed on the GPU into pinned memory: same bytes as
         # write_ppm(ImageRGB(w, h, rgba[..., :3].tobytes())) (sinks.py:298-303)
         ppm = ctx.image_ppm()
-        fname = f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}.ppm"
-        with open(self.dir / fname, "wb") as f:
-            f.write(ppm)
+        path = self.dir / f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}.ppm"
+        if self.async_write:
+            if self._writer is None:
+                from concurrent.futures import ThreadPoolExecutor
+
+                self._writer = ThreadPoolExecutor(max_workers=1, thread_name_prefix="nkb-ppm")
+            self._pending = self._writer.submit(_write_bytes, path, ppm)
+        else:
+            _write_bytes(path, ppm)
         return len(ppm)
 
+    def flush(self):
+        """Wait for the pending PPM write (async_write); re-raises its error."""
+        pending, self._pending = self._pending, None
+        if pending is not None:
+            pending.result()
+
     def finalize(self):
-        pass
+        try:
+            self.flush()
+        finally:
+            if self._writer is not None:
+                self._writer.shutdown(wait=True)
+                self._writer = None
+
+
+def _write_bytes(path, data) -> None:
+    with open(path, "wb") as f:
+        f.write(data)
 
 
 def _device_len(d) -> int:

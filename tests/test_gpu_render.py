@@ -117,6 +117,35 @@ def test_insitu_sink_through_bridge(tmp_path):
     assert sums[0].invocations == 3 and sums[1].invocations == 5
 
 
+def test_insitu_sink_async_write_same_files(tmp_path):
+    """async_write=1 (PPM of step i written while step i+1 runs) leaves the
+    same files, byte for byte, as the synchronous sink once finalize() ran."""
+    from paper_2312_09888_b200.sinks import InsituSink
+
+    case = synth.box(nel=(3, 2, 2))
+    vel = case.fields["velocity"]
+
+    def blk(st):      # a different temperature every step: a write racing the next step would show
+        t = case.fields["temperature"].ravel() + 0.07 * st
+        fields = (FieldArray("velocity", POINT, 3, vel.ravel(), comp_stride=case.n_points),
+                  FieldArray("temperature", POINT, 1, t))
+        return SemBlock(case.n_elements, case.x, case.y, case.z, fields=fields)
+
+    out = {}
+    for mode in ("0", "1"):
+        d = tmp_path / f"w{mode}"
+        sink = InsituSink({"dir": str(d), "iso": "Q=0.5;temperature=0.6", "field": "temperature",
+                           "width": "96", "height": "64", "view": "30,40", "async_write": mode})
+        assert sink.async_write == (mode == "1")
+        n = sum(sink.consume(Snapshot(0.1 * st, st, 0, (blk(st),))) for st in range(4))
+        sink.finalize()
+        out[mode] = {p.name: p.read_bytes() for p in sorted(d.glob("*.ppm"))}
+        assert n == 4 * (len("P6\n96 64\n255\n") + 96 * 64 * 3)
+    assert list(out["0"]) == [f"step{s:06d}_temperature.ppm" for s in range(4)]
+    assert out["0"] == out["1"]
+    assert len(set(out["0"].values())) == 4
+
+
 def test_failing_insitu_sink_is_isolated(tmp_path):
     doc = (f'<sensei><analysis type="insitu" frequency="1" dir="{tmp_path}/o" iso="nope=1" field="temperature"/>'
            f'<analysis type="null" frequency="1"/></sensei>')
