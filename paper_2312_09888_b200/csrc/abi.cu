@@ -89,6 +89,7 @@ static void p2p_release(nkb_ctx* ctx) {
   ctx->p2p.err = nullptr;
   ctx->p2p.dev_epoch = nullptr;
   ctx->p2p.h_res = nullptr;
+  ctx->p2p.h_res_dev = nullptr;
   ctx->p2p.ready = false;
   for (int k = 0; k < 2; ++k) {                       // captured steps reference these buffers
     if (ctx->graph_exec[k]) cudaGraphExecDestroy(ctx->graph_exec[k]);
@@ -117,6 +118,7 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
   NKB_CUDA(cudaMalloc(&P.dev_epoch, sizeof(unsigned long long)));
   NKB_CUDA(cudaMemset(P.dev_epoch, 0, sizeof(unsigned long long)));
   NKB_CUDA(cudaMallocHost(&P.h_res, (1 + kMaxRanks) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaHostGetDevicePointer((void**)&P.h_res_dev, P.h_res, 0));
   constexpr int kH = 5;
   cudaIpcMemHandle_t mine[kH];
   void* ptrs[kH] = {P.keys[0], P.keys[1], P.flags, ctx->rgba, ctx->depth};
@@ -211,6 +213,7 @@ int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
   c->ticket = reinterpret_cast<unsigned int*>(c->counters + 4);
   NKB_CUDA(cudaMalloc(&c->range_dev, 2 * sizeof(double)));
   NKB_CUDA(cudaMallocHost(&c->h_counters, (8 + kMaxRegions) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaHostGetDevicePointer((void**)&c->h_counters_dev, c->h_counters, 0));
   NKB_CUDA(cudaMalloc(&c->region_count, kMaxRegions * sizeof(unsigned long long)));
   for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
   if (const char* g = getenv("NKB_GEOM_CACHE")) c->geo_enabled = strcmp(g, "0") != 0;
@@ -815,18 +818,16 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     NKB_TRY(launch_resolve(rs, s));
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[4], s));
-  NKB_CUDA(cudaMemcpyAsync(ctx->h_counters, ctx->counters, 4 * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, s));
-  NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 4, ctx->range_dev, 2 * sizeof(double),
-                           cudaMemcpyDeviceToHost, s));
-  if (!ordered)
-    NKB_CUDA(cudaMemcpyAsync(ctx->h_counters + 8, ctx->region_count,
-                             sizeof(unsigned long long) * ctx->n_regions, cudaMemcpyDeviceToHost, s));
-  if (p2p) {
-    NKB_CUDA(cudaMemcpyAsync(ctx->p2p.h_res, ctx->p2p.err, sizeof(int), cudaMemcpyDeviceToHost, s));
-    NKB_CUDA(cudaMemcpyAsync(ctx->p2p.h_res + 1, ctx->p2p.flags + 2 * kMaxRanks,
-                             sizeof(unsigned long long) * kMaxRanks, cudaMemcpyDeviceToHost, s));
-  }
+  ReportParams rep;
+  rep.counters = ctx->counters;
+  rep.range = ctx->range_dev;
+  rep.region_count = ordered ? nullptr : ctx->region_count;
+  rep.n_regions = ordered ? 0 : ctx->n_regions;
+  rep.h_counters = ctx->h_counters_dev;
+  rep.err = p2p ? ctx->p2p.err : nullptr;
+  rep.peer_counts = p2p ? ctx->p2p.flags + 2 * kMaxRanks : nullptr;
+  rep.h_res = p2p ? ctx->p2p.h_res_dev : nullptr;
+  NKB_TRY(launch_report(rep, s));
   return NKB_OK;
 }
 

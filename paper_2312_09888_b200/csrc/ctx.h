@@ -117,6 +117,7 @@ struct nkb_ctx {
   int64_t last_ntri = 0;
   // pinned host staging
   unsigned long long* h_counters = nullptr;  // 4 + 2 (range)
+  unsigned long long* h_counters_dev = nullptr;  // mapped device pointer of h_counters
   // structured renderer scratch
   const double** s_ptrs = nullptr;
   int64_t* s_col0 = nullptr;
@@ -161,6 +162,7 @@ struct nkb_ctx {
     unsigned long long epoch = 0;            // host copy of the step epoch
     unsigned long long* dev_epoch = nullptr; // device counter read by the P2P kernels
     unsigned long long* h_res = nullptr;     // pinned: [0] timeout flag, [1..] per-rank triangles
+    unsigned long long* h_res_dev = nullptr; // its mapped device pointer (report_kernel writes it)
   } p2p;
 };
 

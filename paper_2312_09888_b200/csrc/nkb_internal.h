@@ -140,6 +140,19 @@ int launch_p2p_signal(const P2PParams& p, int which, const unsigned long long* c
 int launch_p2p_wait(const P2PParams& p, int which, unsigned long long back, cudaStream_t s);
 int launch_p2p_composite(const P2PParams& p, cudaStream_t s);
 
+// step report -> mapped pinned host words (device pointers of cudaMallocHost memory)
+struct ReportParams {
+  const unsigned long long* counters;       // [4]
+  const double* range;                      // [2]
+  const unsigned long long* region_count;   // [n_regions] or null (ordered mode)
+  int n_regions;
+  unsigned long long* h_counters;           // host words [0..3] counters, [4..5] range bits, [8..] regions
+  const int* err;                           // P2P: timeout flag, or null
+  const unsigned long long* peer_counts;    // P2P: [kMaxRanks] per-rank triangle counts
+  unsigned long long* h_res;                // P2P host words [0] timeout, [1..] counts, or null
+};
+int launch_report(const ReportParams& p, cudaStream_t s);
+
 struct ResolveParams {
   const unsigned long long* zbuf;
   int width, height;

@@ -48,6 +48,20 @@ __global__ void range_words_kernel(const unsigned long long* counters, unsigned 
   words[1] = ~counters[2];
 }
 
+// the step's report words straight into mapped pinned host memory: one
+// kernel instead of 3-5 small D2H copies at the tail of every step
+__global__ void __launch_bounds__(256) report_kernel(const ReportParams p) {
+  const int t = threadIdx.x;
+  if (t < 4) p.h_counters[t] = p.counters[t];
+  if (t == 4 || t == 5) p.h_counters[t] = (unsigned long long)__double_as_longlong(p.range[t - 4]);
+  if (p.region_count)
+    for (int i = t; i < p.n_regions; i += blockDim.x) p.h_counters[8 + i] = p.region_count[i];
+  if (p.h_res) {
+    if (t == 0) p.h_res[0] = (unsigned long long)(unsigned)*p.err;
+    if (t < kMaxRanks) p.h_res[1 + t] = *(volatile const unsigned long long*)(p.peer_counts + t);
+  }
+}
+
 __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
   double lo = p.vmin, hi = p.vmax;
   if (p.range_words) {
@@ -214,6 +228,12 @@ int launch_pack_rgb(const unsigned char* rgba, unsigned char* rgb, int64_t npx, 
   if (npx <= 0) return NKB_OK;
   pack_rgb_kernel<<<grid_for(npx / 4 + 1, 256, 148 * 8), 256, 0, s>>>(reinterpret_cast<const uchar4*>(rgba), rgb,
                                                                      (long long)npx);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_report(const ReportParams& p, cudaStream_t s) {
+  report_kernel<<<1, 256, 0, s>>>(p);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
