@@ -858,7 +858,7 @@ __device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
 }
 
 __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const FusedParams p, int nin, int slot_sc,
-                                                                     int slot_vel, int slot_xyz) {
+                                                                     int slot_vel, int slot_xyz, int plane_slots) {
   extern __shared__ __align__(16) double smem[];
   double* S_ring = smem;                               // 2 * nin * 512
   double* S_dv = S_ring + 2 * nin * kArr;              // 9 * 512 u,v,w derivatives
@@ -906,6 +906,13 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
 
   int off[kNP];                                        // pencil offsets (threads < 192)
   pencil_offsets(tid >> 6 < 3 ? tid >> 6 : 0, tid & 7, (tid >> 3) & 7, off);
+  // staged slot of x, y, z for the slice planes (-1: no plane has a nonzero
+  // normal component there, so the coordinate is not staged and enters the
+  // node-phase distance as 0; only the case bits use it, and a zero of either
+  // sign compares the same against the iso value)
+  const int psx = (plane_slots & 0xff) == 0xff ? -1 : (plane_slots & 0xff);
+  const int psy = ((plane_slots >> 8) & 0xff) == 0xff ? -1 : ((plane_slots >> 8) & 0xff);
+  const int psz = ((plane_slots >> 16) & 0xff) == 0xff ? -1 : ((plane_slots >> 16) & 0xff);
 
   for (long long it = 0; it < n_it; ++it) {
     const long long e = blockIdx.x + it * G;
@@ -984,8 +991,8 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
         const int src = p.surf_src[s];
         double val;
         if (src >= SRC_PLANE)
-          val = plane_dist(p.surf_n[s], S_in[slot_xyz * kArr + q], S_in[(slot_xyz + 1) * kArr + q],
-                           S_in[(slot_xyz + 2) * kArr + q]);
+          val = plane_dist(p.surf_n[s], psx >= 0 ? S_in[psx * kArr + q] : 0.0,
+                           psy >= 0 ? S_in[psy * kArr + q] : 0.0, psz >= 0 ? S_in[psz * kArr + q] : 0.0);
         else if (src == SRC_Q) val = vq;
         else if (src == SRC_WMAG) val = vw;
         else if (src == SRC_UMAG) val = vu;
@@ -1086,8 +1093,11 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     const double* Sy = xyz_staged ? S_in + (slot_xyz + 1) * kArr : p.y + g0;
     const double* Sz = xyz_staged ? S_in + (slot_xyz + 2) * kArr : p.z + g0;
     const double* Su = S_in + slot_vel * kArr;
-    auto value_at = [&](int src, int s, int q) -> double {
-      if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[q], Sy[q], Sz[q]);
+    // pn: the node's index in Sx/Sy/Sz (swizzled when staged, natural in global
+    // memory otherwise); the edge's plane distances always use all three
+    // coordinates, exactly as the oracle does
+    auto value_at = [&](int src, int s, int q, int pn) -> double {
+      if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[pn], Sy[pn], Sz[pn]);
       if (src == SRC_Q) return S_q[q];
       if (src == SRC_WMAG) return S_q[kArr + q];
       if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
@@ -1129,11 +1139,11 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
       const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
       const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
-      const double sa = value_at(src, s, qa), sb = value_at(src, s, qb);
-      const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
-      const double cla = value_at(p.color_src, 0, qa), clb = value_at(p.color_src, 0, qb);
       const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
       const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
+      const double sa = value_at(src, s, qa, pa), sb = value_at(src, s, qb, pb);
+      const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
+      const double cla = value_at(p.color_src, 0, qa, pa), clb = value_at(p.color_src, 0, qb, pb);
       const double xa = Sx[pa], ya = Sy[pa], za = Sz[pa];
       const double xb = Sx[pb], yb = Sy[pb], zb = Sz[pb];
       float4 v;
@@ -1179,13 +1189,22 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
 
 static size_t fused2_smem_bytes(int nin) { return (size_t)(2 * nin + 11) * kArr * sizeof(double) + kNN; }
 
+// coordinates the slice planes use: bit c set when some plane's normal has a
+// nonzero component c (K1g stages only those; emission reads x,y,z via L2)
+static unsigned plane_axes(const FusedParams& p) {
+  unsigned m = 0;
+  for (int i = 0; i < p.n_surf; ++i)
+    if (p.surf_src[i] >= SRC_PLANE)
+      for (int c = 0; c < 3; ++c) m |= (p.surf_n[i][c] != 0.0 ? 1u : 0u) << c;
+  return m;
+}
+
 static bool fused2_on(const FusedParams& p) {
   const char* v = getenv("NKB_FUSED2");               // A/B: NKB_FUSED2=0 forces K1
   if (v && v[0] == '0') return false;
   if (!(p.geo != nullptr && p.need_grad) || p.prof != nullptr) return false;
-  bool has_plane = false;
-  for (int i = 0; i < p.n_surf; ++i) has_plane |= p.surf_src[i] >= SRC_PLANE;
-  const int nin = (has_plane ? 3 : 0) + (p.need_vel ? 3 : 0) + p.n_scalars;
+  const unsigned m = plane_axes(p);
+  const int nin = (int)((m & 1) + ((m >> 1) & 1) + (m >> 2)) + (p.need_vel ? 3 : 0) + p.n_scalars;
   return nin <= kG2MaxIn;
 }
 
@@ -1263,8 +1282,32 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
   const int pass = surface_pass_of(p);
   if (pass == 1) return launch_stream(p, grid, s);
   if (pass == 2) {
-    fused2_kernel<<<(unsigned)fused_grid_for(p, p.n_elements), kG2Threads, fused2_smem_bytes(nin), s>>>(
-        q, nin, slot_sc, slot_vel, slot_xyz);
+    // K1g (always cached): stage only the coordinates a slice plane needs
+    const unsigned m = plane_axes(p);
+    FusedParams q2 = p;
+    int k2 = 0, slot2_xyz = -1, slot2_vel = 0, ps = 0;
+    if (m == 7u) {
+      slot2_xyz = 0;
+      for (int c = 0; c < 3; ++c) q2.in_ptr[k2++] = c == 0 ? p.x : c == 1 ? p.y : p.z;
+      ps = 0 | (1 << 8) | (2 << 16);
+    } else {
+      for (int c = 0; c < 3; ++c) {
+        if (m & (1u << c)) {
+          ps |= k2 << (8 * c);
+          q2.in_ptr[k2++] = c == 0 ? p.x : c == 1 ? p.y : p.z;
+        } else {
+          ps |= 0xff << (8 * c);
+        }
+      }
+    }
+    if (p.need_vel) {
+      slot2_vel = k2;
+      for (int c = 0; c < 3; ++c) q2.in_ptr[k2++] = p.vel[c];
+    }
+    const int slot2_sc = k2;
+    for (int c = 0; c < p.n_scalars; ++c) q2.in_ptr[k2++] = p.scalar[c];
+    fused2_kernel<<<(unsigned)fused_grid_for(p, p.n_elements), kG2Threads, fused2_smem_bytes(k2), s>>>(
+        q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps);
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
   }

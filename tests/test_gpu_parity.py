@@ -75,6 +75,16 @@ BOX_PIPES = {
                                color_field="temperature", background=(10, 20, 30, 40),
                                anchors=((0.0, (0, 0, 0)), (0.3, (255, 0, 0)), (0.7, (0, 255, 0)),
                                         (1.0, (255, 255, 255))), view_dir=(-120.0, 10.0)),
+    # K1g stages only the coordinates a slice normal uses: axis-aligned planes,
+    # including planes through node coordinates (distances of exactly 0)
+    "q_slice_y_on_nodes": Pipeline(surfaces=(Surface("iso", "Q", 0.5), Surface("slice", value=0.5, normal=(0, 1, 0))),
+                                   color_field="temperature"),
+    "q_slices_x_z": Pipeline(surfaces=(Surface("iso", "Q", 0.5), Surface("slice", value=0.25, normal=(1, 0, 0)),
+                                       Surface("slice", value=0.5, normal=(0, 0, 1))),
+                             color_field="Q", view_dir=(20.0, 60.0)),
+    "q_slice_face": Pipeline(surfaces=(Surface("iso", "temperature", 0.6),
+                                       Surface("slice", value=0.0, normal=(0, -1, 0))),
+                             color_field="vorticity:mag"),
     "four_surfaces": Pipeline(surfaces=(Surface("iso", "Q", -0.5), Surface("iso", "Q", 0.5),
                                         Surface("iso", "temperature", 0.2),
                                         Surface("slice", value=0.7, normal=(1, 1, 1))),
