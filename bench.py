@@ -140,15 +140,15 @@ def _pipeline(case, width):
 
 def _bytes_read_per_point(case, cached: bool = False, plane: bool | int = True) -> int:
     """Algorithmic HBM bytes the fused kernel reads per GLL point: every field
-    component once (f64), the coordinates unless the geometry cache replaces
-    them (with the cache, `plane` = how many of x,y,z the slice planes stage:
-    True = all three, an int = the count K1g stages), and the 9 cached
+    component once (f64), the coordinates (`plane` True: all three unless the
+    geometry cache replaces them; an int: the count of x,y,z the slice normals
+    use, which is what K1g and K1s load), and the 9 cached
     Jacobian-inverse entries (72 B) when the cache is used."""
     b = 8 * sum(v.shape[0] for v in case.fields.values())
-    if not cached:
+    if plane is not True and plane is not False:
+        b += 8 * int(plane)
+    elif not cached or plane:
         b += 24
-    elif plane:
-        b += 24 if plane is True else 8 * int(plane)
     if cached:
         b += 72
     return b
@@ -218,8 +218,8 @@ def run_ours(a):
         an.execute(da, fetch_image=False)
     cached = bool(r.geometry_cached)
     plane = any(s.kind == "slice" for s in pipe.surfaces)
-    if plane and cached and r.surface_pass == 2:
-        # K1g stages only the coordinates with a nonzero normal component
+    if (plane and cached and r.surface_pass == 2) or r.surface_pass == 1:
+        # K1g and K1s load only the coordinates with a nonzero normal component
         plane = sum(any(s.normal[c] != 0.0 for s in pipe.surfaces if s.kind == "slice") for c in range(3))
     bpp = _bytes_read_per_point(case, cached, plane)
 

@@ -60,7 +60,7 @@ struct WarpScratch {
 };
 
 struct StreamFlags {
-  int xyz;      // coordinates needed per node (a slice plane)
+  int xyz;      // coordinates needed per node: bit c = some slice normal has a nonzero component c
   int umag;     // |u| needed per node
   int nsc;      // scalar fields loaded per node
 };
@@ -111,11 +111,12 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const FusedParams 
     for (int k = 0; k < 8; ++k) {
       const long long gi = g0 + 64 * k + 2 * lane;
       double2 X = make_double2(0.0, 0.0), Y = X, Z = X, U = X, V = X, W = X, S[kMaxScalars];
-      if (fl.xyz) {
-        X = ld2(p.x + gi);
-        Y = ld2(p.y + gi);
-        Z = ld2(p.z + gi);
-      }
+      // an unloaded coordinate enters the distance as 0: its term is 0*x, which
+      // can only flip the sign of a zero distance, and +-0 compare the same
+      // against the iso value (emission recomputes distances from x,y,z)
+      if (fl.xyz & 1) X = ld2(p.x + gi);
+      if (fl.xyz & 2) Y = ld2(p.y + gi);
+      if (fl.xyz & 4) Z = ld2(p.z + gi);
       if (fl.umag) {
         U = ld2(p.vel[0] + gi);
         V = ld2(p.vel[1] + gi);
@@ -316,7 +317,9 @@ static bool aligned16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
 
 static StreamFlags stream_flags(const FusedParams& p) {
   StreamFlags fl{0, p.need_umag ? 1 : 0, p.n_scalars};
-  for (int i = 0; i < p.n_surf; ++i) fl.xyz |= p.surf_src[i] >= SRC_PLANE;
+  for (int i = 0; i < p.n_surf; ++i)
+    if (p.surf_src[i] >= SRC_PLANE)
+      for (int c = 0; c < 3; ++c) fl.xyz |= (p.surf_n[i][c] != 0.0 ? 1 : 0) << c;
   return fl;
 }
 

@@ -85,6 +85,10 @@ BOX_PIPES = {
     "q_slice_face": Pipeline(surfaces=(Surface("iso", "temperature", 0.6),
                                        Surface("slice", value=0.0, normal=(0, -1, 0))),
                              color_field="vorticity:mag"),
+    # the same for K1s (no gradient): |u| iso + a slice through node coordinates
+    "umag_slice_y_on_nodes": Pipeline(surfaces=(Surface("iso", "velocity:mag", 0.6),
+                                                Surface("slice", value=0.5, normal=(0, 1, 0))),
+                                      color_field="velocity:mag"),
     "four_surfaces": Pipeline(surfaces=(Surface("iso", "Q", -0.5), Surface("iso", "Q", 0.5),
                                         Surface("iso", "temperature", 0.2),
                                         Surface("slice", value=0.7, normal=(1, 1, 1))),
