@@ -153,7 +153,10 @@ int nkb_mesh_set(nkb_ctx* ctx, int64_t n_elements, int order,
  * values are bit-identical to recomputing them.  Calling nkb_mesh_set again
  * with the same pointers, sizes and offsets keeps the cache (static mesh);
  * after editing coordinates in place (moving mesh) call nkb_mesh_modified.
- * nkb_set_geometry_cache(ctx, 0) disables it (default on; env NKB_GEOM_CACHE=0). */
+ * nkb_set_geometry_cache(ctx, 0) disables it; 1 (default) keeps it in the
+ * compact layout when every element is extruded (x, y independent of t, z of
+ * r and s: 2 KB per element instead of 36 KB) and the full one otherwise; 2
+ * forces the full layout.  Env NKB_GEOM_CACHE=0 / full sets the default. */
 /* Global GLL node ids (NekRS mesh->globalIds), DEVICE int64[E*(N+1)^3],
  * read during the call: builds the gather-scatter of nkb_dssum.  Collective
  * when a communicator is initialised (finds the ids shared with other ranks).
@@ -173,6 +176,14 @@ int nkb_dssum(nkb_ctx* ctx, double* field, void* stream);
 int nkb_transit_gather(nkb_ctx* ctx, int root, void* stream);
 int nkb_mesh_modified(nkb_ctx* ctx);
 int nkb_set_geometry_cache(nkb_ctx* ctx, int enable);
+/* Geometry-cache introspection: *layout = NKB_GEO_NONE (not built / off),
+ * NKB_GEO_FULL (9 doubles per GLL point) or NKB_GEO_COMPACT (every element
+ * extruded: 4 x 64 in-plane entries + 8 axial entries per element);
+ * *bytes = device bytes the cache holds (either pointer may be NULL). */
+#define NKB_GEO_NONE    0
+#define NKB_GEO_FULL    1
+#define NKB_GEO_COMPACT 2
+int nkb_geometry_info(nkb_ctx* ctx, int* layout, int64_t* bytes);
 /* register (or re-point) a device-resident point field, borrowed.
  * replaces: FieldArray(name, POINT, comps, values) (data_model.py:27-55) */
 int nkb_field_set(nkb_ctx* ctx, const char* name, int ncomp,
@@ -249,6 +260,13 @@ int nkb_triangles_device(nkb_ctx* ctx, const float** tri, const uint64_t** meta,
 
 /* ---- sort-last composite over NCCL (assemble_global analogue,
  *      data_model.py:188-225 / transport.py:358-376) -------------------- */
+/* In-process sort-last composite of n <= 8 partition contexts on ONE device
+ * (e.g. R element ranges of one mesh, each executed with the same pipeline
+ * and composite = 0): runs the P2P composite kernel (min over the partitions'
+ * key buffers, global colour range, colormap resolve) once per band of rows,
+ * exactly as n ranks would over NVLink, into root's image.  root may be one
+ * of the partitions.  Lets a one-GPU box check R16's kernel bit for bit. */
+int nkb_composite_partitions(nkb_ctx* root, nkb_ctx* const* parts, int n, const nkb_pipeline* p, void* stream);
 int nkb_nccl_unique_id(unsigned char id_out[128]);
 int nkb_comm_init(nkb_ctx* ctx, const unsigned char id[128], int nranks, int rank);
 int nkb_comm_destroy(nkb_ctx* ctx);

@@ -120,6 +120,8 @@ _SIGS = {
     "nkb_set_velocity_name": ([_vp, C.c_char_p], C.c_int),
     "nkb_mesh_modified": ([_vp], C.c_int),
     "nkb_set_geometry_cache": ([_vp, C.c_int], C.c_int),
+    "nkb_geometry_info": ([_vp, _vp, _vp], C.c_int),
+    "nkb_composite_partitions": ([_vp, _vp, C.c_int, _vp, _vp], C.c_int),
     "nkb_execute": ([_vp, C.POINTER(NkbPipeline), C.POINTER(NkbReport), _vp], C.c_int),
     "nkb_image_device": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
     "nkb_image_copy": ([_vp, _vp, _vp, _vp], C.c_int),

@@ -34,7 +34,7 @@ log = logging.getLogger(__name__)
 _ATTRS_BY_KIND: dict[str, frozenset[str]] = {
     "render": frozenset({"dir", "width", "height", "field", "vmin", "vmax"}),
     "insitu": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
-                         "velocity", "composite", "continuous", "projection", "fov"}),
+                         "velocity", "composite", "continuous", "projection", "fov", "async_write"}),
     "transit": frozenset({"dir", "width", "height", "field", "vmin", "vmax", "iso", "slice", "view",
                           "velocity", "endpoint", "projection", "fov"}),
     "stats": frozenset({"path"}),

@@ -74,6 +74,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
         run([cc, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-cudart", "static"])
+    # FP64 peak probe (tools/fp64_probe.cu): the bench's FP64 roofline denominator
+    probe_src = os.path.join(ROOT, "tools", "fp64_probe.cu")
+    probe = os.path.join(LIBDIR, "libnkbprobe.so")
+    if os.path.exists(probe_src) and (force or _stale(probe, [probe_src])):
+        run([cc, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", probe_src, "-o", probe,
+             "-cudart", "static"])
     # the plain-C usage example (examples/insitu_c_api.c), linked against the library
     ex_src = os.path.join(ROOT, "examples", "insitu_c_api.c")
     ex_bin = os.path.join(LIBDIR, "insitu_c_api")

@@ -66,6 +66,7 @@ class Context:
     # -- lifetime --------------------------------------------------------------
     def close(self) -> None:
         if self.handle:
+            self._wait_ppm_readers()            # an async PPM write may still read pinned memory
             N.lib().nkb_ctx_destroy(self.handle)
             self.handle = None
 
@@ -99,8 +100,19 @@ class Context:
         """Coordinates were edited in place (moving mesh): drop the geometry cache."""
         N.call("nkb_mesh_modified", self.handle)
 
-    def set_geometry_cache(self, enable: bool) -> None:
-        N.call("nkb_set_geometry_cache", self.handle, int(bool(enable)))
+    def set_geometry_cache(self, enable: bool | str) -> None:
+        """True / "auto": cache (compact layout when every element is extruded);
+        "full": cache in the full 72 B/point layout; False: recompute every step."""
+        mode = {"auto": 1, "full": 2}.get(enable, None) if isinstance(enable, str) else int(bool(enable))
+        if mode is None:
+            raise ValueError(f"geometry cache mode must be True, False, 'auto' or 'full', got {enable!r}")
+        N.call("nkb_set_geometry_cache", self.handle, mode)
+
+    def geometry_info(self) -> dict:
+        """{"layout": "none" | "full" | "compact", "bytes": device bytes of the cache}."""
+        lay, nb = C.c_int(0), C.c_int64(0)
+        N.call("nkb_geometry_info", self.handle, C.byref(lay), C.byref(nb))
+        return {"layout": ("none", "full", "compact")[lay.value], "bytes": int(nb.value)}
 
     def field_set(self, name: str, base, ncomp: int = 1, comp_stride: int = 0) -> None:
         N.call("nkb_field_set", self.handle, name.encode(), int(ncomp), device_ptr(base), int(comp_stride))
@@ -149,9 +161,22 @@ class Context:
                stream or None)
         return (rgba, dep) if depth else rgba
 
+    def hold_ppm(self, future) -> None:
+        """Register a pending reader of the pinned PPM buffer (an asynchronous
+        file write); image_ppm() and close() wait for it before the buffer is
+        overwritten or freed."""
+        self._ppm_readers = [f for f in getattr(self, "_ppm_readers", []) if not f.done()] + [future]
+
+    def _wait_ppm_readers(self) -> None:
+        readers, self._ppm_readers = getattr(self, "_ppm_readers", []), []
+        for f in readers:
+            f.exception()           # wait; the owning sink re-raises its own error
+
     def image_ppm(self, stream: int = 0) -> memoryview:
         """The last image as complete PPM bytes (header + RGB), packed on the
-        GPU into library-owned pinned memory; valid until the next call."""
+        GPU into library-owned pinned memory; valid until the next call (which
+        first waits for every registered reader of the previous bytes)."""
+        self._wait_ppm_readers()
         ptr, n = C.c_void_p(), C.c_int64()
         N.call("nkb_image_ppm", self.handle, C.byref(ptr), C.byref(n), stream or None)
         return memoryview((C.c_ubyte * n.value).from_address(ptr.value)).cast("B")
@@ -166,6 +191,12 @@ class Context:
         out = (C.c_double * 3)()
         N.call("nkb_stats", self.handle, arr, len(segments), int(bool(collective)), out, stream or None)
         return float(out[0]), float(out[1]), float(out[2])
+
+    def composite_partitions(self, parts, pipeline: N.NkbPipeline, stream: int = 0) -> None:
+        """Depth-composite the key buffers of partition contexts on this
+        device into this context's image (nkb_composite_partitions)."""
+        arr = (C.c_void_p * len(parts))(*[c.handle for c in parts])
+        N.call("nkb_composite_partitions", self.handle, arr, len(parts), C.byref(pipeline), stream or None)
 
     def image_device(self) -> tuple[int, int, int]:
         a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()

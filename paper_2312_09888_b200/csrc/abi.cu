@@ -111,13 +111,13 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
   const size_t npx = (size_t)W * H;
   NKB_CUDA(cudaMalloc(&P.keys[0], (npx + 2) * sizeof(unsigned long long)));
   NKB_CUDA(cudaMalloc(&P.keys[1], (npx + 2) * sizeof(unsigned long long)));
-  NKB_CUDA(cudaMalloc(&P.flags, 3 * kMaxRanks * sizeof(unsigned long long)));
-  NKB_CUDA(cudaMemset(P.flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&P.flags, 4 * kMaxRanks * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMemset(P.flags, 0, 4 * kMaxRanks * sizeof(unsigned long long)));
   NKB_CUDA(cudaMalloc(&P.err, sizeof(int)));
   NKB_CUDA(cudaMemset(P.err, 0, sizeof(int)));
   NKB_CUDA(cudaMalloc(&P.dev_epoch, sizeof(unsigned long long)));
   NKB_CUDA(cudaMemset(P.dev_epoch, 0, sizeof(unsigned long long)));
-  NKB_CUDA(cudaMallocHost(&P.h_res, (1 + kMaxRanks) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMallocHost(&P.h_res, (2 + kMaxRanks) * sizeof(unsigned long long)));
   NKB_CUDA(cudaHostGetDevicePointer((void**)&P.h_res_dev, P.h_res, 0));
   constexpr int kH = 5;
   cudaIpcMemHandle_t mine[kH];
@@ -132,9 +132,9 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
   std::vector<cudaIpcMemHandle_t> all((size_t)kH * ctx->nranks);
   NKB_CUDA(cudaMemcpyAsync(all.data(), d_recv, hb * ctx->nranks, cudaMemcpyDeviceToHost, s));
   NKB_CUDA(cudaStreamSynchronize(s));
-  cudaFree(d_send);
   cudaFree(d_recv);
-  for (int q = 0; q < ctx->nranks; ++q) {
+  int ok = 1;
+  for (int q = 0; q < ctx->nranks && ok; ++q) {
     void* mapped[kH];
     for (int i = 0; i < kH; ++i) {
       if (q == ctx->rank) {
@@ -144,12 +144,12 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
       cudaError_t e = cudaIpcOpenMemHandle(&mapped[i], all[(size_t)q * kH + i], cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) {
         cudaGetLastError();
-        p2p_release(ctx);
-        P.unavailable = true;   // no peer mapping: the NCCL composite is used instead
-        return NKB_OK;
+        ok = 0;
+        break;
       }
       P.opened.push_back(mapped[i]);
     }
+    if (!ok) break;
     P.peer_keys[0][q] = (const unsigned long long*)mapped[0];
     P.peer_keys[1][q] = (const unsigned long long*)mapped[1];
     P.peer_flags[q] = (unsigned long long*)mapped[2];
@@ -157,6 +157,20 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
       P.root_rgba = (unsigned char*)mapped[3];
       P.root_depth = (float*)mapped[4];
     }
+  }
+  // every rank takes the same path: one rank that cannot map a peer (partial
+  // peer-access topology) sends all of them to the NCCL composite
+  int* d_ok = reinterpret_cast<int*>(d_send);
+  NKB_CUDA(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+  NKB_NCCL(g_nccl.AllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, ctx->comm, s));
+  int all_ok = 0;
+  NKB_CUDA(cudaMemcpyAsync(&all_ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  cudaFree(d_send);
+  if (!all_ok) {
+    p2p_release(ctx);           // closes the mappings this rank did open
+    P.unavailable = true;       // no peer mapping somewhere: the NCCL composite is used instead
+    return NKB_OK;
   }
   P.W = W;
   P.H = H;
@@ -216,7 +230,7 @@ int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
   NKB_CUDA(cudaHostGetDevicePointer((void**)&c->h_counters_dev, c->h_counters, 0));
   NKB_CUDA(cudaMalloc(&c->region_count, kMaxRegions * sizeof(unsigned long long)));
   for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
-  if (const char* g = getenv("NKB_GEOM_CACHE")) c->geo_enabled = strcmp(g, "0") != 0;
+  if (const char* g = getenv("NKB_GEOM_CACHE")) c->geo_enabled = strcmp(g, "0") == 0 ? 0 : (strcmp(g, "full") == 0 ? 2 : 1);
   *out = c;
   return NKB_OK;
 }
@@ -240,6 +254,7 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->depth);
   cudaFree(ctx->range_dev);
   cudaFree(ctx->geo);
+  cudaFree(ctx->geo_flag);
   cudaFree(ctx->prof);
   for (auto& kv : ctx->stats_cache)
     if (kv.second) stats_tables_free(*kv.second);
@@ -327,45 +342,81 @@ int nkb_mesh_modified(nkb_ctx* ctx) {
   return NKB_OK;
 }
 
+static void geo_release(nkb_ctx* ctx) {
+  cudaFree(ctx->geo);
+  ctx->geo = nullptr;
+  ctx->geo_bytes = 0;
+  ctx->geo_layout = NKB_GEO_NONE;
+  ctx->geo_valid = false;
+}
+
 int nkb_set_geometry_cache(nkb_ctx* ctx, int enable) {
   NKB_TRY(ctx_check(ctx));
-  ctx->geo_enabled = enable != 0;
-  if (!ctx->geo_enabled) {
-    cudaFree(ctx->geo);                    // give the 72 B/point back
-    ctx->geo = nullptr;
-    ctx->geo_cap = 0;
-    ctx->geo_valid = false;
-  }
+  if (enable < 0 || enable > 2) return fail(NKB_EINVAL, "geometry cache mode must be 0 (off), 1 (on) or 2 (full layout)");
+  if (enable != ctx->geo_enabled) geo_release(ctx);   // give the memory back / rebuild in the new layout
+  ctx->geo_enabled = enable;
+  return NKB_OK;
+}
+
+int nkb_geometry_info(nkb_ctx* ctx, int* layout, int64_t* bytes) {
+  NKB_TRY(ctx_check(ctx));
+  const bool built = ctx->geo_valid && ctx->geo != nullptr;
+  if (layout) *layout = built ? ctx->geo_layout : NKB_GEO_NONE;
+  if (bytes) *bytes = built ? ctx->geo_bytes : 0;
   return NKB_OK;
 }
 
 // Attach the geometry cache to a gradient step, building it first when the
-// mesh changed.  On allocation failure the step runs uncached (the other
-// GPU kernel variant -- same results), never on the CPU.
+// mesh changed: the compact layout when every element is extruded (one host
+// read of the build's flag, once per mesh), else the full layout.  On
+// allocation failure the step runs uncached (the other GPU kernel variant --
+// same results), never on the CPU.
 }  // extern "C"
 
 int nkb::geo_attach(nkb_ctx* ctx, FusedParams& fp, cudaStream_t s) {
   fp.geo = nullptr;
+  fp.geo_compact = 0;
   if (!fp.need_grad || !ctx->geo_enabled || ctx->E <= 0) return NKB_OK;
-  const int64_t npts = ctx->E * kNN;
-  if (ctx->geo_cap < npts) {
-    cudaFree(ctx->geo);
-    ctx->geo = nullptr;
-    ctx->geo_cap = 0;
-    ctx->geo_valid = false;
-    if (cudaMalloc(&ctx->geo, (size_t)npts * 9 * sizeof(double)) != cudaSuccess) {
-      cudaGetLastError();
-      ctx->geo = nullptr;
-      return NKB_OK;
-    }
-    ctx->geo_cap = npts;
-  }
   if (!ctx->geo_valid) {
-    NKB_TRY(launch_geometry(ctx->x, ctx->y, ctx->z, ctx->E, ctx->geo, s));
+    geo_release(ctx);
+    const int64_t E = ctx->E;
+    if (ctx->geo_enabled == 1) {
+      if (!ctx->geo_flag) NKB_CUDA(cudaMalloc(&ctx->geo_flag, sizeof(unsigned long long)));
+      double* c = nullptr;
+      const size_t cb = (size_t)E * kGeoCompactDoubles * sizeof(double);
+      if (cudaMalloc(&c, cb) == cudaSuccess) {
+        NKB_CUDA(cudaMemsetAsync(ctx->geo_flag, 0, sizeof(unsigned long long), s));
+        NKB_TRY(launch_geometry(ctx->x, ctx->y, ctx->z, E, nullptr, c, ctx->geo_flag, s));
+        unsigned long long n_general = 0;
+        NKB_CUDA(cudaMemcpyAsync(&n_general, ctx->geo_flag, sizeof(n_general), cudaMemcpyDeviceToHost, s));
+        NKB_CUDA(cudaStreamSynchronize(s));
+        if (n_general == 0) {
+          ctx->geo = c;
+          ctx->geo_bytes = (int64_t)cb;
+          ctx->geo_layout = NKB_GEO_COMPACT;
+        } else {
+          cudaFree(c);
+        }
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (!ctx->geo) {
+      const size_t fb = (size_t)E * kNN * 9 * sizeof(double);
+      if (cudaMalloc(&ctx->geo, fb) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->geo = nullptr;
+        return NKB_OK;
+      }
+      NKB_TRY(launch_geometry(ctx->x, ctx->y, ctx->z, E, ctx->geo, nullptr, nullptr, s));
+      ctx->geo_bytes = (int64_t)fb;
+      ctx->geo_layout = NKB_GEO_FULL;
+    }
     ctx->geo_valid = true;
     ctx->geo_built = true;
   }
   fp.geo = ctx->geo;
+  fp.geo_compact = ctx->geo_layout == NKB_GEO_COMPACT ? 1 : 0;
   ctx->geo_used = true;
   return NKB_OK;
 }
@@ -760,6 +811,7 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     pp.range_out = ctx->range_dev;
     pp.err = P.err;
     pp.dev_epoch = P.dev_epoch;
+    pp.overflow = ctx->counters + 6;
     zbuf = P.keys[ep & 1];
     NKB_TRY(launch_p2p_epoch(pp, s));                // device epoch := ep
     // every peer has finished reading this key buffer (epoch ep-2) before it is cleared
@@ -783,7 +835,8 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   rp.height = p->height;
   rp.zbuf = zbuf;
   NKB_TRY(launch_raster(rp, s));
-  NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, s));
+  NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, rp.region_count == ctx->counters ? nullptr : rp.region_count,
+                             rp.n_regions, rp.region_cap, ctx->tri_cap, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[2], s));
   if (p2p) {
     // fused sort-last composite + resolve over NVLink peer memory
@@ -798,6 +851,8 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     NKB_NCCL(g_nccl.GroupStart());
     NKB_NCCL(g_nccl.Reduce(ctx->zbuf, ctx->zbuf, (size_t)npx + 2, ncclUint64, ncclMin, 0, ctx->comm, s));
     NKB_NCCL(g_nccl.AllReduce(ctx->counters, ctx->counters + 3, 1, ncclUint64, ncclSum, ctx->comm, s));
+    // any rank overflowed -> every rank re-runs (counters[7])
+    NKB_NCCL(g_nccl.AllReduce(ctx->counters + 6, ctx->counters + 7, 1, ncclUint64, ncclMax, ctx->comm, s));
     NKB_NCCL(g_nccl.GroupEnd());
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[3], s));
@@ -826,6 +881,8 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   rep.h_counters = ctx->h_counters_dev;
   rep.err = p2p ? ctx->p2p.err : nullptr;
   rep.peer_counts = p2p ? ctx->p2p.flags + 2 * kMaxRanks : nullptr;
+  rep.peer_overflow = p2p ? ctx->p2p.flags + 3 * kMaxRanks : nullptr;
+  rep.nranks = ctx->nranks;
   rep.h_res = p2p ? ctx->p2p.h_res_dev : nullptr;
   NKB_TRY(launch_report(rep, s));
   return NKB_OK;
@@ -897,8 +954,10 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   }
   NKB_CUDA(cudaStreamSynchronize(s));
   if (p2p) {
-    if (*reinterpret_cast<const int*>(ctx->p2p.h_res))
+    if (*reinterpret_cast<const int*>(ctx->p2p.h_res)) {
+      cudaMemset(ctx->p2p.err, 0, sizeof(int));   // report once; a later step starts clean
       return fail(NKB_ENCCL, "P2P composite: timed out waiting for a peer rank");
+    }
     unsigned long long tot = 0;
     for (int q = 0; q < ctx->nranks; ++q) tot += ctx->p2p.h_res[1 + q];
     ctx->h_counters[3] = tot;   // meaningful on rank 0 (every rank reports to every rank)
@@ -1065,11 +1124,22 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     }
     fp.prof = nullptr;
   }
+  // Overflow: the step's triangles did not fit (counted, not written).  The
+  // decision is collective -- every rank sees whether ANY rank overflowed
+  // (P2P flags / NCCL max) -- so all ranks grow (those that overflowed) and
+  // re-run together, and the composite is redone from complete triangle sets.
   int reran = 0;
   int64_t ntri = (int64_t)ctx->h_counters[0];
-  const int64_t need = needed_capacity(ctx, ordered);
-  if (need > ctx->tri_cap) {  // grow and re-run once (deterministic result)
-    NKB_TRY(ensure_tri(ctx, need + need / 4 + 1024 * ctx->n_regions, p->emit_meta));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool own_over = ctx->h_counters[6] != 0;
+    bool any_over = own_over;
+    if (composite) any_over = ctx->p2p.ready ? ctx->p2p.h_res[1 + kMaxRanks] != 0 : ctx->h_counters[7] != 0;
+    if (!any_over) break;
+    if (own_over) {
+      const int64_t need = needed_capacity(ctx, ordered);
+      NKB_TRY(ensure_tri(ctx, std::max(need + need / 4 + 1024 * ctx->n_regions, ctx->tri_cap + ctx->tri_cap / 4),
+                         p->emit_meta));
+    }
     NKB_TRY(run_step(ctx, p, fp, cm, s, composite, ordered));
     ntri = (int64_t)ctx->h_counters[0];
     reran = 1;
@@ -1107,6 +1177,72 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
       cudaEventElapsedTime(&out->ms_resolve, ctx->ev[3], ctx->ev[4]);
     }
   }
+  return NKB_OK;
+}
+
+int nkb_composite_partitions(nkb_ctx* root, nkb_ctx* const* parts, int n, const nkb_pipeline* p, void* stream) {
+  NKB_TRY(ctx_check(root));
+  if (!p || !parts) return fail(NKB_EINVAL, "null pipeline or partition list");
+  if (n < 1 || n > kMaxRanks) return fail(NKB_EINVAL, "partition count must be in [1, 8]");
+  const int W = p->width, H = p->height;
+  for (int q = 0; q < n; ++q) {
+    if (!parts[q] || parts[q]->device != root->device)
+      return fail(NKB_EINVAL, "every partition context must live on the root's device");
+    if (!parts[q]->zbuf || parts[q]->W != W || parts[q]->H != H)
+      return fail(NKB_ESTATE, "partition " + std::to_string(q) + " has no key buffer of this image size "
+                              "(execute it with the same pipeline and composite = 0 first)");
+  }
+  Colormap cm;
+  NKB_TRY(build_colormap(p, cm));
+  NKB_TRY(ensure_image(root, W, H));
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int q = 0; q < n; ++q)            // the partitions' steps ran on their own streams
+    if (parts[q] != root) NKB_CUDA(cudaDeviceSynchronize());
+  // the flag protocol is satisfied up front: every "keys ready" word at epoch 1
+  unsigned long long* flags = nullptr;
+  int* err = nullptr;
+  NKB_CUDA(cudaMalloc(&flags, (4 * kMaxRanks + 1) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&err, sizeof(int)));
+  std::vector<unsigned long long> h(4 * kMaxRanks + 1, 0ULL);
+  for (int q = 0; q < n; ++q) h[q] = 1ULL;
+  h[4 * kMaxRanks] = 1ULL;               // the device epoch
+  NKB_CUDA(cudaMemcpyAsync(flags, h.data(), h.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  NKB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+  P2PParams pp;
+  memset(&pp, 0, sizeof(pp));
+  pp.nranks = n;
+  pp.flags = flags;
+  for (int q = 0; q < n; ++q) {
+    pp.peer_flags[q] = flags;
+    pp.peer_keys[q] = parts[q]->zbuf;
+  }
+  pp.npx = (long long)W * H;
+  pp.width = W;
+  pp.height = H;
+  pp.vmin = p->vmin;
+  pp.vmax = p->vmax;
+  pp.cmap = cm;
+  memcpy(pp.bg, p->background, 4);
+  pp.root_rgba = root->rgba;
+  pp.root_depth = root->depth;
+  pp.range_out = root->range_dev;
+  pp.err = err;
+  pp.dev_epoch = flags + 4 * kMaxRanks;
+  int rc = NKB_OK;
+  for (int r = 0; r < n && rc == NKB_OK; ++r) {   // each "rank" resolves its band of rows
+    pp.rank = r;
+    rc = launch_p2p_composite(pp, s);
+  }
+  int h_err = 0;
+  if (rc == NKB_OK) {
+    cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) rc = fail(NKB_ECUDA, cudaGetErrorString(cudaGetLastError()));
+  }
+  cudaFree(flags);
+  cudaFree(err);
+  NKB_TRY(rc);
+  if (h_err) return fail(NKB_ECUDA, "partition composite: flag wait failed");
+  root->image_valid = true;
   return NKB_OK;
 }
 

@@ -70,6 +70,7 @@ __global__ void signal_kernel(P2PParams p, int which, const unsigned long long* 
   const int q = threadIdx.x;
   if (q < p.nranks) {
     if (count) p.peer_flags[q][2 * kMaxRanks + p.rank] = *count;
+    if (which == 0) p.peer_flags[q][3 * kMaxRanks + p.rank] = *p.overflow;
     __threadfence_system();
     st_release_sys(p.peer_flags[q] + which * kMaxRanks + p.rank, epoch);
   }

@@ -127,11 +127,15 @@ struct nkb_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   cudaEvent_t ev[9] = {};                   // stage events; 6-8: P2P composite detail (timing)
-  // geometry cache: 9 SoA arrays of d(r,s,t)/d(x,y,z) (fused.cu geometry_kernel)
-  bool geo_enabled = true;
+  // geometry cache of d(r,s,t)/d(x,y,z) (fused.cu geometry_kernel): compact
+  // (all elements extruded, kGeoCompact doubles per element) or full (9 SoA
+  // arrays of 512 doubles per element)
+  int geo_enabled = 1;                       // 0 off, 1 compact when possible, 2 full layout only
   bool geo_valid = false;
   double* geo = nullptr;
-  int64_t geo_cap = 0;                       // points
+  int geo_layout = 0;                        // NKB_GEO_NONE / FULL / COMPACT
+  int64_t geo_bytes = 0;
+  unsigned long long* geo_flag = nullptr;    // device counter of non-extruded elements (build only)
   bool geo_used = false;                     // last step used it
   bool geo_built = false;                    // last step (re)built it
   unsigned long long* prof = nullptr;        // debug phase profile (NKB_PROFILE_PHASES=1)

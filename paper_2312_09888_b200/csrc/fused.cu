@@ -133,7 +133,13 @@ constexpr int kMaxTriPerElem = kNC * NKB_MC_MAX_TRI * NKB_MAX_SURFACES;   // 686
 
 // even-odd 8-point derivatives of three staged fields along one pencil
 // (oracle deriv8): e_m = v_m + v_{7-m}, o_m = v_m - v_{7-m},
-// out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 DFMAs
+// out[i] = E_i + O_i, out[7-i] = O_i - E_i; each coefficient feeds 3 DFMAs.
+// kGeo (coordinate pencils, oracle deriv8_geo): a pencil whose 8 values all
+// compare equal (every o_m == 0 and e_0 == e_1 == e_2 == e_3) has derivative
+// exactly +0 -- the derivative of a constant -- instead of the rounding
+// residue of D applied to it.  Extruded elements then have exact zeros in
+// their Jacobian, which jinv's block branch and the compact cache rely on.
+template <bool kGeo = false>
 __device__ __forceinline__ void pencil3(const double* s0, const double* s1, const double* s2, double* d0,
                                         double* d1, double* d2, const int* off) {
   double e0[4], e1[4], e2[4], o0[4], o1[4], o2[4];
@@ -148,6 +154,15 @@ __device__ __forceinline__ void pencil3(const double* s0, const double* s1, cons
     o1[m] = __dsub_rn(a1, b1);
     e2[m] = __dadd_rn(a2, b2);
     o2[m] = __dsub_rn(a2, b2);
+  }
+  bool c0 = false, c1 = false, c2 = false;
+  if (kGeo) {
+    c0 = o0[0] == 0.0 && o0[1] == 0.0 && o0[2] == 0.0 && o0[3] == 0.0 && e0[0] == e0[1] && e0[0] == e0[2] &&
+         e0[0] == e0[3];
+    c1 = o1[0] == 0.0 && o1[1] == 0.0 && o1[2] == 0.0 && o1[3] == 0.0 && e1[0] == e1[1] && e1[0] == e1[2] &&
+         e1[0] == e1[3];
+    c2 = o2[0] == 0.0 && o2[1] == 0.0 && o2[2] == 0.0 && o2[3] == 0.0 && e2[0] == e2[1] && e2[0] == e2[2] &&
+         e2[0] == e2[3];
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -164,12 +179,12 @@ __device__ __forceinline__ void pencil3(const double* s0, const double* s1, cons
       O1 = __fma_rn(ao, o1[m], O1);
       O2 = __fma_rn(ao, o2[m], O2);
     }
-    d0[off[i]] = __dadd_rn(E0, O0);
-    d1[off[i]] = __dadd_rn(E1, O1);
-    d2[off[i]] = __dadd_rn(E2, O2);
-    d0[off[kNP - 1 - i]] = __dsub_rn(O0, E0);
-    d1[off[kNP - 1 - i]] = __dsub_rn(O1, E1);
-    d2[off[kNP - 1 - i]] = __dsub_rn(O2, E2);
+    d0[off[i]] = c0 ? 0.0 : __dadd_rn(E0, O0);
+    d1[off[i]] = c1 ? 0.0 : __dadd_rn(E1, O1);
+    d2[off[i]] = c2 ? 0.0 : __dadd_rn(E2, O2);
+    d0[off[kNP - 1 - i]] = c0 ? 0.0 : __dsub_rn(O0, E0);
+    d1[off[kNP - 1 - i]] = c1 ? 0.0 : __dsub_rn(O1, E1);
+    d2[off[kNP - 1 - i]] = c2 ? 0.0 : __dsub_rn(O2, E2);
   }
 }
 
@@ -187,11 +202,30 @@ __device__ __forceinline__ void pencil_offsets(int dir, int pa, int pb, int* off
 }
 
 // Jacobian inverse d(r,s,t)/d(x,y,z) from the 9 reference derivatives
-// G = (xr,xs,xt, yr,ys,yt, zr,zs,zt): cofactors, det, 1/det (oracle order)
+// G = (xr,xs,xt, yr,ys,yt, zr,zs,zt): cofactors, det, 1/det (oracle order).
+// J[3d + b] = d r_d / d x_b.  When xt = yt = zr = zs = 0 exactly (an element
+// extruded along t: x, y independent of t and z of r, s -- the coordinate
+// pencils of kGeo give exact zeros there), the Jacobian is block diagonal and
+// its inverse is taken blockwise (oracle jinv, same branch): the 2x2 block
+// [[ys, -xs], [-yr, xr]] / (xr ys - xs yr) and 1/zt, +0 elsewhere.  Its
+// entries then depend on (i, j) and on k only, which the compact cache uses.
 __device__ __forceinline__ void jinv(const double* G, double* J) {
   const double xr = G[0], xs = G[1], xt = G[2];
   const double yr = G[3], ys = G[4], yt = G[5];
   const double zr = G[6], zs = G[7], zt = G[8];
+  if (xt == 0.0 && yt == 0.0 && zr == 0.0 && zs == 0.0) {
+    const double r2 = __drcp_rn(__fma_rn(xr, ys, -__dmul_rn(xs, yr)));
+    J[0] = __dmul_rn(ys, r2);
+    J[1] = __dmul_rn(-xs, r2);
+    J[2] = 0.0;
+    J[3] = __dmul_rn(-yr, r2);
+    J[4] = __dmul_rn(xr, r2);
+    J[5] = 0.0;
+    J[6] = 0.0;
+    J[7] = 0.0;
+    J[8] = __drcp_rn(zt);
+    return;
+  }
   J[0] = __fma_rn(ys, zt, -__dmul_rn(yt, zs));
   J[1] = __fma_rn(xt, zs, -__dmul_rn(xs, zt));
   J[2] = __fma_rn(xs, yt, -__dmul_rn(xt, ys));
@@ -205,6 +239,24 @@ __device__ __forceinline__ void jinv(const double* G, double* J) {
   const double rdet = __drcp_rn(det);           // == 1.0/det, correctly rounded
 #pragma unroll
   for (int c = 0; c < 9; ++c) J[c] = __dmul_rn(J[c], rdet);
+}
+
+// compact geometry cache (every element extruded): per element
+// kGeoCompactDoubles = 264 doubles, J0, J1, J3, J4 by in-plane node
+// ij = i + 8j (4 x 64), then J8 by k (8).  The zeros are the +0 of jinv's
+// block branch; the node phase keeps the general 27-FMA chain rule over all
+// nine entries, so results are the full layout's bit for bit.
+__device__ __forceinline__ void geo_compact_node(const double* g, int n, double* J) {
+  const int ij = n & 63, k = n >> 6;
+  J[0] = g[ij];
+  J[1] = g[64 + ij];
+  J[2] = 0.0;
+  J[3] = g[128 + ij];
+  J[4] = g[192 + ij];
+  J[5] = 0.0;
+  J[6] = 0.0;
+  J[7] = 0.0;
+  J[8] = g[256 + k];
 }
 
 struct McScratch {
@@ -474,10 +526,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
   if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
   if (n_it > 0) prefetch(blockIdx.x, 0);
   __shared__ unsigned long long s_geo_bar;
-  constexpr unsigned kGeoBytes = 9u * kNN * sizeof(double);
+  // geometry block per element: full (36 KB) or compact (2112 B)
+  const long long geo_stride = p.geo_compact ? kGeoCompactDoubles : 9 * kNN;
+  const unsigned geo_bytes = (unsigned)(geo_stride * sizeof(double));
   if (kCached && tid == 0) {
     mbar_init(&s_geo_bar, 1);
-    if (n_it > 0) bulk_load(S_geo, p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes, &s_geo_bar);
+    if (n_it > 0) bulk_load(S_geo, p.geo + (long long)blockIdx.x * geo_stride, geo_bytes, &s_geo_bar);
   }
   cp_async_commit();
   int cls_any = 0;                                     // my sub-hex of the last element emits triangles
@@ -526,11 +580,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
           pencil3(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
         }
       } else {
-        // g = 0: x,y,z   1: u,v,w
+        // g = 0: x,y,z (constant-pencil rule)   1: u,v,w
         const int sf = (g == 0) ? slot_xyz : slot_vel;
-        pencil3(S_in + (sf + 0) * kArr, S_in + (sf + 1) * kArr, S_in + (sf + 2) * kArr,
-                S_d + (3 * (3 * g + 0) + dir) * kArr, S_d + (3 * (3 * g + 1) + dir) * kArr,
-                S_d + (3 * (3 * g + 2) + dir) * kArr, off);
+        if (g == 0)
+          pencil3<true>(S_in + (sf + 0) * kArr, S_in + (sf + 1) * kArr, S_in + (sf + 2) * kArr,
+                        S_d + (3 * (3 * g + 0) + dir) * kArr, S_d + (3 * (3 * g + 1) + dir) * kArr,
+                        S_d + (3 * (3 * g + 2) + dir) * kArr, off);
+        else
+          pencil3(S_in + (sf + 0) * kArr, S_in + (sf + 1) * kArr, S_in + (sf + 2) * kArr,
+                  S_d + (3 * (3 * g + 0) + dir) * kArr, S_d + (3 * (3 * g + 1) + dir) * kArr,
+                  S_d + (3 * (3 * g + 2) + dir) * kArr, off);
       }
     }
     if (it == n_it) break;
@@ -549,7 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
       double vq = 0.0, vw = 0.0, vu = 0.0;
       if (p.need_grad) {
         double J[9];
-        if (kCached) {
+        if (kCached && p.geo_compact) {
+          geo_compact_node(S_geo, n, J);
+        } else if (kCached) {
 #pragma unroll
           for (int c = 0; c < 9; ++c) J[c] = S_geo[c * kArr + n];
         } else {
@@ -628,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
     __syncthreads();                                   // case bits of element `it` ready
     tick(4);
     if (kCached && tid == 0 && it + 1 < n_it)          // S_geo consumed: fetch element it+1
-      bulk_load(S_geo, p.geo + (e + G) * 9 * kNN, kGeoBytes, &s_geo_bar);
+      bulk_load(S_geo, p.geo + (e + G) * geo_stride, geo_bytes, &s_geo_bar);
     if (p.n_surf == 0) continue;
     if ((s_bor & ~s_band) == 0) continue;               // no surface crosses this element
 
@@ -779,13 +840,19 @@ int launch_compact(const float4* tri, const unsigned long long* meta, const unsi
 }
 
 // ---- per-mesh geometry cache: d(r,s,t)/d(x,y,z) at every GLL node ----
-// Same pencil3/jinv code as the uncached fused kernel, so the cached values
-// are bit-identical to what the fused kernel would recompute each step.
-// Layout: per element 9 arrays of 512 doubles (component c of node n of
-// element e at geo[(9e + c) * 512 + n]) so one element is one 36 KB block.
+// Same pencil3<true>/jinv code as the uncached fused kernel, so the cached
+// values are bit-identical to what the fused kernel would recompute each step.
+// Full layout (`full`): per element 9 arrays of 512 doubles (component c of
+// node n of element e at geo[(9e + c) * 512 + n]), one 36 KB block per
+// element.  Compact layout (`compact`, kGeoCompactDoubles doubles per element): the
+// element's J0, J1, J3, J4 on the k = 0 plane and J8 along k; an element
+// whose values do not have that structure (not extruded, so jinv took the
+// general branch somewhere, or an entry varies where it must not) adds 1 to
+// *n_general -- the host then builds the full layout instead.
 __global__ void __launch_bounds__(kNN) geometry_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                                       const double* __restrict__ z, long long E, double* geo) {
-  __shared__ double S[12 * kArr];                  // x,y,z + 9 derivatives (48 KB)
+                                                       const double* __restrict__ z, long long E, double* full,
+                                                       double* compact, unsigned long long* n_general) {
+  __shared__ double S[12 * kArr];                  // x,y,z + 9 derivatives (48 KB); then J (node order)
   const int tid = threadIdx.x;
   const int q = sw_node(tid);
   for (long long e = blockIdx.x; e < E; e += gridDim.x) {
@@ -799,23 +866,44 @@ __global__ void __launch_bounds__(kNN) geometry_kernel(const double* __restrict_
       int off[kNP];
       pencil_offsets(dir, tid & 7, (tid >> 3) & 7, off);
       double* D = S + 3 * kArr;
-      pencil3(S, S + kArr, S + 2 * kArr, D + dir * kArr, D + (3 + dir) * kArr, D + (6 + dir) * kArr, off);
+      pencil3<true>(S, S + kArr, S + 2 * kArr, D + dir * kArr, D + (3 + dir) * kArr, D + (6 + dir) * kArr, off);
     }
     __syncthreads();
     double G9[9], J[9];
 #pragma unroll
     for (int c = 0; c < 9; ++c) G9[c] = S[(3 + c) * kArr + q];
     jinv(G9, J);
+    if (full) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) geo[(e * 9 + c) * kNN + tid] = J[c];
+      for (int c = 0; c < 9; ++c) full[(e * 9 + c) * kNN + tid] = J[c];
+    }
+    if (compact) {
+      __syncthreads();                             // S is reused for J in node order
+      const int cs[5] = {0, 1, 3, 4, 8};
+#pragma unroll
+      for (int u = 0; u < 5; ++u) S[u * kArr + tid] = J[cs[u]];
+      __syncthreads();
+      const int ij = tid & 63, k = tid >> 6;
+      const auto bits = [](double v) { return __double_as_longlong(v); };
+      bool ok = bits(J[2]) == 0 && bits(J[5]) == 0 && bits(J[6]) == 0 && bits(J[7]) == 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ok = ok && bits(S[u * kArr + ij]) == bits(J[cs[u]]);
+      ok = ok && bits(S[4 * kArr + 64 * k]) == bits(J[8]);
+      const int all_ok = __syncthreads_and(ok);
+      double* dst = compact + e * kGeoCompactDoubles;
+      if (tid < 256) dst[tid] = S[(tid >> 6) * kArr + (tid & 63)];
+      else if (tid < 264) dst[tid] = S[4 * kArr + 64 * (tid - 256)];
+      if (tid == 0 && !all_ok) atomicAdd(n_general, 1ULL);
+    }
     __syncthreads();
   }
 }
 
-int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* geo, cudaStream_t s) {
+int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* full, double* compact,
+                    unsigned long long* n_general, cudaStream_t s) {
   if (E <= 0) return NKB_OK;
   const long long grid = E < 148LL * 64 ? E : 148LL * 64;
-  geometry_kernel<<<(unsigned)grid, kNN, 0, s>>>(x, y, z, (long long)E, geo);
+  geometry_kernel<<<(unsigned)grid, kNN, 0, s>>>(x, y, z, (long long)E, full, compact, n_general);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
@@ -857,13 +945,17 @@ __device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
 }
 
+// kCompact: the compact geometry cache (2112 B per element) is staged with
+// the fields into shared memory; otherwise J^-1 is read from the full cache.
+template <bool kCompact>
 __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const FusedParams p, int nin, int slot_sc,
                                                                      int slot_vel, int slot_xyz, int plane_slots) {
   extern __shared__ __align__(16) double smem[];
   double* S_ring = smem;                               // 2 * nin * 512
   double* S_dv = S_ring + 2 * nin * kArr;              // 9 * 512 u,v,w derivatives
   double* S_q = S_dv + 9 * kArr;                       // Q, |w| (swizzled)
-  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_q + 2 * kArr);   // 512 case bits, node order
+  double* S_gc = S_q + 2 * kArr;                       // kCompact: 2 x kGeoCompactDoubles
+  unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_gc + (kCompact ? 2 * kGeoCompactDoubles : 0));
   __shared__ G2Scratch mc;
   __shared__ double s_mn[kG2Threads / 32], s_mx[kG2Threads / 32];
 
@@ -897,10 +989,19 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
         for (int h = 0; h < 8; ++h) cp_async8(d + qs[h], src + 64 * h);
       }
     }
+    if (kCompact) {                                    // the element's compact J^-1 block
+      const double* src = p.geo + e * kGeoCompactDoubles;
+      double* d = S_gc + b * kGeoCompactDoubles;
+#pragma unroll
+      for (int h = 0; h < 5; ++h) {
+        const int i = (tid & 63) + 64 * h;
+        if (i < kGeoCompactDoubles) cp_async8(d + i, src + i);
+      }
+    }
   };
   if (n_it > 0) {
     if (tid >= 192) prefetch(blockIdx.x, 0);
-    if (tid == 0) l2_prefetch(p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes);
+    if (!kCompact && tid == 0) l2_prefetch(p.geo + (long long)blockIdx.x * 9 * kNN, kGeoBytes);
   }
   cp_async_commit();
 
@@ -925,15 +1026,17 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     __syncthreads();                                   // element `it` staged; iteration it-1 finished
     if (it + 1 < n_it) {
       if (tid >= 192) prefetch(e + G, b ^ 1);
-      if (tid == 0) l2_prefetch(p.geo + (e + G) * 9 * kNN, kGeoBytes);
+      if (!kCompact && tid == 0) l2_prefetch(p.geo + (e + G) * 9 * kNN, kGeoBytes);
     }
     cp_async_commit();
     const double* S_in = S_ring + b * nin * kArr;
 
     // J^-1 of my first node: loads in flight across the pencil phase
     double J0[9];
+    if (!kCompact) {
 #pragma unroll
-    for (int c = 0; c < 9; ++c) J0[c] = __ldg(p.geo + (e * 9 + c) * kNN + tid);
+      for (int c = 0; c < 9; ++c) J0[c] = __ldg(p.geo + (e * 9 + c) * kNN + tid);
+    }
 
     // ---- u,v,w pencils: thread = (dir, pencil), 3 fields share offsets ----
     if (tid < 192) {
@@ -951,8 +1054,12 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       const int n = tid + kG2Threads * h;
       const int q = h ? q1 : q0;
       double J[9];
+      if (kCompact) {
+        geo_compact_node(S_gc + b * kGeoCompactDoubles, n, J);
+      } else {
 #pragma unroll
-      for (int c = 0; c < 9; ++c) J[c] = h ? __ldg(p.geo + (e * 9 + c) * kNN + n) : J0[c];
+        for (int c = 0; c < 9; ++c) J[c] = h ? __ldg(p.geo + (e * 9 + c) * kNN + n) : J0[c];
+      }
       double U[9];
 #pragma unroll
       for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
@@ -1187,7 +1294,10 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
   }
 }
 
-static size_t fused2_smem_bytes(int nin) { return (size_t)(2 * nin + 11) * kArr * sizeof(double) + kNN; }
+static size_t fused2_smem_bytes(int nin, bool compact) {
+  return (size_t)(2 * nin + 11) * kArr * sizeof(double) + (compact ? 2 * kGeoCompactDoubles * sizeof(double) : 0) +
+         kNN;
+}
 
 // coordinates the slice planes use: bit c set when some plane's normal has a
 // nonzero component c (K1g stages only those; emission reads x,y,z via L2)
@@ -1205,7 +1315,8 @@ static bool fused2_on(const FusedParams& p) {
   if (!(p.geo != nullptr && p.need_grad) || p.prof != nullptr) return false;
   const unsigned m = plane_axes(p);
   const int nin = (int)((m & 1) + ((m >> 1) & 1) + (m >> 2)) + (p.need_vel ? 3 : 0) + p.n_scalars;
-  return nin <= kG2MaxIn;
+  // two CTAs per SM: (2 nin + 11) x 4 KB (+ 4 KB of compact geometry) each
+  return nin <= (p.geo_compact ? kG2MaxIn - 1 : kG2MaxIn);
 }
 
 static size_t fused_smem_bytes(int nin) {
@@ -1222,8 +1333,10 @@ int launch_fused_prepare() {
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_TRY(launch_stream_prepare());
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)fused2_smem_bytes(kG2MaxIn)));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused2_smem_bytes(kG2MaxIn, false)));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused2_smem_bytes(kG2MaxIn, true)));
   int dev = 0;
   NKB_CUDA(cudaGetDevice(&dev));
   NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1306,8 +1419,13 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     }
     const int slot2_sc = k2;
     for (int c = 0; c < p.n_scalars; ++c) q2.in_ptr[k2++] = p.scalar[c];
-    fused2_kernel<<<(unsigned)fused_grid_for(p, p.n_elements), kG2Threads, fused2_smem_bytes(k2), s>>>(
-        q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps);
+    const unsigned g2 = (unsigned)fused_grid_for(p, p.n_elements);
+    if (p.geo_compact)
+      fused2_kernel<true><<<g2, kG2Threads, fused2_smem_bytes(k2, true), s>>>(q2, k2, slot2_sc, slot2_vel,
+                                                                             slot2_xyz, ps);
+    else
+      fused2_kernel<false><<<g2, kG2Threads, fused2_smem_bytes(k2, false), s>>>(q2, k2, slot2_sc, slot2_vel,
+                                                                               slot2_xyz, ps);
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
   }

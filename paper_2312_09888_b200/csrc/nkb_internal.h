@@ -93,7 +93,8 @@ struct FusedParams {
   int* elem_count;                  // [n_elements] (COUNT mode)
   const long long* elem_offset;     // [n_elements] exclusive scan (ORDERED mode)
   unsigned long long* counters;     // [0] total triangles, [1] enc(min colour), [2] enc(max colour)
-  const double* geo;                // optional geometry cache d(r,s,t)/d(x,y,z): [E][9][512]
+  const double* geo;                // optional geometry cache d(r,s,t)/d(x,y,z): [E][9][512] (full)
+  int geo_compact;                  // 1: geo is the compact layout [E][kGeoCompactDoubles]
   unsigned long long* prof;         // debug: [role 3][phase 6] cycle sums (NKB_PROFILE_PHASES=1)
 };
 enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
@@ -119,7 +120,8 @@ struct Colormap {
 constexpr int kMaxRanks = 8;
 struct P2PParams {
   int rank, nranks;
-  unsigned long long* flags;                          // local [3*kMaxRanks]: ready | done | tri count
+  unsigned long long* flags;                          // local [4*kMaxRanks]: ready | done | tri count | overflow
+  const unsigned long long* overflow;                 // local counters[6]: this step overflowed
   unsigned long long* peer_flags[kMaxRanks];          // every rank's flags (IPC-mapped)
   const unsigned long long* peer_keys[kMaxRanks];     // every rank's key buffer of this epoch
   long long npx;
@@ -149,7 +151,10 @@ struct ReportParams {
   unsigned long long* h_counters;           // host words [0..3] counters, [4..5] range bits, [8..] regions
   const int* err;                           // P2P: timeout flag, or null
   const unsigned long long* peer_counts;    // P2P: [kMaxRanks] per-rank triangle counts
-  unsigned long long* h_res;                // P2P host words [0] timeout, [1..] counts, or null
+  const unsigned long long* peer_overflow;  // P2P: [kMaxRanks] per-rank overflow words
+  int nranks;
+  unsigned long long* h_res;                // P2P host words [0] timeout, [1..kMaxRanks] counts,
+                                            // [1+kMaxRanks] any rank overflowed; or null
 };
 int launch_report(const ReportParams& p, cudaStream_t s);
 
@@ -178,14 +183,21 @@ int surface_pass_of(const FusedParams& p);     // 0 K1, 1 K1s (stream.cu), 2 K1g
 int fused_grid_for(const FusedParams& p, int64_t n_elements);   // triangle regions of that pass
 int launch_stream(const FusedParams& p, int grid, cudaStream_t s);
 int launch_stream_prepare();
-int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* geo, cudaStream_t s);
+// geometry cache build: full layout (9 x 512 doubles per element) and/or the
+// compact one (kGeoCompactDoubles per element; *n_general counts elements
+// that do not fit it)
+constexpr int kGeoCompactDoubles = 4 * 64 + 8;
+int launch_geometry(const double* x, const double* y, const double* z, int64_t E, double* full, double* compact,
+                    unsigned long long* n_general, cudaStream_t s);
 int launch_compact(const float4* tri, const unsigned long long* meta, const unsigned long long* region_count,
                    int n_regions, int64_t region_cap, float4* out_tri, unsigned long long* out_meta,
                    int64_t n_total, cudaStream_t s);
 int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long long* total, cudaStream_t s);
 int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
 int launch_raster(const RasterParams& p, cudaStream_t s);
-int launch_range_words(const unsigned long long* counters, unsigned long long* words, cudaStream_t s);
+int launch_range_words(unsigned long long* counters, unsigned long long* words,
+                       const unsigned long long* region_count, int n_regions, int64_t region_cap, int64_t tri_cap,
+                       cudaStream_t s);
 int launch_resolve(const ResolveParams& p, cudaStream_t s);
 // ---- stats.cu: numpy-exact min / max / mean ----
 constexpr long long kChunk = 32768;      // values per CTA subtree (<= 640 leaves of 57..128)

@@ -42,23 +42,49 @@ __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
   }
 }
 
-// counters [1]=enc(min) [2]=enc(max) -> composite words: enc(min), ~enc(max)
-__global__ void range_words_kernel(const unsigned long long* counters, unsigned long long* words) {
-  words[0] = counters[1];
-  words[1] = ~counters[2];
+// counters [1]=enc(min) [2]=enc(max) -> composite words: enc(min), ~enc(max);
+// counters[6] = 1 when the step's triangles overflowed the buffer (a CTA
+// region in FAST mode, the whole buffer in ordered mode).  Multi-rank steps
+// share this word (P2P flags / an NCCL max) so that every rank decides alike
+// whether the step must grow and re-run.
+__global__ void __launch_bounds__(256) range_words_kernel(unsigned long long* counters, unsigned long long* words,
+                                                          const unsigned long long* region_count, int n_regions,
+                                                          long long region_cap, long long tri_cap) {
+  __shared__ int s_over;
+  if (threadIdx.x == 0) {
+    words[0] = counters[1];
+    words[1] = ~counters[2];
+    s_over = 0;
+  }
+  __syncthreads();
+  int over = 0;
+  if (region_count) {
+    for (int r = threadIdx.x; r < n_regions; r += blockDim.x)
+      over |= region_count[r] > (unsigned long long)region_cap;
+  } else if (threadIdx.x == 0) {
+    over = counters[0] > (unsigned long long)tri_cap;
+  }
+  if (over) s_over = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) counters[6] = (unsigned long long)s_over;
 }
 
 // the step's report words straight into mapped pinned host memory: one
 // kernel instead of 3-5 small D2H copies at the tail of every step
 __global__ void __launch_bounds__(256) report_kernel(const ReportParams p) {
   const int t = threadIdx.x;
-  if (t < 4) p.h_counters[t] = p.counters[t];
+  if (t < 4 || t == 6 || t == 7) p.h_counters[t] = p.counters[t];
   if (t == 4 || t == 5) p.h_counters[t] = (unsigned long long)__double_as_longlong(p.range[t - 4]);
   if (p.region_count)
     for (int i = t; i < p.n_regions; i += blockDim.x) p.h_counters[8 + i] = p.region_count[i];
   if (p.h_res) {
     if (t == 0) p.h_res[0] = (unsigned long long)(unsigned)*p.err;
     if (t < kMaxRanks) p.h_res[1 + t] = *(volatile const unsigned long long*)(p.peer_counts + t);
+    if (t == 32) {      // any rank overflowed (its flag was written before its "keys ready" release)
+      unsigned long long any = 0;
+      for (int q = 0; q < p.nranks; ++q) any |= *(volatile const unsigned long long*)(p.peer_overflow + q);
+      p.h_res[1 + kMaxRanks] = any;
+    }
   }
 }
 
@@ -217,9 +243,11 @@ int launch_raster(const RasterParams& p, cudaStream_t s) {
   return NKB_OK;
 }
 
-int launch_range_words(const unsigned long long* counters, unsigned long long* words,
+int launch_range_words(unsigned long long* counters, unsigned long long* words,
+                       const unsigned long long* region_count, int n_regions, int64_t region_cap, int64_t tri_cap,
                        cudaStream_t s) {
-  range_words_kernel<<<1, 1, 0, s>>>(counters, words);
+  range_words_kernel<<<1, 256, 0, s>>>(counters, words, region_count, n_regions, (long long)region_cap,
+                                       (long long)tri_cap);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

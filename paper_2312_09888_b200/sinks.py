@@ -221,8 +221,10 @@ class InsituSink:
         self.async_write = params.get("async_write", "0").strip().lower() in ("1", "true", "yes", "on")
         self._writer = None
         self._pending = None
-        root = comm is None or comm.rank == 0
-        if root:
+        # who writes: the composite root, or -- composite="0" on several
+        # ranks -- every rank, its own partial image under a rank-suffixed name
+        self.per_rank = comm is not None and comm.size > 1 and not self.pipeline.composite
+        if comm is None or comm.rank == 0 or self.per_rank:
             self.dir.mkdir(parents=True, exist_ok=True)
             _probe_writable(self.dir)
 
@@ -240,13 +242,17 @@ class InsituSink:
         # header + RGB packed on the GPU into pinned memory: same bytes as
         # write_ppm(ImageRGB(w, h, rgba[..., :3].tobytes())) (sinks.py:298-303)
         ppm = ctx.image_ppm()
-        path = self.dir / f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}.ppm"
+        suffix = f"_rank{ctx.rank:04d}" if self.per_rank else ""
+        path = self.dir / f"step{s.step:06d}_{self.pipeline.color_field.replace(':', '_')}{suffix}.ppm"
         if self.async_write:
             if self._writer is None:
                 from concurrent.futures import ThreadPoolExecutor
 
                 self._writer = ThreadPoolExecutor(max_workers=1, thread_name_prefix="nkb-ppm")
+            # the write reads the context's pinned PPM buffer: every later
+            # image_ppm on this context (any sink) waits for it first
             self._pending = self._writer.submit(_write_bytes, path, ppm)
+            ctx.hold_ppm(self._pending)
         else:
             _write_bytes(path, ppm)
         return len(ppm)

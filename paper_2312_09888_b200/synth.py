@@ -26,10 +26,17 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .context import gll
-
 NP = 8
 NN = NP * NP * NP
+
+# GLL nodes of order N=7, bit for bit what nkb_gll(7) (csrc/gll.cpp) and the
+# oracle's orc_gll compute (tests/test_host.py checks all three agree).  They
+# are spelled out here so that generating a synthetic case maps no native
+# library: the bench's CPU reference arm builds the very same input bytes
+# without loading libnekb200.
+GLL7 = np.array([float.fromhex(h) for h in (
+    "-0x1.0000000000000p+0", "-0x1.be54b988eafaap-1", "-0x1.2ef3538095d15p-1", "-0x1.aca5117fc1960p-3",
+    "0x1.aca5117fc1960p-3", "0x1.2ef3538095d15p-1", "0x1.be54b988eafaap-1", "0x1.0000000000000p+0")])
 
 
 @dataclass
@@ -58,8 +65,7 @@ class SemCase:
 
 def _ref_coords(nel: tuple[int, int, int], e0: int, e1: int):
     """Logical coordinates in [0,1]^3 of every node of elements [e0, e1)."""
-    r, _ = gll(7)
-    t = (r + 1.0) / 2.0                         # GLL nodes on [0, 1]
+    t = (GLL7 + 1.0) / 2.0                         # GLL nodes on [0, 1]
     nx, ny, nz = nel
     e = np.arange(e0, e1)
     ex, ey, ez = e % nx, (e // nx) % ny, e // (nx * ny)
@@ -109,7 +115,7 @@ def taylor_green(e0: int = 0, e1: int | None = None, n: int = 8) -> SemCase:
     p = (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0) / 16.0
     return SemCase("c1", e1 - e0, e0, E, x, y, z,
                    {"velocity": np.stack([u, v, w]), "pressure": p[None]},
-                   {"iso": "Q=0.1", "field": "velocity:mag", "view": "35,30"}, nel=(n, n, n))
+                   dict(PARAMS["c1"]), nel=(n, n, n))
 
 
 def rbc_cylinder(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (32, 32, 32),
@@ -137,8 +143,7 @@ def rbc_cylinder(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] =
         vel.append(acc)
     return SemCase("c2", e1 - e0, e0, E, x, y, z,
                    {"velocity": np.stack(vel), "temperature": T[None]},
-                   {"iso": "temperature=0.5;Q=1.0", "slice": "y=0", "field": "temperature",
-                    "view": "-60,25"}, nel=tuple(nel))
+                   dict(PARAMS["c2"]), nel=tuple(nel))
 
 
 def turb_pipe(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (25, 25, 400),
@@ -161,7 +166,7 @@ def turb_pipe(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (2
         for c in range(3):
             vel[c] = vel[c] + amp[c] * damp * np.sin(arg + ph[c])
     return SemCase("c3", e1 - e0, e0, E, x, y, z, {"velocity": np.stack(vel)},
-                   {"iso": "Q=5.0", "field": "vorticity:mag", "view": "-70,20"}, nel=tuple(nel))
+                   dict(PARAMS["c3"]), nel=tuple(nel))
 
 
 def pebble_bed(e0: int = 0, e1: int | None = None, n: int = 128, n_spheres: int = 146, seed: int = 3) -> SemCase:
@@ -185,8 +190,7 @@ def pebble_bed(e0: int = 0, e1: int | None = None, n: int = 128, n_spheres: int 
         v = v - k * 3.0 * dx * dy / d5
         w = w - k * 3.0 * dx * dz / d5
     return SemCase("c4", e1 - e0, e0, E, x, y, z, {"velocity": np.stack([u, v, w])},
-                   {"iso": "velocity:mag=1.2", "slice": "z=0.5", "field": "velocity:mag", "view": "+z"},
-                   nel=(n, n, n))
+                   dict(PARAMS["c4"]), nel=(n, n, n))
 
 
 def box(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (4, 4, 4), seed: int = 0) -> SemCase:
@@ -209,18 +213,68 @@ def box(e0: int = 0, e1: int | None = None, nel: tuple[int, int, int] = (4, 4, 4
                     "view": "30,40"}, nel=tuple(nel))
 
 
+def c5_lattice(n_elements: int) -> tuple[int, int, int]:
+    """Element lattice of a C5 box: the most cubic (nx >= ny >= nz) power-of-two
+    split, e.g. 65,536 = 64 x 32 x 32, 2,097,152 = 128 x 128 x 128."""
+    if n_elements < 1 or n_elements & (n_elements - 1):
+        raise ValueError(f"C5 element counts are powers of two, got {n_elements}")
+    b = n_elements.bit_length() - 1
+    ex = [b // 3 + (1 if i < b % 3 else 0) for i in range(3)]
+    return (1 << ex[0], 1 << ex[1], 1 << ex[2])
+
+
+C5_ELEMENTS = (65536, 131072, 262144, 524288, 1048576, 2097152)
+
+
+def c5_box(e0: int = 0, e1: int | None = None, n_elements: int = 65536) -> SemCase:
+    """C5: weak-scaling box (BASELINE configs[4]).  Cubic affine elements of
+    edge pi/8 on the lattice `c5_lattice(E)`, periodic Taylor-Green velocity
+    (the C1 flow, its period spanning 16 elements); full pipeline: Q iso,
+    colour |u|."""
+    nel = c5_lattice(n_elements)
+    e1 = n_elements if e1 is None else e1
+    X, Y, Z = _ref_coords(nel, e0, e1)
+    h = math.pi / 8.0
+    x, y, z = (h * nel[0]) * X, (h * nel[1]) * Y, (h * nel[2]) * Z
+    u = np.sin(x) * np.cos(y) * np.cos(z)
+    v = -np.cos(x) * np.sin(y) * np.cos(z)
+    w = np.zeros_like(x)
+    return SemCase("c5", e1 - e0, e0, n_elements, x, y, z, {"velocity": np.stack([u, v, w])},
+                   dict(PARAMS["c5"]), nel=nel)
+
+
+# insitu sink attributes of every config (the generators return copies)
+PARAMS = {
+    "c1": {"iso": "Q=0.1", "field": "velocity:mag", "view": "35,30"},
+    "c2": {"iso": "temperature=0.5;Q=1.0", "slice": "y=0", "field": "temperature", "view": "-60,25"},
+    "c3": {"iso": "Q=5.0", "field": "vorticity:mag", "view": "-70,20"},
+    "c4": {"iso": "velocity:mag=1.2", "slice": "z=0.5", "field": "velocity:mag", "view": "+z"},
+    "c5": {"iso": "Q=0.1", "field": "velocity:mag", "view": "35,30"},
+}
+
 CONFIGS = {
     "c1": lambda e0=0, e1=None, scale=1: taylor_green(e0, e1),
     "c2": lambda e0=0, e1=None, scale=1: rbc_cylinder(e0, e1, nel=(32, 32, 32 * scale)),
     "c3": lambda e0=0, e1=None, scale=1: turb_pipe(e0, e1, nel=(25, 25, 400 * scale), length=20.0 * scale),
     "c4": lambda e0=0, e1=None, scale=1: pebble_bed(e0, e1),
+    # c5: `scale` is the element count of the box
+    "c5": lambda e0=0, e1=None, scale=65536: c5_box(e0, e1, n_elements=scale),
 }
-CONFIG_ELEMENTS = {"c1": 512, "c2": 32768, "c3": 250000, "c4": 1048576}
+CONFIG_ELEMENTS = {"c1": 512, "c2": 32768, "c3": 250000, "c4": 1048576, "c5": 65536}
+
+
+def global_elements(name: str, scale: int = 1) -> int:
+    """Elements of config `name` at `scale` (c2/c3: streamwise multiple; c5:
+    the element count itself; c1/c4: fixed)."""
+    if name == "c5":
+        return int(scale)
+    return CONFIG_ELEMENTS[name] * (scale if name in ("c2", "c3") else 1)
 
 
 def make_case(name: str, rank: int = 0, nranks: int = 1, scale: int = 1) -> SemCase:
     """Partition `rank` of config `name`; `scale` multiplies the element count
-    along the streamwise axis (weak scaling: scale = nranks)."""
-    E = CONFIG_ELEMENTS[name] * (scale if name in ("c2", "c3") else 1)
+    along the streamwise axis (weak scaling: scale = nranks), or is the box's
+    element count for c5."""
+    E = global_elements(name, scale)
     e0, e1 = partition(E, rank, nranks)
     return CONFIGS[name](e0, e1, scale)

@@ -14,7 +14,6 @@ import math
 import numpy as np
 
 from . import synth
-from .context import gll
 
 NN = 512
 
@@ -27,8 +26,7 @@ def _torch():
 
 def _ref_coords(nel, e0, e1, device):
     torch = _torch()
-    r, _ = gll(7)
-    t = torch.tensor((r + 1.0) / 2.0, dtype=torch.float64, device=device)
+    t = torch.tensor((synth.GLL7 + 1.0) / 2.0, dtype=torch.float64, device=device)
     nx, ny, nz = nel
     e = torch.arange(e0, e1, device=device, dtype=torch.int64)
     ex, ey, ez = e % nx, (e // nx) % ny, e // (nx * ny)
@@ -81,7 +79,7 @@ def rbc_cylinder(e0, e1, nel, device, seed=1):
         vel.append(acc)
     E = nel[0] * nel[1] * nel[2]
     return DeviceCase("c2", e1 - e0, e0, E, x, y, z, {"velocity": torch.stack(vel), "temperature": T[None]},
-                      {"iso": "temperature=0.5;Q=1.0", "slice": "y=0", "field": "temperature", "view": "-60,25"})
+                      dict(synth.PARAMS["c2"]))
 
 
 def turb_pipe(e0, e1, nel, length, device, seed=2):
@@ -102,7 +100,7 @@ def turb_pipe(e0, e1, nel, length, device, seed=2):
             vel[c] = vel[c] + amp[c] * damp * torch.sin(arg + ph[c])
     E = nel[0] * nel[1] * nel[2]
     return DeviceCase("c3", e1 - e0, e0, E, x, y, z, {"velocity": torch.stack(vel)},
-                      {"iso": "Q=5.0", "field": "vorticity:mag", "view": "-70,20"})
+                      dict(synth.PARAMS["c3"]))
 
 
 def pebble_bed(e0, e1, n, device, n_spheres=146, seed=3):
@@ -123,12 +121,25 @@ def pebble_bed(e0, e1, n, device, n_spheres=146, seed=3):
         v = v - k * 3.0 * dx * dy / d5
         w = w - k * 3.0 * dx * dz / d5
     return DeviceCase("c4", e1 - e0, e0, n ** 3, x, y, z, {"velocity": torch.stack([u, v, w])},
-                      {"iso": "velocity:mag=1.2", "slice": "z=0.5", "field": "velocity:mag", "view": "+z"})
+                      dict(synth.PARAMS["c4"]))
+
+
+def c5_box(e0, e1, n_elements, device):
+    torch = _torch()
+    nel = synth.c5_lattice(n_elements)
+    X, Y, Z = _ref_coords(nel, e0, e1, device)
+    h = math.pi / 8.0
+    x, y, z = (h * nel[0]) * X, (h * nel[1]) * Y, (h * nel[2]) * Z
+    u = torch.sin(x) * torch.cos(y) * torch.cos(z)
+    v = -torch.cos(x) * torch.sin(y) * torch.cos(z)
+    w = torch.zeros_like(x)
+    return DeviceCase("c5", e1 - e0, e0, n_elements, x, y, z, {"velocity": torch.stack([u, v, w])},
+                      dict(synth.PARAMS["c5"]))
 
 
 def make_case(name: str, rank: int = 0, nranks: int = 1, scale: int = 1, device="cuda"):
     """Device partition `rank` of config `name` (see synth.make_case)."""
-    E = synth.CONFIG_ELEMENTS[name] * (scale if name in ("c2", "c3") else 1)
+    E = synth.global_elements(name, scale)
     e0, e1 = synth.partition(E, rank, nranks)
     if name == "c2":
         return rbc_cylinder(e0, e1, (32, 32, 32 * scale), device)
@@ -136,6 +147,8 @@ def make_case(name: str, rank: int = 0, nranks: int = 1, scale: int = 1, device=
         return turb_pipe(e0, e1, (25, 25, 400 * scale), 20.0 * scale, device)
     if name == "c4":
         return pebble_bed(e0, e1, 128, device)
+    if name == "c5":
+        return c5_box(e0, e1, E, device)
     if name == "c1":
         return None
     raise KeyError(name)

@@ -32,11 +32,11 @@ def ctx():
     c.close()
 
 
-@pytest.fixture(params=["geo_cached", "geo_uncached"])
+@pytest.fixture(params=["geo_compact", "geo_full", "geo_uncached"])
 def ctx_geo(request, ctx):
-    """The session context with the per-mesh geometry cache on or off: both
-    fused-kernel variants must give bit-identical results."""
-    on = request.param == "geo_cached"
-    ctx.set_geometry_cache(on)
+    """The session context with the per-mesh geometry cache in its default
+    (compact when every element is extruded) or full layout, or off: every
+    fused-kernel variant must give bit-identical results."""
+    ctx.set_geometry_cache({"geo_compact": "auto", "geo_full": "full", "geo_uncached": False}[request.param])
     yield ctx
     ctx.set_geometry_cache(True)

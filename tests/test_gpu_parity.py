@@ -283,6 +283,30 @@ def test_moving_mesh_rebuilds_geometry_cache(ctx):
     _check_against_oracle(ctx, case, pipe, an.execute(da, depth=True))
 
 
+def test_geometry_cache_layouts(ctx):
+    """Extruded meshes (boxes, the curved C2-style cylinder) keep the compact
+    cache (264 doubles per element); a mesh whose z varies in-plane falls
+    back to the full 9 x 512 layout.  Compact, full and recomputed geometry
+    give the oracle's results bit for bit."""
+    pipe = Pipeline(surfaces=(Surface("iso", "Q", 0.5), Surface("slice", value=0.0, normal=(0, 1, 0))),
+                    color_field="vorticity:mag", emit_meta=True)
+    cyl = synth.rbc_cylinder(nel=(4, 4, 3))
+    twisted = synth.box(nel=(3, 2, 2))
+    twisted.z = twisted.z + 0.03 * np.cos(2.0 * twisted.x)          # z depends on (i, j): not extruded
+    for case, layout in ((synth.box(nel=(3, 3, 2)), "compact"), (cyl, "compact"), (twisted, "full")):
+        for mode, want in (("auto", layout), ("full", "full"), (False, "none")):
+            ctx.set_geometry_cache(mode)
+            da, res = _run(ctx, case, pipe)
+            info = ctx.geometry_info()
+            assert info["layout"] == want, (mode, info)
+            if want == "compact":
+                assert info["bytes"] == case.n_elements * 264 * 8
+            elif want == "full":
+                assert info["bytes"] == case.n_points * 72
+            _check_against_oracle(ctx, case, pipe, res)
+    ctx.set_geometry_cache(True)
+
+
 # ---------------------------------------------------------------- DataAdaptor
 
 
@@ -422,23 +446,30 @@ def test_gradient_pipelines_use_fused_pass(ctx):
     assert res.report.surface_pass == 2
 
 
+@pytest.mark.parametrize("geo", ["auto", "full"])
 @pytest.mark.parametrize("name", ["q_iso", "three_surfaces", "colour_wmag", "four_surfaces"])
-def test_two_cta_gradient_pass_matches_k1_and_oracle(ctx, name, monkeypatch):
+def test_two_cta_gradient_pass_matches_k1_and_oracle(ctx, name, geo, monkeypatch):
     """K1g (two 256-thread CTAs per SM) against K1 and the oracle: ordered
-    triangles and case words, fast-path multisets, images and ranges."""
+    triangles and case words, fast-path multisets, images and ranges; with
+    the compact (extruded box) and the full geometry cache.  K1g stages up to
+    7 inputs (6 with the compact cache); beyond that K1 runs."""
     case = synth.box(nel=(5, 4, 3))
-    ctx.set_geometry_cache(True)
+    ctx.set_geometry_cache(geo)
+    staged = {"q_iso": 4, "three_surfaces": 7, "colour_wmag": 3, "four_surfaces": 7}[name]
+    fits = staged <= (6 if geo == "auto" else 7)
     out = {}
     for mode in ("1", "0"):
         monkeypatch.setenv("NKB_FUSED2", mode)
         pipe = Pipeline(**{**BOX_PIPES[name].__dict__, "emit_meta": True})
         _, res = _run(ctx, case, pipe)
-        assert res.report.surface_pass == (2 if mode == "1" else 0)
+        assert res.report.surface_pass == (2 if (mode == "1" and fits) else 0)
+        assert ctx.geometry_info()["layout"] == ("compact" if geo == "auto" else "full")
         _check_against_oracle(ctx, case, pipe, res)
         _, fast = _run(ctx, case, BOX_PIPES[name])
         out[mode] = (_rows(ctx.triangles()), fast.rgba.copy(), fast.report.range)
     assert out["1"][0] == out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
+    ctx.set_geometry_cache(True)
 
 
 def test_large_triangles_raster_bit_exact(ctx):

@@ -57,6 +57,19 @@ def test_gll_through_abi_without_gpu():
     assert x[0] == -1.0 and x[-1] == 1.0 and D.shape == (8, 8)
 
 
+def test_synth_gll_constants_match_library_and_oracle():
+    # synth.py spells out the N=7 nodes so case generation maps no native
+    # library (the bench's reference arm); they must be the library's bits
+    from oracle import oracle as orc
+    from paper_2312_09888_b200 import synth
+    from paper_2312_09888_b200.context import gll
+
+    x, _ = gll(7)
+    xo, _ = orc.gll(7)
+    assert np.array_equal(synth.GLL7.view(np.uint64), x.view(np.uint64))
+    assert np.array_equal(synth.GLL7.view(np.uint64), xo.view(np.uint64))
+
+
 def test_pipeline_struct_layout_matches_header():
     # offsets the C compiler assigns must match ctypes (checked via a tiny C program)
     import subprocess
@@ -343,3 +356,31 @@ def test_perspective_view_maps_sphere_into_image():
     d = np.array([math.cos(math.radians(30)), math.sin(math.radians(30)), 0.0])
     assert abs(proj(c + r * d)[2]) < 1e-12 and abs(proj(c - r * d)[2] - 1.0) < 1e-12
     assert proj(c + [0, 0, 0.4])[1] < sy                       # higher z -> smaller row (up)
+
+
+def test_insitu_async_write_attribute_parses_and_reaches_the_sink(tmp_path):
+    """async_write is an insitu attribute: the bridge keeps
+    it and the sink built from the parsed params writes on a writer thread."""
+    from paper_2312_09888_b200.sinks import InsituSink
+
+    cfg = parse_config(f'<sensei><analysis type="insitu" frequency="1" iso="Q=1" async_write="1" '
+                       f'dir="{tmp_path}"/></sensei>')
+    s = cfg.specs[0]
+    assert s.params["async_write"] == "1"
+    assert InsituSink(s.params).async_write
+
+
+def test_insitu_sink_without_composite_writes_one_file_per_rank(tmp_path):
+    """composite="0" on several ranks: each rank writes its own partial image
+    under a rank-suffixed name (no clobbering), and probes the directory."""
+    from paper_2312_09888_b200.sinks import InsituSink
+
+    class _Comm:
+        def __init__(self, rank, size):
+            self.rank, self.size = rank, size
+
+    d = tmp_path / "parts"
+    s1 = InsituSink({"dir": str(d), "composite": "0", "iso": "Q=1"}, comm=_Comm(1, 2))
+    assert s1.per_rank and d.is_dir()
+    s0 = InsituSink({"dir": str(tmp_path / "one"), "iso": "Q=1"}, comm=_Comm(1, 2))
+    assert not s0.per_rank and not (tmp_path / "one").exists()      # composite: rank 0 writes
