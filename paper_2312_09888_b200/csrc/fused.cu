@@ -623,12 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const FusedParams p,
 #pragma unroll
         for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
         double A[9];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b)
-            A[3 * a + b] = __fma_rn(U[3 * a + 2], J[6 + b],
-                                    __fma_rn(U[3 * a + 1], J[3 + b], __dmul_rn(U[3 * a + 0], J[0 + b])));
+        chain_rule(U, J, A);
         const double off = __fma_rn(A[5], A[7], __fma_rn(A[2], A[6], __dmul_rn(A[1], A[3])));
         const double dia = __fma_rn(A[8], A[8], __fma_rn(A[4], A[4], __dmul_rn(A[0], A[0])));
         vq = -__fma_rn(0.5, dia, off);
@@ -947,7 +942,10 @@ __device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
 
 // kCompact: the compact geometry cache (2112 B per element) is staged with
 // the fields into shared memory; otherwise J^-1 is read from the full cache.
-template <bool kCompact>
+// kWmag: |vorticity| is used (surface, colour or export); kOut: some derived
+// array is exported (q_out / wmag_out / vort_out).  Both are compile-time so
+// the node phase carries no dead work for the common pipelines.
+template <bool kCompact, bool kWmag, bool kOut>
 __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const FusedParams p, int nin, int slot_sc,
                                                                      int slot_vel, int slot_xyz, int plane_slots) {
   extern __shared__ __align__(16) double smem[];
@@ -1064,12 +1062,8 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
 #pragma unroll
       for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
       double A[9];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 3; ++bb)
-          A[3 * a + bb] = __fma_rn(U[3 * a + 2], J[6 + bb],
-                                   __fma_rn(U[3 * a + 1], J[3 + bb], __dmul_rn(U[3 * a + 0], J[0 + bb])));
+      if (kCompact) chain_rule_block(U, J, A);           // every compact node is block diagonal
+      else chain_rule(U, J, A);
       const double offd = __fma_rn(A[5], A[7], __fma_rn(A[2], A[6], __dmul_rn(A[1], A[3])));
       const double dia = __fma_rn(A[8], A[8], __fma_rn(A[4], A[4], __dmul_rn(A[0], A[0])));
       const double vq = -__fma_rn(0.5, dia, offd);
@@ -1078,16 +1072,18 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       const double om2 = __dsub_rn(A[3], A[1]);
       double vw = 0.0, vu = 0.0;
       S_q[q] = vq;
-      if (p.need_wmag) {
+      if (kWmag) {
         vw = mag3(om0, om1, om2);
         S_q[kArr + q] = vw;
       }
-      if (p.q_out) p.q_out[g0 + n] = vq;
-      if (p.wmag_out) p.wmag_out[g0 + n] = vw;
-      if (p.vort_out) {
-        p.vort_out[3 * (g0 + n) + 0] = om0;
-        p.vort_out[3 * (g0 + n) + 1] = om1;
-        p.vort_out[3 * (g0 + n) + 2] = om2;
+      if (kOut) {
+        if (p.q_out) p.q_out[g0 + n] = vq;
+        if (p.wmag_out) p.wmag_out[g0 + n] = vw;
+        if (p.vort_out) {
+          p.vort_out[3 * (g0 + n) + 0] = om0;
+          p.vort_out[3 * (g0 + n) + 1] = om1;
+          p.vort_out[3 * (g0 + n) + 2] = om2;
+        }
       }
       if (p.need_umag)
         vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
@@ -1333,10 +1329,15 @@ int launch_fused_prepare() {
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_TRY(launch_stream_prepare());
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)fused2_smem_bytes(kG2MaxIn, false)));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)fused2_smem_bytes(kG2MaxIn, true)));
+  const int f2 = (int)fused2_smem_bytes(kG2MaxIn, false), f2c = (int)fused2_smem_bytes(kG2MaxIn, true);
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
+  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
   int dev = 0;
   NKB_CUDA(cudaGetDevice(&dev));
   NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1420,12 +1421,18 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     const int slot2_sc = k2;
     for (int c = 0; c < p.n_scalars; ++c) q2.in_ptr[k2++] = p.scalar[c];
     const unsigned g2 = (unsigned)fused_grid_for(p, p.n_elements);
-    if (p.geo_compact)
-      fused2_kernel<true><<<g2, kG2Threads, fused2_smem_bytes(k2, true), s>>>(q2, k2, slot2_sc, slot2_vel,
-                                                                             slot2_xyz, ps);
-    else
-      fused2_kernel<false><<<g2, kG2Threads, fused2_smem_bytes(k2, false), s>>>(q2, k2, slot2_sc, slot2_vel,
-                                                                               slot2_xyz, ps);
+    const bool compact = p.geo_compact != 0, wm = p.need_wmag != 0;
+    const bool out = p.q_out != nullptr || p.wmag_out != nullptr || p.vort_out != nullptr;
+    const size_t sh = fused2_smem_bytes(k2, compact);
+#define NKB_F2(C, W, O) fused2_kernel<C, W, O><<<g2, kG2Threads, sh, s>>>(q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps)
+    if (compact) {
+      if (wm) { if (out) NKB_F2(true, true, true); else NKB_F2(true, true, false); }
+      else { if (out) NKB_F2(true, false, true); else NKB_F2(true, false, false); }
+    } else {
+      if (wm) { if (out) NKB_F2(false, true, true); else NKB_F2(false, true, false); }
+      else { if (out) NKB_F2(false, false, true); else NKB_F2(false, false, false); }
+    }
+#undef NKB_F2
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
   }

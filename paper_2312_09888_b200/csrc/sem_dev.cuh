@@ -18,6 +18,35 @@ __device__ __forceinline__ double plane_dist(const double* n, double x, double y
   return __fma_rn(n[2], z, __fma_rn(n[1], y, __dmul_rn(n[0], x)));
 }
 
+// Velocity gradient A[3a + b] = sum_d U[3a + d] J[3d + b] (U[3a + d] =
+// du_a/dr_d, J = d(r,s,t)/d(x,y,z)), oracle chain_rule.  When J is block
+// diagonal -- J2 = J5 = J6 = J7 = +0 exactly, jinv's block branch and every
+// node of the compact cache -- the zero terms are skipped; otherwise the
+// 3-term fma chain in d order.
+__device__ __forceinline__ bool jinv_is_block(const double* J) {
+  return (__double_as_longlong(J[2]) | __double_as_longlong(J[5]) | __double_as_longlong(J[6]) |
+          __double_as_longlong(J[7])) == 0;
+}
+__device__ __forceinline__ void chain_rule_block(const double* U, const double* J, double* A) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    A[3 * a + 0] = __fma_rn(U[3 * a + 1], J[3], __dmul_rn(U[3 * a + 0], J[0]));
+    A[3 * a + 1] = __fma_rn(U[3 * a + 1], J[4], __dmul_rn(U[3 * a + 0], J[1]));
+    A[3 * a + 2] = __dmul_rn(U[3 * a + 2], J[8]);
+  }
+}
+__device__ __forceinline__ void chain_rule(const double* U, const double* J, double* A) {
+  if (jinv_is_block(J)) {
+    chain_rule_block(U, J, A);
+    return;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      A[3 * a + b] = __fma_rn(U[3 * a + 2], J[6 + b], __fma_rn(U[3 * a + 1], J[3 + b], __dmul_rn(U[3 * a + 0], J[0 + b])));
+}
+
 // VTK_HEXAHEDRON corner v -> lattice offset (matches NKB_MC_VERT_OFF_DATA)
 __device__ __forceinline__ int voff_i(int v) { return (v ^ (v >> 1)) & 1; }
 __device__ __forceinline__ int voff_j(int v) { return (v >> 1) & 1; }
