@@ -899,7 +899,7 @@ static std::string step_key(nkb_ctx* ctx, const nkb_pipeline* p, const FusedPara
   const void* ptrs[] = {ctx->tri, ctx->meta, ctx->zbuf, ctx->rgba, ctx->depth, ctx->counters, ctx->region_count,
                         ctx->elem_count, ctx->elem_offset, ctx->range_dev, ctx->h_counters};
   add(ptrs, sizeof(ptrs));
-  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0, surface_pass_of(fp)};
+  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0, surface_pass_of(fp), fused_node_prog(fp)};
   add(v, sizeof(v));
   return k;
 }

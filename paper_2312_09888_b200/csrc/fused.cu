@@ -904,6 +904,60 @@ int launch_geometry(const double* x, const double* y, const double* z, int64_t E
 }
 
 
+// ---- node programs: compile-time surface / colour sources of a pipeline ----
+// The node phase's per-surface source dispatch (Q, |w|, |u|, a staged scalar
+// or a plane distance, chosen per node from runtime codes) cost as many
+// instructions as the velocity gradient itself (ncu, C2).  A node program
+// fixes the source kind of every surface and of the colour at compile time;
+// only the scalar slots, iso values and plane normals stay runtime.  Program 0
+// is the generic runtime dispatch and runs every other pipeline.  The values
+// and their operation order are the generic path's, so results are identical.
+enum NodeKind : int { NK_NONE = 0, NK_Q, NK_W, NK_U, NK_SC, NK_PL };
+struct NodeProg {
+  int s[NKB_MAX_SURFACES];
+  int c;
+};
+__host__ __device__ constexpr NodeProg node_prog(int k) {
+  return k == 1   ? NodeProg{{NK_Q, NK_NONE, NK_NONE, NK_NONE}, NK_U}      // Q iso, colour |u|
+         : k == 2 ? NodeProg{{NK_Q, NK_NONE, NK_NONE, NK_NONE}, NK_W}      // Q iso, colour |w|
+         : k == 3 ? NodeProg{{NK_Q, NK_NONE, NK_NONE, NK_NONE}, NK_SC}     // Q iso, colour by a scalar
+         : k == 4 ? NodeProg{{NK_SC, NK_Q, NK_PL, NK_NONE}, NK_SC}         // scalar iso + Q iso + slice, colour scalar
+                  : NodeProg{{NK_NONE, NK_NONE, NK_NONE, NK_NONE}, NK_NONE};
+}
+constexpr int kNodeProgs = 5;
+__host__ __device__ constexpr bool prog_uses(int k, int kind) {
+  return node_prog(k).c == kind || node_prog(k).s[0] == kind || node_prog(k).s[1] == kind ||
+         node_prog(k).s[2] == kind || node_prog(k).s[3] == kind;
+}
+
+static int node_kind_of(int src) {
+  return src < 0             ? NK_NONE
+         : src >= SRC_PLANE  ? NK_PL
+         : src == SRC_Q      ? NK_Q
+         : src == SRC_WMAG   ? NK_W
+         : src == SRC_UMAG   ? NK_U
+                             : NK_SC;
+}
+
+// the node program that runs pipeline `p` in K1g (0 = generic)
+static int node_prog_of(const FusedParams& p) {
+  const char* v = getenv("NKB_NODE_PROGS");            // A/B: NKB_NODE_PROGS=0 forces the generic program
+  if (v && v[0] == '0') return 0;
+  if (p.q_out || p.wmag_out || p.vort_out) return 0;
+  for (int k = 1; k < kNodeProgs; ++k) {
+    const NodeProg P = node_prog(k);
+    bool ok = P.c == node_kind_of(p.color_src);
+    for (int s = 0; s < NKB_MAX_SURFACES; ++s)
+      ok = ok && P.s[s] == (s < p.n_surf ? node_kind_of(p.surf_src[s]) : NK_NONE);
+    // |w| / |u| computed exactly when the program uses them
+    ok = ok && (p.need_wmag != 0) == prog_uses(k, NK_W) && (p.need_umag != 0) == prog_uses(k, NK_U);
+    if (ok) return k;
+  }
+  return 0;
+}
+
+int fused_node_prog(const FusedParams& p) { return node_prog_of(p); }
+
 // ---- K1g: the cached-geometry gradient pass, two independent CTAs per SM ----
 // K1 runs one 512-thread CTA per SM whose phases (pencils | node | classify |
 // emit) are serialised by CTA-wide barriers; its phase profile shows the SM
@@ -945,7 +999,8 @@ __device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
 // kWmag: |vorticity| is used (surface, colour or export); kOut: some derived
 // array is exported (q_out / wmag_out / vort_out).  Both are compile-time so
 // the node phase carries no dead work for the common pipelines.
-template <bool kCompact, bool kWmag, bool kOut>
+// kProg: node program (0 = generic runtime dispatch).
+template <bool kCompact, bool kWmag, bool kOut, int kProg>
 __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const FusedParams p, int nin, int slot_sc,
                                                                      int slot_vel, int slot_xyz, int plane_slots) {
   extern __shared__ __align__(16) double smem[];
@@ -1012,6 +1067,13 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
   const int psx = (plane_slots & 0xff) == 0xff ? -1 : (plane_slots & 0xff);
   const int psy = ((plane_slots >> 8) & 0xff) == 0xff ? -1 : ((plane_slots >> 8) & 0xff);
   const int psz = ((plane_slots >> 16) & 0xff) == 0xff ? -1 : ((plane_slots >> 16) & 0xff);
+  constexpr NodeProg NP = node_prog(kProg);
+  // node programs: staged-array offset of each scalar surface and of a scalar colour
+  int sc_off[NKB_MAX_SURFACES], sc_off_c = 0;
+#pragma unroll
+  for (int s = 0; s < NKB_MAX_SURFACES; ++s)
+    sc_off[s] = (NP.s[s] == NK_SC) ? (slot_sc + p.surf_src[s] - SRC_SCALAR0) * kArr : 0;
+  if (NP.c == NK_SC) sc_off_c = (slot_sc + p.color_src - SRC_SCALAR0) * kArr;
 
   for (long long it = 0; it < n_it; ++it) {
     const long long e = blockIdx.x + it * G;
@@ -1085,35 +1147,61 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
           p.vort_out[3 * (g0 + n) + 2] = om2;
         }
       }
-      if (p.need_umag)
-        vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
       unsigned bits = 0;
+      if (kProg == 0) {                               // generic: runtime source dispatch
+        if (p.need_umag)
+          vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
 #pragma unroll
-      for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
-        if (s >= p.n_surf) break;
-        const int src = p.surf_src[s];
-        double val;
-        if (src >= SRC_PLANE)
-          val = plane_dist(p.surf_n[s], psx >= 0 ? S_in[psx * kArr + q] : 0.0,
-                           psy >= 0 ? S_in[psy * kArr + q] : 0.0, psz >= 0 ? S_in[psz * kArr + q] : 0.0);
-        else if (src == SRC_Q) val = vq;
-        else if (src == SRC_WMAG) val = vw;
-        else if (src == SRC_UMAG) val = vu;
-        else val = S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
-        bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+        for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
+          if (s >= p.n_surf) break;
+          const int src = p.surf_src[s];
+          double val;
+          if (src >= SRC_PLANE)
+            val = plane_dist(p.surf_n[s], psx >= 0 ? S_in[psx * kArr + q] : 0.0,
+                             psy >= 0 ? S_in[psy * kArr + q] : 0.0, psz >= 0 ? S_in[psz * kArr + q] : 0.0);
+          else if (src == SRC_Q) val = vq;
+          else if (src == SRC_WMAG) val = vw;
+          else if (src == SRC_UMAG) val = vu;
+          else val = S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+          bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+        }
+        if (p.color_src >= 0) {
+          const int src = p.color_src;
+          const double c = (src == SRC_Q)      ? vq
+                           : (src == SRC_WMAG) ? vw
+                           : (src == SRC_UMAG) ? vu
+                                               : S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
+          cmin = fmin(cmin, c);
+          cmax = fmax(cmax, c);
+        }
+      } else {                                        // node program: sources fixed at compile time
+        if (prog_uses(kProg, NK_U))
+          vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
+#pragma unroll
+        for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
+          if (NP.s[s] == NK_NONE) continue;
+          double val;
+          if (NP.s[s] == NK_PL)
+            val = plane_dist(p.surf_n[s], psx >= 0 ? S_in[psx * kArr + q] : 0.0,
+                             psy >= 0 ? S_in[psy * kArr + q] : 0.0, psz >= 0 ? S_in[psz * kArr + q] : 0.0);
+          else if (NP.s[s] == NK_Q) val = vq;
+          else if (NP.s[s] == NK_W) val = vw;
+          else if (NP.s[s] == NK_U) val = vu;
+          else val = S_in[sc_off[s] + q];
+          bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
+        }
+        if (NP.c != NK_NONE) {
+          const double c = (NP.c == NK_Q)   ? vq
+                           : (NP.c == NK_W) ? vw
+                           : (NP.c == NK_U) ? vu
+                                            : S_in[sc_off_c + q];
+          cmin = fmin(cmin, c);
+          cmax = fmax(cmax, c);
+        }
       }
       S_bits[n] = (unsigned char)bits;
       wand &= bits;
       wor |= bits;
-      if (p.color_src >= 0) {
-        const int src = p.color_src;
-        const double c = (src == SRC_Q)      ? vq
-                         : (src == SRC_WMAG) ? vw
-                         : (src == SRC_UMAG) ? vu
-                                             : S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
-        cmin = fmin(cmin, c);
-        cmax = fmax(cmax, c);
-      }
     }
     {
       const unsigned wa = __reduce_and_sync(0xffffffffu, wand), wo = __reduce_or_sync(0xffffffffu, wor);
@@ -1295,6 +1383,38 @@ static size_t fused2_smem_bytes(int nin, bool compact) {
          kNN;
 }
 
+// K1g instantiations: generic program x (|w|, exports) and the node programs
+using F2Kernel = void (*)(const FusedParams, int, int, int, int, int);
+template <bool C>
+static F2Kernel f2_kernel_c(int wo, int prog) {
+  switch (prog) {
+    case 1: return fused2_kernel<C, prog_uses(1, NK_W), false, 1>;
+    case 2: return fused2_kernel<C, prog_uses(2, NK_W), false, 2>;
+    case 3: return fused2_kernel<C, prog_uses(3, NK_W), false, 3>;
+    case 4: return fused2_kernel<C, prog_uses(4, NK_W), false, 4>;
+    default: break;
+  }
+  switch (wo) {
+    case 0: return fused2_kernel<C, false, false, 0>;
+    case 1: return fused2_kernel<C, false, true, 0>;
+    case 2: return fused2_kernel<C, true, false, 0>;
+    default: return fused2_kernel<C, true, true, 0>;
+  }
+}
+static F2Kernel f2_kernel(bool compact, int wo, int prog) {
+  return compact ? f2_kernel_c<true>(wo, prog) : f2_kernel_c<false>(wo, prog);
+}
+static int fused2_prepare() {
+  for (int c = 0; c < 2; ++c) {
+    const int bytes = (int)fused2_smem_bytes(kG2MaxIn, c == 1);
+    for (int wo = 0; wo < 4; ++wo)
+      NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, wo, 0), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    for (int k = 1; k < kNodeProgs; ++k)
+      NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, 0, k), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  }
+  return NKB_OK;
+}
+
 // coordinates the slice planes use: bit c set when some plane's normal has a
 // nonzero component c (K1g stages only those; emission reads x,y,z via L2)
 static unsigned plane_axes(const FusedParams& p) {
@@ -1329,15 +1449,7 @@ int launch_fused_prepare() {
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_CUDA(cudaFuncSetAttribute(fused_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   NKB_TRY(launch_stream_prepare());
-  const int f2 = (int)fused2_smem_bytes(kG2MaxIn, false), f2c = (int)fused2_smem_bytes(kG2MaxIn, true);
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
-  NKB_CUDA(cudaFuncSetAttribute(fused2_kernel<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2c));
+  NKB_TRY(fused2_prepare());
   int dev = 0;
   NKB_CUDA(cudaGetDevice(&dev));
   NKB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1421,18 +1533,13 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     const int slot2_sc = k2;
     for (int c = 0; c < p.n_scalars; ++c) q2.in_ptr[k2++] = p.scalar[c];
     const unsigned g2 = (unsigned)fused_grid_for(p, p.n_elements);
-    const bool compact = p.geo_compact != 0, wm = p.need_wmag != 0;
-    const bool out = p.q_out != nullptr || p.wmag_out != nullptr || p.vort_out != nullptr;
+    const bool compact = p.geo_compact != 0;
+    const int prog = node_prog_of(p);
+    const int wm = p.need_wmag != 0 ? 1 : 0;
+    const int out = (p.q_out != nullptr || p.wmag_out != nullptr || p.vort_out != nullptr) ? 1 : 0;
     const size_t sh = fused2_smem_bytes(k2, compact);
-#define NKB_F2(C, W, O) fused2_kernel<C, W, O><<<g2, kG2Threads, sh, s>>>(q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps)
-    if (compact) {
-      if (wm) { if (out) NKB_F2(true, true, true); else NKB_F2(true, true, false); }
-      else { if (out) NKB_F2(true, false, true); else NKB_F2(true, false, false); }
-    } else {
-      if (wm) { if (out) NKB_F2(false, true, true); else NKB_F2(false, true, false); }
-      else { if (out) NKB_F2(false, false, true); else NKB_F2(false, false, false); }
-    }
-#undef NKB_F2
+    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog);
+    k<<<g2, kG2Threads, sh, s>>>(q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps);
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
   }

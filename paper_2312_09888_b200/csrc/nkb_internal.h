@@ -179,6 +179,7 @@ int launch_fused_prepare();
 // K1s (stream.cu): pipelines without a velocity gradient (no exports, fields
 // 16-byte aligned); launch_fused dispatches to it when surface_pass_of == 1
 bool stream_eligible(const FusedParams& p);
+int fused_node_prog(const FusedParams& p);   // K1g node program (graph key)
 int surface_pass_of(const FusedParams& p);     // 0 K1, 1 K1s (stream.cu), 2 K1g (two CTAs per SM)
 int fused_grid_for(const FusedParams& p, int64_t n_elements);   // triangle regions of that pass
 int launch_stream(const FusedParams& p, int grid, cudaStream_t s);

@@ -93,6 +93,14 @@ BOX_PIPES = {
                                         Surface("iso", "temperature", 0.2),
                                         Surface("slice", value=0.7, normal=(1, 1, 1))),
                               color_field="Q", width=300, height=200),
+    # the shapes K1g runs as compile-time node programs (fused.cu node_prog):
+    # C2 (scalar iso + Q iso + slice, colour scalar), C3 (Q iso, colour |w|),
+    # C1/C5 (Q iso, colour |u|); q_iso above is program 3
+    "prog_c2": Pipeline(surfaces=(Surface("iso", "temperature", 0.6), Surface("iso", "Q", 0.5),
+                                  Surface("slice", value=0.75, normal=(0, 1, 0))), color_field="temperature",
+                        view_dir=(-60.0, 25.0)),
+    "prog_c3": Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="vorticity:mag"),
+    "prog_c1": Pipeline(surfaces=(Surface("iso", "Q", 0.5),), color_field="velocity:mag", view_dir=(35.0, 30.0)),
 }
 
 
@@ -483,3 +491,22 @@ def test_large_triangles_raster_bit_exact(ctx):
     tri = ctx.triangles()
     assert len(tri) > 0
     _check_against_oracle(ctx, case, pipe, res)
+
+
+@pytest.mark.parametrize("name", ["prog_c2", "prog_c3", "prog_c1", "q_iso"])
+def test_node_programs_equal_generic_dispatch(ctx, name, monkeypatch):
+    """Compile-time node programs (K1g) against the generic runtime dispatch
+    (NKB_NODE_PROGS=0): identical ordered triangles, case words and images."""
+    case = synth.rbc_cylinder(nel=(4, 4, 4))
+    ctx.set_geometry_cache(True)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("NKB_NODE_PROGS", mode)
+        pipe = Pipeline(**{**BOX_PIPES[name].__dict__, "emit_meta": True})
+        _, res = _run(ctx, case, pipe)
+        assert res.report.surface_pass == 2
+        _check_against_oracle(ctx, case, pipe, res)
+        out[mode] = (ctx.triangles(with_meta=True), res.rgba.copy(), res.report.range)
+    assert np.array_equal(out["1"][0][1], out["0"][0][1])
+    assert np.array_equal(out["1"][0][0].view(np.uint32), out["0"][0][0].view(np.uint32))
+    assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
