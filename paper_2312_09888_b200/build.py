@@ -46,9 +46,15 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+CHECKED_LIB = os.path.join(LIBDIR, "libnekb200_checked.so")
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """Build libnekb200.so; checked=True builds libnekb200_checked.so instead:
+    the same sources with -DNKB_CHECKED (device bounds checks, checked.cuh)."""
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj_checked" if checked else "obj")
+    lib_path = CHECKED_LIB if checked else LIB
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "nekb200.h"))
@@ -60,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([cc, *_flags(), "-c", s, "-o", o])
+            jobs.append([cc, *_flags(), *(["-DNKB_CHECKED"] if checked else []), "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -72,8 +78,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run([cc, *ARCH, "-shared", "-o", LIB, *objs, "-ldl", "-cudart", "static"])
+    if force or jobs or _stale(lib_path, objs):
+        run([cc, *ARCH, "-shared", "-o", lib_path, *objs, "-ldl", "-cudart", "static"])
+    if checked:
+        return lib_path
     # FP64 peak probe (tools/fp64_probe.cu): the bench's FP64 roofline denominator
     probe_src = os.path.join(ROOT, "tools", "fp64_probe.cu")
     probe = os.path.join(LIBDIR, "libnkbprobe.so")
@@ -90,4 +98,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

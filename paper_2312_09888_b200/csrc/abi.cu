@@ -179,6 +179,25 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
   return NKB_OK;
 }
 
+// checked build (NKB_CHECKED): device bounds-check violations of the last
+// kernels, per source file; the product build's accessors return 0
+int nkb::checked_violations() {
+  struct {
+    const char* file;
+    unsigned long long (*read)(int*);
+  } src[] = {{"fused.cu", checked_read_fused},
+             {"stream.cu", checked_read_stream},
+             {"raster.cu", checked_read_raster},
+             {"composite.cu", checked_read_composite}};
+  for (auto& f : src) {
+    int line = 0;
+    const unsigned long long n = f.read(&line);
+    if (n) return fail(NKB_ECUDA, std::string("device bounds check failed ") + std::to_string(n) + "x, first at " +
+                                      f.file + ":" + std::to_string(line));
+  }
+  return NKB_OK;
+}
+
 int nkb::ctx_check(nkb_ctx* ctx) {
   if (!ctx) return fail(NKB_EINVAL, "null context");
   NKB_CUDA(cudaSetDevice(ctx->device));
@@ -1145,6 +1164,11 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     reran = 1;
   }
   ctx->last_ntri = ntri;
+  if (getenv("NKB_CHECKED_SELFTEST")) {
+    NKB_TRY(checked_selftest(s));
+    NKB_CUDA(cudaStreamSynchronize(s));
+  }
+  NKB_TRY(checked_violations());
   ctx->image_valid = (!composite || ctx->rank == 0);
   if (out) {
     memset(out, 0, sizeof(*out));
@@ -1242,6 +1266,7 @@ int nkb_composite_partitions(nkb_ctx* root, nkb_ctx* const* parts, int n, const 
   cudaFree(err);
   NKB_TRY(rc);
   if (h_err) return fail(NKB_ECUDA, "partition composite: flag wait failed");
+  NKB_TRY(checked_violations());
   root->image_valid = true;
   return NKB_OK;
 }

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include "checked.cuh"
 #include "nkb_internal.h"
 #include "raster_dev.cuh"
 
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(256) p2p_composite_kernel(P2PParams p) {
       t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
       o = rdev::cmap_rgba(p.cmap, t);
     }
+    NKB_DCHECK(i >= i0 && i < i1 && i < p.npx);
     reinterpret_cast<uchar4*>(p.root_rgba)[i] = o;
     p.root_depth[i] = dep;
   };
@@ -185,5 +187,7 @@ int launch_p2p_composite(const P2PParams& p, cudaStream_t s) {
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
+
+NKB_CHECKED_ACCESSOR(checked_read_composite)
 
 }  // namespace nkb

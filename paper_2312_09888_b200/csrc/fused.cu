@@ -46,6 +46,7 @@
 
 #define NKB_MC_NO_HOST_TABLES
 #include "mc_tables.h"
+#include "checked.cuh"
 #include "nkb_internal.h"
 #include "sem_dev.cuh"
 
@@ -956,7 +957,7 @@ static int node_prog_of(const FusedParams& p) {
   return 0;
 }
 
-int fused_node_prog(const FusedParams& p) { return node_prog_of(p); }
+int fused_node_prog(const FusedParams& p) { return node_prog_of(p) + 16 * stream_prog_of(p); }
 
 // ---- K1g: the cached-geometry gradient pass, two independent CTAs per SM ----
 // K1 runs one 512-thread CTA per SM whose phases (pencils | node | classify |
@@ -1039,7 +1040,10 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
         const double* src = p.in_ptr[f] + g0;
         double* d = dst + f * kArr;
 #pragma unroll
-        for (int h = 0; h < 8; ++h) cp_async8(d + qs[h], src + 64 * h);
+        for (int h = 0; h < 8; ++h) {
+          NKB_DCHECK(qs[h] >= 0 && qs[h] < kArr && e >= 0 && e < E && f * kArr + (b + 1) * nin * kArr <= 2 * nin * kArr);
+          cp_async8(d + qs[h], src + 64 * h);
+        }
       }
     }
     if (kCompact) {                                    // the element's compact J^-1 block
@@ -1100,6 +1104,9 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
 
     // ---- u,v,w pencils: thread = (dir, pencil), 3 fields share offsets ----
     if (tid < 192) {
+#pragma unroll
+      for (int m = 0; m < kNP; ++m) NKB_DCHECK(off[m] >= 0 && off[m] < kArr);
+      NKB_DCHECK(slot_vel >= 0 && slot_vel + 3 <= nin);
       const double* su = S_in + slot_vel * kArr;
       double* d0 = S_dv + (tid >> 6) * kArr;
       pencil3(su, su + kArr, su + 2 * kArr, d0, d0 + 3 * kArr, d0 + 6 * kArr, off);
@@ -1113,6 +1120,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     for (int h = 0; h < 2; ++h) {
       const int n = tid + kG2Threads * h;
       const int q = h ? q1 : q0;
+      NKB_DCHECK(n < kNN && q >= 0 && q < kArr);
       double J[9];
       if (kCompact) {
         geo_compact_node(S_gc + b * kGeoCompactDoubles, n, J);
@@ -1187,7 +1195,10 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
           else if (NP.s[s] == NK_Q) val = vq;
           else if (NP.s[s] == NK_W) val = vw;
           else if (NP.s[s] == NK_U) val = vu;
-          else val = S_in[sc_off[s] + q];
+          else {
+            NKB_DCHECK(sc_off[s] >= 0 && sc_off[s] + kArr <= nin * kArr);
+            val = S_in[sc_off[s] + q];
+          }
           bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
         }
         if (NP.c != NK_NONE) {
@@ -1256,6 +1267,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
 #pragma unroll
     for (int u = 0; u < 2; ++u)
       if (nt[u] > 0) {
+        NKB_DCHECK(act >= 0 && act < kNC && 2 * tid + u < kNC);
         mc.act_cell[act] = (unsigned short)(2 * tid + u);
         mc.act_cases[act] = pk[u];
         mc.act_off[act] = (unsigned short)tri_off;
@@ -1306,6 +1318,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
         if ((int)mc.act_off[mid] <= tt) lo = mid;
         else hi = mid - 1;
       }
+      NKB_DCHECK(lo >= 0 && lo < n_act && n_act <= kNC);
       const int c = mc.act_cell[lo];
       const unsigned packed = mc.act_cases[lo];
       int li = tt - (int)mc.act_off[lo], s = 0;
@@ -1332,6 +1345,9 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
       const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
       const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
+      NKB_DCHECK(c >= 0 && c < kNC && s >= 0 && s < p.n_surf && k >= 0 && k < NKB_MC_MAX_TRI);
+      NKB_DCHECK(qa >= 0 && qa < kArr && qb >= 0 && qb < kArr && pa >= 0 && pa < kNN && pb >= 0 && pb < kNN);
+      NKB_DCHECK(out >= 0 && out < p.tri_cap);
       const double sa = value_at(src, s, qa, pa), sb = value_at(src, s, qb, pb);
       const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
       const double cla = value_at(p.color_src, 0, qa, pa), clb = value_at(p.color_src, 0, qb, pb);
@@ -1559,5 +1575,7 @@ int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long l
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
+
+NKB_CHECKED_ACCESSOR(checked_read_fused)
 
 }  // namespace nkb

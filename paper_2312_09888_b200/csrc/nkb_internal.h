@@ -179,7 +179,15 @@ int launch_fused_prepare();
 // K1s (stream.cu): pipelines without a velocity gradient (no exports, fields
 // 16-byte aligned); launch_fused dispatches to it when surface_pass_of == 1
 bool stream_eligible(const FusedParams& p);
-int fused_node_prog(const FusedParams& p);   // K1g node program (graph key)
+// checked build: per-file device bounds-check counters (checked.cuh)
+unsigned long long checked_read_fused(int* line);
+unsigned long long checked_read_stream(int* line);
+unsigned long long checked_read_raster(int* line);
+unsigned long long checked_read_composite(int* line);
+int checked_violations();
+int checked_selftest(cudaStream_t s);          // NKB_CHECKED_SELFTEST=1: one failing check
+int fused_node_prog(const FusedParams& p);   // K1g + 16 x K1s node program (graph key)
+int stream_prog_of(const FusedParams& p);    // K1s node program
 int surface_pass_of(const FusedParams& p);     // 0 K1, 1 K1s (stream.cu), 2 K1g (two CTAs per SM)
 int fused_grid_for(const FusedParams& p, int64_t n_elements);   // triangle regions of that pass
 int launch_stream(const FusedParams& p, int grid, cudaStream_t s);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include "checked.cuh"
 #include "nkb_internal.h"
 #include "raster_dev.cuh"
 
@@ -38,6 +39,7 @@ __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
   const long long gw = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;   // region-local warp
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long t = gw * 32 + (threadIdx.x & 31); t < ntri; t += nw * 32) {
+    NKB_DCHECK(t >= 0 && t < p.region_cap && r < p.n_regions);
     rdev::raster_triangle(p.view, W, H, tri + 3 * t, p.zbuf);
   }
 }
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
   const double span = __dsub_rn(hi, lo);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
+    NKB_DCHECK(i >= 0 && i < n);
     const unsigned long long key = p.zbuf[i];
     uchar4 o;
     float dep;
@@ -283,5 +286,20 @@ int launch_structured_render(const StructuredParams& p, cudaStream_t s) {
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
+
+#ifdef NKB_CHECKED
+// a check that always fails (NKB_CHECKED_SELFTEST=1): proves a violation
+// reaches nkb_execute's error
+__global__ void checked_selftest_kernel() { NKB_DCHECK(threadIdx.x > 0); }
+int checked_selftest(cudaStream_t s) {
+  checked_selftest_kernel<<<1, 32, 0, s>>>();
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+#else
+int checked_selftest(cudaStream_t) { return NKB_OK; }
+#endif
+
+NKB_CHECKED_ACCESSOR(checked_read_raster)
 
 }  // namespace nkb

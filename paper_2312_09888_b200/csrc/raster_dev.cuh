@@ -7,6 +7,8 @@
 // oracle/sem_oracle.c restates them operation for operation.
 #pragma once
 
+#include "checked.cuh"
+
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -166,6 +168,7 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
           const unsigned long long key =
               ((unsigned long long)__float_as_uint(__double2float_rn(d)) << 32) |
               (unsigned long long)__float_as_uint(__double2float_rn(c));
+          NKB_DCHECK(px >= 0 && px < W && py >= 0 && py < H);
           atomicMin(zbuf + py * W + px, key);
         }
       }

@@ -32,9 +32,11 @@
 // bit-identical to K1 and to the CPU oracle.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #define NKB_MC_NO_HOST_TABLES
 #include "mc_tables.h"
+#include "checked.cuh"
 #include "nkb_internal.h"
 #include "sem_dev.cuh"
 
@@ -48,8 +50,7 @@ __device__ const unsigned char gs_mc_ntri[256] = {NKB_MC_NTRI_DATA};
 __device__ const signed char gs_mc_tri[256][3 * NKB_MC_MAX_TRI] = {NKB_MC_TRI_DATA};
 __device__ const unsigned char gs_mc_edge_v[12][2] = {NKB_MC_EDGE_V_DATA};
 
-constexpr int kSThreads = 768;
-constexpr int kSWarps = kSThreads / 32;
+constexpr int kSMaxThreads = 1024;                 // block sizes: 768 (default), 896, 1024
 constexpr int kChunks = (kNC + 31) / 32;   // 11 chunks of 32 sub-hexes
 
 struct WarpScratch {
@@ -69,7 +70,13 @@ __device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpr
 
 }  // namespace
 
+// kSProg: node program (cf. fused.cu node_prog).  0 = generic runtime
+// dispatch; 1 = the C4 shape -- |u| iso (surface 0) + one slice plane
+// (surface 1), colour |u|, no scalars: only u,v,w and the plane's coordinates
+// are loaded and live, so the node loop needs fewer registers.
+template <int kSThreads, int kSProg>
 __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const FusedParams p, const StreamFlags fl) {
+  constexpr int kSWarps = kSThreads / 32;
   extern __shared__ __align__(16) unsigned char s_raw[];
   __shared__ unsigned char t_ntri[256];
   __shared__ signed char t_tri[256][3 * NKB_MC_MAX_TRI];
@@ -104,9 +111,34 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const FusedParams 
     if ((long long)it >= n_it) break;
     const long long e = blockIdx.x + (long long)it * G;
     const long long g0 = e * (long long)kNN;
+    NKB_DCHECK(e >= 0 && e < E);
 
     // ---- node phase: 2 nodes per lane per step, 16-byte loads ----
     unsigned band = 0xffu, bor = 0u;
+    if (kSProg == 1) {
+#pragma unroll 1
+      for (int k = 0; k < 8; ++k) {
+        const long long gi = g0 + 64 * k + 2 * lane;
+        double2 X = make_double2(0.0, 0.0), Y = X, Z = X;
+        if (fl.xyz & 1) X = ld2(p.x + gi);
+        if (fl.xyz & 2) Y = ld2(p.y + gi);
+        if (fl.xyz & 4) Z = ld2(p.z + gi);
+        const double2 U = ld2(p.vel[0] + gi), V = ld2(p.vel[1] + gi), W = ld2(p.vel[2] + gi);
+        unsigned b2 = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double vu = mag3(h ? U.y : U.x, h ? V.y : V.x, h ? W.y : W.x);
+          const double pd = plane_dist(p.surf_n[1], h ? X.y : X.x, h ? Y.y : Y.x, h ? Z.y : Z.x);
+          const unsigned bits = (vu >= p.surf_iso[0] ? 1u : 0u) | ((pd >= p.surf_iso[1] ? 1u : 0u) << 1);
+          b2 |= bits << (8 * h);
+          cmin = fmin(cmin, vu);
+          cmax = fmax(cmax, vu);
+        }
+        reinterpret_cast<unsigned short*>(bytes)[32 * k + lane] = (unsigned short)b2;
+        band &= b2 & (b2 >> 8);
+        bor |= (b2 | (b2 >> 8)) & 0xffu;
+      }
+    } else
 #pragma unroll 1
     for (int k = 0; k < 8; ++k) {
       const long long gi = g0 + 64 * k + 2 * lane;
@@ -194,6 +226,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const FusedParams 
       const unsigned act = __ballot_sync(full, nc > 0);
       if (nc > 0) {
         const int a = n_act + __popc(act & lt_mask);
+        NKB_DCHECK(a >= 0 && a < kNC && c < kNC);
         ws.cell[a] = (unsigned short)c;
         ws.cases[a] = packed;
         ws.off[a] = (unsigned short)(total + incl - nc);
@@ -251,6 +284,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const FusedParams 
             const int va = t_edge[ed][0], vb = t_edge[ed][1];
             const int na = (ca + voff_i(va)) + kNP * (cb + voff_j(va)) + kNP * kNP * (ck + voff_k(va));
             const int nb = (ca + voff_i(vb)) + kNP * (cb + voff_j(vb)) + kNP * kNP * (ck + voff_k(vb));
+            NKB_DCHECK(na >= 0 && na < kNN && nb >= 0 && nb < kNN && out >= 0 && out < p.tri_cap);
             const double sa = value_at(src, s, na), sb = value_at(src, s, nb);
             const double tv = __ddiv_rn(__dsub_rn(iso, sa), __dsub_rn(sb, sa));
             const double cla = (p.color_src == src) ? sa : (p.color_src >= 0 ? value_at(p.color_src, 0, na) : 0.0);
@@ -307,9 +341,27 @@ __global__ void __launch_bounds__(kSThreads, 1) stream_kernel(const FusedParams 
   }
 }
 
+// block size: the generic program 896 threads (28 warps, <= 72 registers:
+// C4 3.90 -> 3.54 ms against 768; 1024 spills), node program 1 1024 threads
+// (32 warps, no spills: C4 2.90 -> 2.85 ms against 896);
+// NKB_STREAM_THREADS=768 / 896 / 1024 overrides (A/B runs)
+static int stream_threads(int prog) {
+  const char* v = getenv("NKB_STREAM_THREADS");
+  const int n = v ? atoi(v) : (prog == 1 ? 1024 : 896);
+  return (n == 768 || n == 1024) ? n : 896;
+}
+
 int launch_stream_prepare() {
-  NKB_CUDA(cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(WarpScratch) * kSWarps)));
+#define NKB_SP(T, P)                                                                              \
+  NKB_CUDA(cudaFuncSetAttribute(stream_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                (int)(sizeof(WarpScratch) * (T / 32))))
+  NKB_SP(768, 0);
+  NKB_SP(896, 0);
+  NKB_SP(1024, 0);
+  NKB_SP(768, 1);
+  NKB_SP(896, 1);
+  NKB_SP(1024, 1);
+#undef NKB_SP
   return NKB_OK;
 }
 
@@ -323,6 +375,16 @@ static StreamFlags stream_flags(const FusedParams& p) {
   return fl;
 }
 
+// the K1s node program of pipeline `p` (0 = generic)
+int stream_prog_of(const FusedParams& p) {
+  const char* v = getenv("NKB_NODE_PROGS");             // A/B: NKB_NODE_PROGS=0 forces the generic program
+  if (v && v[0] == '0') return 0;
+  const StreamFlags fl = stream_flags(p);
+  return (p.n_surf == 2 && p.surf_src[0] == SRC_UMAG && p.surf_src[1] >= SRC_PLANE && p.color_src == SRC_UMAG &&
+          fl.nsc == 0 && fl.umag) ? 1 : 0;
+}
+
+
 bool stream_eligible(const FusedParams& p) {
   if (p.need_grad || p.q_out || p.wmag_out || p.vort_out) return false;
   const StreamFlags fl = stream_flags(p);
@@ -334,9 +396,25 @@ bool stream_eligible(const FusedParams& p) {
 }
 
 int launch_stream(const FusedParams& p, int grid, cudaStream_t s) {
-  stream_kernel<<<(unsigned)grid, kSThreads, sizeof(WarpScratch) * kSWarps, s>>>(p, stream_flags(p));
+  const StreamFlags fl = stream_flags(p);
+  const int prog = stream_prog_of(p);
+  const int t = stream_threads(prog);
+  const size_t sh = sizeof(WarpScratch) * (t / 32);
+#define NKB_SL(T, P) stream_kernel<T, P><<<(unsigned)grid, T, sh, s>>>(p, fl)
+  if (prog == 1) {
+    if (t == 1024) NKB_SL(1024, 1);
+    else if (t == 896) NKB_SL(896, 1);
+    else NKB_SL(768, 1);
+  } else {
+    if (t == 1024) NKB_SL(1024, 0);
+    else if (t == 896) NKB_SL(896, 0);
+    else NKB_SL(768, 0);
+  }
+#undef NKB_SL
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
+
+NKB_CHECKED_ACCESSOR(checked_read_stream)
 
 }  // namespace nkb

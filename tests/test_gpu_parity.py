@@ -510,3 +510,20 @@ def test_node_programs_equal_generic_dispatch(ctx, name, monkeypatch):
     assert np.array_equal(out["1"][0][1], out["0"][0][1])
     assert np.array_equal(out["1"][0][0].view(np.uint32), out["0"][0][0].view(np.uint32))
     assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
+
+
+def test_stream_node_program_equals_generic(ctx, monkeypatch):
+    """K1s node program 1 (|u| iso + slice, colour |u|: the C4 shape) against
+    the generic K1s dispatch and the oracle."""
+    case = synth.box(nel=(4, 3, 3))
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("NKB_NODE_PROGS", mode)
+        pipe = Pipeline(**{**NOGRAD_PIPES["umag_iso_umag_colour"].__dict__, "emit_meta": True})
+        _, res = _run(ctx, case, pipe)
+        assert res.report.surface_pass == 1
+        _check_against_oracle(ctx, case, pipe, res)
+        out[mode] = (ctx.triangles(with_meta=True), res.rgba.copy(), res.report.range)
+    assert np.array_equal(out["1"][0][1], out["0"][0][1])
+    assert np.array_equal(out["1"][0][0].view(np.uint32), out["0"][0][0].view(np.uint32))
+    assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
