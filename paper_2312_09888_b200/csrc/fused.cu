@@ -1041,7 +1041,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
         double* d = dst + f * kArr;
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-          NKB_DCHECK(qs[h] >= 0 && qs[h] < kArr && e >= 0 && e < E && f * kArr + (b + 1) * nin * kArr <= 2 * nin * kArr);
+          NKB_DCHECK(qs[h] >= 0 && qs[h] < kArr && e >= 0 && e < E && f < nin && (b == 0 || b == 1));
           cp_async8(d + qs[h], src + 64 * h);
         }
       }
