@@ -905,6 +905,9 @@ int launch_geometry(const double* x, const double* y, const double* z, int64_t E
 }
 
 
+// A/B switch (NKB_EMIT_PREFETCH=0): L2 prefetch of an emitting element's coordinates in K1g
+__constant__ int g_emit_prefetch = 1;
+
 // ---- node programs: compile-time surface / colour sources of a pipeline ----
 // The node phase's per-surface source dispatch (Q, |w|, |u|, a staged scalar
 // or a plane distance, chosen per node from runtime codes) cost as many
@@ -1072,6 +1075,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
   const int psy = ((plane_slots >> 8) & 0xff) == 0xff ? -1 : ((plane_slots >> 8) & 0xff);
   const int psz = ((plane_slots >> 16) & 0xff) == 0xff ? -1 : ((plane_slots >> 16) & 0xff);
   constexpr NodeProg NP = node_prog(kProg);
+  const bool kEmitPrefetch = g_emit_prefetch;
   // node programs: staged-array offset of each scalar surface and of a scalar colour
   int sc_off[NKB_MAX_SURFACES], sc_off_c = 0;
 #pragma unroll
@@ -1226,6 +1230,15 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     if ((mc.bor & ~mc.band) == 0) {                    // no surface crosses this element
       if (p.mode == FUSED_COUNT && tid == 0) p.elem_count[e] = 0;
       continue;
+    }
+    // the element emits: its corner coordinates (never staged unless a slice
+    // uses them) are read by the emission a few hundred cycles from now --
+    // pull the three 4 KB blocks toward L2 while classification runs
+    if (kEmitPrefetch && tid == 0 && p.mode != FUSED_COUNT) {
+      const long long gx = e * (long long)kNN;
+      l2_prefetch(p.x + gx, kNN * sizeof(double));
+      l2_prefetch(p.y + gx, kNN * sizeof(double));
+      l2_prefetch(p.z + gx, kNN * sizeof(double));
     }
 
     // ---- classify: sub-hexes 2t, 2t+1; one block scan of (triangles, active cells) ----
@@ -1421,6 +1434,9 @@ static F2Kernel f2_kernel(bool compact, int wo, int prog) {
   return compact ? f2_kernel_c<true>(wo, prog) : f2_kernel_c<false>(wo, prog);
 }
 static int fused2_prepare() {
+  const char* v = getenv("NKB_EMIT_PREFETCH");
+  const int on = !(v && v[0] == '0');
+  NKB_CUDA(cudaMemcpyToSymbol(g_emit_prefetch, &on, sizeof(on)));
   for (int c = 0; c < 2; ++c) {
     const int bytes = (int)fused2_smem_bytes(kG2MaxIn, c == 1);
     for (int wo = 0; wo < 4; ++wo)
