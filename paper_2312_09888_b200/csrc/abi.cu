@@ -1111,7 +1111,12 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   if (p->composite && ctx->nranks > 1 && !ctx->comm) return fail(NKB_ENCCL, "composite without comm");
 
   NKB_TRY(ensure_image(ctx, p->width, p->height));
-  if (ctx->tri_cap == 0) NKB_TRY(ensure_tri(ctx, std::max<int64_t>(1 << 16, ctx->E * 16), p->emit_meta));
+  if (ctx->tri_cap == 0) {
+    // initial capacity; NKB_TRI_CAP0 overrides it (tests force an overflow on one rank)
+    const char* c0 = getenv("NKB_TRI_CAP0");
+    const int64_t cap0 = c0 ? std::max<int64_t>(1, atoll(c0)) : std::max<int64_t>(1 << 16, ctx->E * 16);
+    NKB_TRY(ensure_tri(ctx, cap0, p->emit_meta));
+  }
   else NKB_TRY(ensure_tri(ctx, ctx->tri_cap, p->emit_meta));
 
   const bool ordered = p->emit_meta && ctx->E > 0 && p->n_surfaces > 0;

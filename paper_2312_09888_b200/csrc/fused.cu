@@ -960,35 +960,39 @@ static int node_prog_of(const FusedParams& p) {
   return 0;
 }
 
-int fused_node_prog(const FusedParams& p) { return node_prog_of(p) + 16 * stream_prog_of(p); }
 
-// ---- K1g: the cached-geometry gradient pass, two independent CTAs per SM ----
+// ---- K1g: the cached-geometry gradient pass, 2-3 independent CTAs per SM ----
 // K1 runs one 512-thread CTA per SM whose phases (pencils | node | classify |
 // emit) are serialised by CTA-wide barriers; its phase profile shows the SM
-// waiting at them.  K1g runs TWO 256-thread CTAs per SM, each owning one
-// element at a time start to finish, so one CTA's barrier waits and load
-// latency are covered by the other CTA's work:
+// waiting at them.  K1g runs two (or three, kOcc) 256-thread CTAs per SM,
+// each owning one element at a time start to finish, so one CTA's barrier
+// waits and load latency are covered by the others' work:
 //   - inputs double-buffered (cp.async, 8 B per node, the swizzled layout of
-//     K1), issued by warps 6-7 while warps 0-5 run the pencils;
-//   - the cached J^-1 is read per node straight from global memory (coalesced),
-//     pulled toward L2 one element ahead by a bulk prefetch, instead of staged;
-//   - u,v,w pencils on 192 threads (pencil3 of K1), then 2 nodes per thread,
-//     then classification (2 sub-hexes per thread), one block scan of packed
+//     K1), issued by warps 6-7 while warps 0-5 run the pencils; with the
+//     compact cache the element's 2112-byte J^-1 block is staged alongside
+//     (full cache: J^-1 read per node from global memory, pulled toward L2 one
+//     element ahead by a bulk prefetch);
+//   - u,v,w pencils on 192 threads (pencil3 of K1), then 2 nodes per thread
+//     (node programs: compile-time sources, see node_prog), then
+//     classification (2 sub-hexes per thread), one block scan of packed
 //     (triangle, active-cell) counts, and emission with one task per triangle
-//     vertex over all 256 threads -- all inside the element's iteration.
+//     vertex over all 256 threads -- all inside the element's iteration;
+//   - three CTAs per SM when a CTA fits in 75 KB of shared memory (compact
+//     cache, <= 3 staged arrays: C1, C3, C5) and 85 registers.  (C2 stages
+//     5 arrays; reading its scalar and slice coordinate per node from global
+//     memory instead, to fit three CTAs, was slower: 0.270 -> 0.309 ms.)
 // Every value is computed by K1's device functions in K1's order, so the
 // results are bit-identical to K1 and to the oracle.
 constexpr int kG2Threads = 256;
-constexpr int kG2PerSM = 2;
 constexpr int kG2MaxIn = 7;                 // 2 CTAs/SM of (2*nin + 11) * 4 KB shared memory
 
+// static shared scratch of K1g; the per-element active-cell lists live in the
+// derivative arrays' space (dead once the node phase has read them) and the
+// triangle table is read through L1 (g_mc_tri), which keeps a CTA at <= 75 KB
+// so that three fit on an SM when the staging is small (kOcc = 3)
 struct G2Scratch {
   unsigned char t_ntri[256];
-  signed char t_tri[256][3 * NKB_MC_MAX_TRI];
   unsigned char t_edge[12][2];
-  unsigned act_cases[kNC];
-  unsigned short act_cell[kNC];
-  unsigned short act_off[kNC];
   int wsum[kG2Threads / 32];
   unsigned long long base;
   unsigned band, bor;
@@ -1004,14 +1008,21 @@ __device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
 // array is exported (q_out / wmag_out / vort_out).  Both are compile-time so
 // the node phase carries no dead work for the common pipelines.
 // kProg: node program (0 = generic runtime dispatch).
-template <bool kCompact, bool kWmag, bool kOut, int kProg>
-__global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const FusedParams p, int nin, int slot_sc,
-                                                                     int slot_vel, int slot_xyz, int plane_slots) {
+// kOcc: CTAs per SM the registers are budgeted for (2, or 3 for compact
+// pipelines staging <= 3 arrays).
+template <bool kCompact, bool kWmag, bool kOut, int kProg, int kOcc>
+__global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedParams p, int nin, int slot_sc,
+                                                                 int slot_vel, int slot_xyz, int plane_slots) {
   extern __shared__ __align__(16) double smem[];
   double* S_ring = smem;                               // 2 * nin * 512
   double* S_dv = S_ring + 2 * nin * kArr;              // 9 * 512 u,v,w derivatives
-  double* S_q = S_dv + 9 * kArr;                       // Q, |w| (swizzled)
-  double* S_gc = S_q + 2 * kArr;                       // kCompact: 2 x kGeoCompactDoubles
+  double* S_q = S_dv + 9 * kArr;                       // Q (and |w| with kWmag), swizzled
+  double* S_gc = S_q + (kWmag ? 2 : 1) * kArr;          // kCompact: 2 x kGeoCompactDoubles
+  // active-cell lists of the element being emitted: in S_dv's space, free
+  // between the node-phase barrier and the next iteration's pencils
+  unsigned* act_cases = reinterpret_cast<unsigned*>(S_dv);
+  unsigned short* act_cell = reinterpret_cast<unsigned short*>(act_cases + kNC);
+  unsigned short* act_off = act_cell + kNC;
   unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_gc + (kCompact ? 2 * kGeoCompactDoubles : 0));
   __shared__ G2Scratch mc;
   __shared__ double s_mn[kG2Threads / 32], s_mx[kG2Threads / 32];
@@ -1025,7 +1036,6 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
   constexpr unsigned kGeoBytes = 9u * kNN * sizeof(double);
 
   for (int i = tid; i < 256; i += kG2Threads) mc.t_ntri[i] = g_mc_ntri[i];
-  for (int i = tid; i < 256 * 3 * NKB_MC_MAX_TRI; i += kG2Threads) (&mc.t_tri[0][0])[i] = (&g_mc_tri[0][0])[i];
   if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
 
   const int q0 = sw_node(tid), q1 = sw_node(tid + kG2Threads);
@@ -1281,9 +1291,9 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
     for (int u = 0; u < 2; ++u)
       if (nt[u] > 0) {
         NKB_DCHECK(act >= 0 && act < kNC && 2 * tid + u < kNC);
-        mc.act_cell[act] = (unsigned short)(2 * tid + u);
-        mc.act_cases[act] = pk[u];
-        mc.act_off[act] = (unsigned short)tri_off;
+        act_cell[act] = (unsigned short)(2 * tid + u);
+        act_cases[act] = pk[u];
+        act_off[act] = (unsigned short)tri_off;
         ++act;
         tri_off += nt[u];
       }
@@ -1328,13 +1338,13 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       int lo = 0, hi = n_act - 1;                      // last active cell with act_off <= tt
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if ((int)mc.act_off[mid] <= tt) lo = mid;
+        if ((int)act_off[mid] <= tt) lo = mid;
         else hi = mid - 1;
       }
       NKB_DCHECK(lo >= 0 && lo < n_act && n_act <= kNC);
-      const int c = mc.act_cell[lo];
-      const unsigned packed = mc.act_cases[lo];
-      int li = tt - (int)mc.act_off[lo], s = 0;
+      const int c = act_cell[lo];
+      const unsigned packed = act_cases[lo];
+      int li = tt - (int)act_off[lo], s = 0;
       unsigned cs = packed & 0xffu;
       for (;;) {
         const int nt = mc.t_ntri[cs];
@@ -1351,7 +1361,7 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
       const int ca = c % kN, cb = (c / kN) % kN, ck = c / (kN * kN);
       const int src = p.surf_src[s];
       const double iso = p.surf_iso[s];
-      const int ed = mc.t_tri[cs][3 * k + r];
+      const int ed = g_mc_tri[cs][3 * k + r];
       const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
       const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
       const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
@@ -1407,43 +1417,59 @@ __global__ void __launch_bounds__(kG2Threads, kG2PerSM) fused2_kernel(const Fuse
   }
 }
 
-static size_t fused2_smem_bytes(int nin, bool compact) {
-  return (size_t)(2 * nin + 11) * kArr * sizeof(double) + (compact ? 2 * kGeoCompactDoubles * sizeof(double) : 0) +
-         kNN;
+static size_t fused2_smem_bytes(int nin, bool compact, bool wmag) {
+  return (size_t)(2 * nin + 10 + (wmag ? 1 : 0)) * kArr * sizeof(double) +
+         (compact ? 2 * kGeoCompactDoubles * sizeof(double) : 0) + kNN;
 }
 
-// K1g instantiations: generic program x (|w|, exports) and the node programs
+// K1g instantiations: generic program x (|w|, exports) and the node
+// programs, budgeted for 2 CTAs per SM; compact pipelines whose CTA fits in
+// 75 KB of shared memory (staging <= 3 arrays) also for 3 (kOcc = 3, <= 85
+// registers)
 using F2Kernel = void (*)(const FusedParams, int, int, int, int, int);
-template <bool C>
-static F2Kernel f2_kernel_c(int wo, int prog) {
+template <bool C, int O>
+static F2Kernel f2_kernel_co(int wo, int prog) {
   switch (prog) {
-    case 1: return fused2_kernel<C, prog_uses(1, NK_W), false, 1>;
-    case 2: return fused2_kernel<C, prog_uses(2, NK_W), false, 2>;
-    case 3: return fused2_kernel<C, prog_uses(3, NK_W), false, 3>;
-    case 4: return fused2_kernel<C, prog_uses(4, NK_W), false, 4>;
+    case 1: return fused2_kernel<C, prog_uses(1, NK_W), false, 1, O>;
+    case 2: return fused2_kernel<C, prog_uses(2, NK_W), false, 2, O>;
+    case 3: return fused2_kernel<C, prog_uses(3, NK_W), false, 3, O>;
+    case 4: return fused2_kernel<C, prog_uses(4, NK_W), false, 4, O>;
     default: break;
   }
   switch (wo) {
-    case 0: return fused2_kernel<C, false, false, 0>;
-    case 1: return fused2_kernel<C, false, true, 0>;
-    case 2: return fused2_kernel<C, true, false, 0>;
-    default: return fused2_kernel<C, true, true, 0>;
+    case 0: return fused2_kernel<C, false, false, 0, O>;
+    case 1: return fused2_kernel<C, false, true, 0, O>;
+    case 2: return fused2_kernel<C, true, false, 0, O>;
+    default: return fused2_kernel<C, true, true, 0, O>;
   }
 }
-static F2Kernel f2_kernel(bool compact, int wo, int prog) {
-  return compact ? f2_kernel_c<true>(wo, prog) : f2_kernel_c<false>(wo, prog);
+static F2Kernel f2_kernel(bool compact, int wo, int prog, int occ = 2) {
+  if (compact) return occ == 3 ? f2_kernel_co<true, 3>(wo, prog) : f2_kernel_co<true, 2>(wo, prog);
+  return f2_kernel_co<false, 2>(wo, prog);
+}
+constexpr size_t kOcc3MaxSmem = 75u * 1024u - 512u;   // dynamic bytes per CTA that let 3 CTAs share an SM
+static int fused2_occ(int nin, bool compact, bool wmag) {
+  static const int forced = [] {
+    const char* v = getenv("NKB_K1G_OCC");               // A/B: NKB_K1G_OCC=2 forces two CTAs per SM
+    return v ? atoi(v) : 0;
+  }();
+  if (!compact || forced == 2) return 2;
+  return fused2_smem_bytes(nin, true, wmag) <= kOcc3MaxSmem ? 3 : 2;
 }
 static int fused2_prepare() {
   const char* v = getenv("NKB_EMIT_PREFETCH");
   const int on = !(v && v[0] == '0');
   NKB_CUDA(cudaMemcpyToSymbol(g_emit_prefetch, &on, sizeof(on)));
-  for (int c = 0; c < 2; ++c) {
-    const int bytes = (int)fused2_smem_bytes(kG2MaxIn, c == 1);
-    for (int wo = 0; wo < 4; ++wo)
-      NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, wo, 0), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    for (int k = 1; k < kNodeProgs; ++k)
-      NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, 0, k), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  }
+  for (int c = 0; c < 2; ++c)
+    for (int occ = 2; occ <= (c == 1 ? 3 : 2); ++occ) {
+      const int bytes = (int)fused2_smem_bytes(occ == 3 ? 3 : kG2MaxIn, c == 1, true);
+      for (int wo = 0; wo < 4; ++wo)
+        NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, wo, 0, occ), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      bytes));
+      for (int k = 1; k < kNodeProgs; ++k)
+        NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, 0, k, occ), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      bytes));
+    }
   return NKB_OK;
 }
 
@@ -1457,14 +1483,18 @@ static unsigned plane_axes(const FusedParams& p) {
   return m;
 }
 
+// arrays K1g stages per element: the coordinates a slice normal uses, u,v,w, scalars
+static int k1g_nin(const FusedParams& p) {
+  const unsigned m = plane_axes(p);
+  return (int)((m & 1) + ((m >> 1) & 1) + (m >> 2)) + (p.need_vel ? 3 : 0) + p.n_scalars;
+}
+
 static bool fused2_on(const FusedParams& p) {
   const char* v = getenv("NKB_FUSED2");               // A/B: NKB_FUSED2=0 forces K1
   if (v && v[0] == '0') return false;
   if (!(p.geo != nullptr && p.need_grad) || p.prof != nullptr) return false;
-  const unsigned m = plane_axes(p);
-  const int nin = (int)((m & 1) + ((m >> 1) & 1) + (m >> 2)) + (p.need_vel ? 3 : 0) + p.n_scalars;
   // two CTAs per SM: (2 nin + 11) x 4 KB (+ 4 KB of compact geometry) each
-  return nin <= (p.geo_compact ? kG2MaxIn - 1 : kG2MaxIn);
+  return k1g_nin(p) <= (p.geo_compact ? kG2MaxIn - 1 : kG2MaxIn);
 }
 
 static size_t fused_smem_bytes(int nin) {
@@ -1503,7 +1533,7 @@ int surface_pass_of(const FusedParams& p) {
 int fused_grid_for(const FusedParams& p, int64_t n_elements) {
   const int g = fused_grid(n_elements);                 // min(E, SMs)
   if (surface_pass_of(p) != 2) return g;
-  const int64_t g2 = (int64_t)kG2PerSM * g_num_sms;
+  const int64_t g2 = (int64_t)fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0) * g_num_sms;
   return (int)(n_elements < g2 ? (n_elements < 1 ? 1 : n_elements) : g2);
 }
 
@@ -1569,8 +1599,8 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     const int prog = node_prog_of(p);
     const int wm = p.need_wmag != 0 ? 1 : 0;
     const int out = (p.q_out != nullptr || p.wmag_out != nullptr || p.vort_out != nullptr) ? 1 : 0;
-    const size_t sh = fused2_smem_bytes(k2, compact);
-    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog);
+    const size_t sh = fused2_smem_bytes(k2, compact, wm != 0);
+    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog, fused2_occ(k2, compact, wm != 0));
     k<<<g2, kG2Threads, sh, s>>>(q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps);
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
@@ -1590,6 +1620,11 @@ int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long l
   count_scan_kernel<<<1, 1024, 0, s>>>(cnt, n, off, total);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
+}
+
+// the kernel variant a step runs (CUDA-graph cache key; env switches change it)
+int fused_node_prog(const FusedParams& p) {
+  return node_prog_of(p) + 16 * stream_prog_of(p) + 64 * fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0);
 }
 
 NKB_CHECKED_ACCESSOR(checked_read_fused)

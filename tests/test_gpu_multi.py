@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _image(rank, size, out_dir, steps=3, cuts=None):
+def _image(rank, size, out_dir, steps=3, cuts=None, reran_out=None):
     import torch.distributed as dist
 
     from paper_2312_09888_b200 import synth
@@ -44,8 +44,11 @@ def _image(rank, size, out_dir, steps=3, cuts=None):
                                                 element_offset=e0, n_elements_global=E),)))
     params = {**c.params, "width": str(W), "height": str(H)}
     an = InsituAnalysis(pipeline_from_params(params))
+    reran = []
     for _ in range(steps):            # several epochs: exercises the double-buffered key exchange
         res = an.execute(da, depth=True)
+        reran.append(bool(res.report.reran))
+    np.save(os.path.join(out_dir, f"reran{size}_{rank}.npy"), np.array(reran))
     if rank == 0:
         np.savez(os.path.join(out_dir, f"g{size}.npz"), rgba=res.rgba, dep=res.depth,
                  n=res.report.n_triangles_global, rng=np.array(res.report.range))
@@ -53,10 +56,12 @@ def _image(rank, size, out_dir, steps=3, cuts=None):
     comm.close()
 
 
-def _worker(rank, size, port, out_dir, mode="p2p", cuts=None):
+def _worker(rank, size, port, out_dir, mode="p2p", cuts=None, cap0_rank0=None):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK=str(rank), NKB_COMPOSITE=mode)
+    if cap0_rank0 is not None and rank == 0 and size > 1:
+        os.environ["NKB_TRI_CAP0"] = str(cap0_rank0)     # only rank 0 starts too small and overflows
     dist.init_process_group("gloo", rank=rank, world_size=size)
     try:
         _image(rank, size, out_dir, cuts=cuts)
@@ -104,6 +109,27 @@ def test_composite_ragged_partitions_p2p(tmp_path):
     assert np.array_equal(a["rng"], b["rng"])
     assert np.array_equal(a["rgba"], b["rgba"])
     assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_overflow_on_one_rank_reruns_every_rank(tmp_path, mode):
+    """ADVICE (round 1, high): only rank 0 overflows its triangle buffer on the
+    first step.  The decision to grow and re-run is collective, so both ranks
+    re-run that step together (no hang, no stale NCCL/P2P state) and every
+    step's composite equals the one-GPU image."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode, None, 64), nprocs=2, join=True)
+    a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
+    assert int(a["n"]) == int(b["n"])
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
+    r0, r1 = np.load(tmp_path / "reran2_0.npy"), np.load(tmp_path / "reran2_1.npy")
+    assert r0[0] and r1[0], (r0, r1)          # rank 1 did not overflow but re-ran with rank 0
+    assert not r0[1:].any() and not r1[1:].any()
 
 
 _STAT_SIZES = {2: [70, 1000001], 4: [100003, 5, 0, 250], 3: [40, 300000, 77]}
