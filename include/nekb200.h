@@ -117,6 +117,9 @@ typedef struct {
     int     surface_pass;         /* surface pass that ran: 0 = K1 fused (velocity gradient),
                                      1 = K1s stream (no gradient; NKB_STREAM=0 forces K1),
                                      2 = K1g two-CTA gradient pass (geometry cache; NKB_FUSED2=0 forces K1) */
+    int     overflowed;           /* nkb_execute_wait only: the step's triangles overflowed on some
+                                     rank (its triangle set and image are incomplete; the buffer
+                                     has grown for the steps enqueued from now on) */
 } nkb_report;
 
 typedef struct {
@@ -223,6 +226,17 @@ int nkb_set_velocity_name(nkb_ctx* ctx, const char* name);
 
 /* ---- AnalysisAdaptor::Execute (RenderSink.consume, sinks.py:342-348) --- */
 int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stream);
+/* Stream-ordered Execute: enqueue the step on `stream` and return without
+ * a host synchronisation, so consecutive steps (and, across ranks, the P2P
+ * composite) are ordered on the device only and host jitter does not couple
+ * the ranks.  nkb_execute_wait synchronises and fills the report of the
+ * last enqueued step.  The triangle buffer cannot grow behind an enqueued
+ * step: a step that overflows is reported (overflowed = 1, triangles and image
+ * incomplete) and the buffer grows for later steps; nkb_execute (which
+ * re-runs an overflowing step) guarantees a complete result.  pipeline.timing
+ * must be 0. */
+int nkb_execute_async(nkb_ctx* ctx, const nkb_pipeline* p, void* stream);
+int nkb_execute_wait(nkb_ctx* ctx, nkb_report* out, void* stream);
 /* results of the last execute (device pointers, library-owned) */
 int nkb_image_device(nkb_ctx* ctx, const unsigned char** rgba, const float** depth,
                      const uint64_t** zbuf);

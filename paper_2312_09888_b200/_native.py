@@ -74,6 +74,7 @@ class NkbReport(C.Structure):
         ("geometry_cached", C.c_int),
         ("ms_geometry", C.c_float),
         ("surface_pass", C.c_int),
+        ("overflowed", C.c_int),
     ]
 
 
@@ -122,6 +123,8 @@ _SIGS = {
     "nkb_set_geometry_cache": ([_vp, C.c_int], C.c_int),
     "nkb_geometry_info": ([_vp, _vp, _vp], C.c_int),
     "nkb_composite_partitions": ([_vp, _vp, C.c_int, _vp, _vp], C.c_int),
+    "nkb_execute_async": ([_vp, _vp, _vp], C.c_int),
+    "nkb_execute_wait": ([_vp, _vp, _vp], C.c_int),
     "nkb_execute": ([_vp, C.POINTER(NkbPipeline), C.POINTER(NkbReport), _vp], C.c_int),
     "nkb_image_device": ([_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
     "nkb_image_copy": ([_vp, _vp, _vp, _vp], C.c_int),

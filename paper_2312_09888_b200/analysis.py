@@ -262,5 +262,19 @@ class InsituAnalysis:
                 res.rgba = ctx.image(self.pipeline.width, self.pipeline.height)
         return res
 
+    def execute_async(self, data_adaptor) -> None:
+        """Enqueue one step without waiting (nkb_execute_async): steps are
+        ordered on the device only; `wait()` returns the last step's report."""
+        view = self.view_for(data_adaptor)
+        if self._native is None or self._native[0] is not self.pipeline or self._native[1] != view:
+            self._native = (self.pipeline, view, self.pipeline.native(view))
+        data_adaptor.ctx.execute_async(self._native[2])
+        self._async_ctx = data_adaptor.ctx
+        self.executions += 1
+
+    def wait(self) -> Report:
+        """Report of the last execute_async step (synchronises)."""
+        return self._async_ctx.wait()
+
     def finalize(self) -> None:
         pass

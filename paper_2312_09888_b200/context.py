@@ -28,6 +28,7 @@ class Report:
     geometry_cached: bool = False
     ms_geometry: float = 0.0
     surface_pass: int = 0          # 0: K1 fused, 1: K1s stream (no gradient), 2: K1g (cached geometry)
+    overflowed: bool = False       # execute_async steps only: triangles overflowed (result incomplete)
 
     @classmethod
     def from_native(cls, r: N.NkbReport) -> "Report":
@@ -37,6 +38,7 @@ class Report:
             (float(r.data_range[0]), float(r.data_range[1])),
             float(r.ms_fused), float(r.ms_raster), float(r.ms_composite), float(r.ms_resolve),
             bool(r.reran), bool(r.geometry_cached), float(r.ms_geometry), int(r.surface_pass),
+            bool(r.overflowed),
         )
 
 
@@ -152,6 +154,16 @@ class Context:
     def execute(self, pipeline: N.NkbPipeline, stream: int = 0) -> Report:
         r = N.NkbReport()
         N.call("nkb_execute", self.handle, C.byref(pipeline), C.byref(r), stream or None)
+        return Report.from_native(r)
+
+    def execute_async(self, pipeline: N.NkbPipeline, stream: int = 0) -> None:
+        """Enqueue one step without a host synchronisation (nkb_execute_async)."""
+        N.call("nkb_execute_async", self.handle, C.byref(pipeline), stream or None)
+
+    def wait(self, stream: int = 0) -> Report:
+        """Synchronise and return the report of the last execute_async step."""
+        r = N.NkbReport()
+        N.call("nkb_execute_wait", self.handle, C.byref(r), stream or None)
         return Report.from_native(r)
 
     def image(self, width: int, height: int, depth: bool = False, stream: int = 0):

@@ -923,8 +923,23 @@ static std::string step_key(nkb_ctx* ctx, const nkb_pipeline* p, const FusedPara
   return k;
 }
 
+// after the step's report words have landed (stream synchronised): the P2P
+// timeout flag and the global triangle count
+static int collect_step(nkb_ctx* ctx, bool p2p) {
+  if (p2p) {
+    if (*reinterpret_cast<const int*>(ctx->p2p.h_res)) {
+      cudaMemset(ctx->p2p.err, 0, sizeof(int));   // report once; a later step starts clean
+      return fail(NKB_ENCCL, "P2P composite: timed out waiting for a peer rank");
+    }
+    unsigned long long tot = 0;
+    for (int q = 0; q < ctx->nranks; ++q) tot += ctx->p2p.h_res[1 + q];
+    ctx->h_counters[3] = tot;   // meaningful on rank 0 (every rank reports to every rank)
+  }
+  return NKB_OK;
+}
+
 static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
-                    cudaStream_t s, bool composite, bool ordered) {
+                    cudaStream_t s, bool composite, bool ordered, bool sync = true) {
   const bool p2p = composite && ctx->p2p.ready;
   const unsigned long long ep = p2p ? ++ctx->p2p.epoch : 0;   // the device counter follows in-stream
   // Steps replay a CUDA graph of the whole launch sequence (one launch
@@ -971,18 +986,10 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   } else {
     NKB_TRY(enqueue_step(ctx, p, fp, cm, s, composite, ordered, ep));
   }
-  NKB_CUDA(cudaStreamSynchronize(s));
-  if (p2p) {
-    if (*reinterpret_cast<const int*>(ctx->p2p.h_res)) {
-      cudaMemset(ctx->p2p.err, 0, sizeof(int));   // report once; a later step starts clean
-      return fail(NKB_ENCCL, "P2P composite: timed out waiting for a peer rank");
-    }
-    unsigned long long tot = 0;
-    for (int q = 0; q < ctx->nranks; ++q) tot += ctx->p2p.h_res[1 + q];
-    ctx->h_counters[3] = tot;   // meaningful on rank 0 (every rank reports to every rank)
-  }
   ctx->last_fast = !ordered;
-  return NKB_OK;
+  if (!sync) return NKB_OK;                        // stream-ordered (nkb_execute_async): collected at the wait
+  NKB_CUDA(cudaStreamSynchronize(s));
+  return collect_step(ctx, p2p);
 }
 
 // capacity the step needed (per-region maximum in FAST mode)
@@ -1059,7 +1066,15 @@ static int continuous_prepass(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams& 
   return NKB_OK;
 }
 
-int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stream) {
+// one step's parameters, validated and resolved (shared by the synchronous
+// and the stream-ordered Execute)
+struct StepPlan {
+  FusedParams fp;
+  Colormap cm;
+  bool composite = false, ordered = false;
+};
+
+static int prepare_step(nkb_ctx* ctx, const nkb_pipeline* p, cudaStream_t s, StepPlan& plan) {
   NKB_TRY(ctx_check(ctx));
   if (!p) return fail(NKB_EINVAL, "null pipeline");
   if (!ctx->x) return fail(NKB_ESTATE, "Execute before mesh_set");
@@ -1071,9 +1086,7 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     if (!isfinite(p->view[i])) return fail(NKB_EINVAL, "view matrix must be finite");
   for (int i = 0; i < 4; ++i)
     if (!isfinite(p->persp[i])) return fail(NKB_EINVAL, "perspective row must be finite");
-  cudaStream_t s = (cudaStream_t)stream;
-
-  FusedParams fp;
+  FusedParams& fp = plan.fp;
   NKB_TRY(fused_params_base(ctx, fp));
   fp.n_surf = p->n_surfaces;
   for (int k = 0; k < p->n_surfaces; ++k) {
@@ -1104,10 +1117,10 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
     cname[NKB_NAME_MAX] = 0;
     NKB_TRY(resolve_src(ctx, cname, fp, &fp.color_src));
   }
-  Colormap cm;
+  Colormap& cm = plan.cm;
   NKB_TRY(build_colormap(p, cm));
 
-  const bool composite = p->composite && ctx->comm && ctx->nranks > 1;
+  const bool composite = plan.composite = p->composite && ctx->comm && ctx->nranks > 1;
   if (p->composite && ctx->nranks > 1 && !ctx->comm) return fail(NKB_ENCCL, "composite without comm");
 
   NKB_TRY(ensure_image(ctx, p->width, p->height));
@@ -1119,7 +1132,7 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   }
   else NKB_TRY(ensure_tri(ctx, ctx->tri_cap, p->emit_meta));
 
-  const bool ordered = p->emit_meta && ctx->E > 0 && p->n_surfaces > 0;
+  const bool ordered = plan.ordered = p->emit_meta && ctx->E > 0 && p->n_surfaces > 0;
   if (composite && !ctx->p2p.unavailable) {
     const char* mode = getenv("NKB_COMPOSITE");
     if (!(mode && strcmp(mode, "nccl") == 0)) NKB_TRY(p2p_setup(ctx, p->width, p->height, s));
@@ -1128,6 +1141,17 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
   if (p->timing) NKB_CUDA(cudaEventRecord(ctx->ev[5], s));
   if (p->continuous) NKB_TRY(continuous_prepass(ctx, p, fp, s));
   NKB_TRY(geo_attach(ctx, fp, s));
+  return NKB_OK;
+}
+
+int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ctx && ctx->async_pending) return fail(NKB_ESTATE, "an nkb_execute_async step is pending: nkb_execute_wait first");
+  StepPlan plan;
+  NKB_TRY(prepare_step(ctx, p, s, plan));
+  FusedParams& fp = plan.fp;
+  const Colormap& cm = plan.cm;
+  const bool composite = plan.composite, ordered = plan.ordered;
   const bool prof = getenv("NKB_PROFILE_PHASES") != nullptr && !ordered;
   if (prof) {
     if (!ctx->prof) NKB_CUDA(cudaMalloc(&ctx->prof, 18 * sizeof(unsigned long long)));
@@ -1205,6 +1229,65 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
       }
       cudaEventElapsedTime(&out->ms_resolve, ctx->ev[3], ctx->ev[4]);
     }
+  }
+  return NKB_OK;
+}
+
+int nkb_execute_async(nkb_ctx* ctx, const nkb_pipeline* p, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p) return fail(NKB_EINVAL, "null pipeline");
+  if (p->timing) return fail(NKB_EINVAL, "nkb_execute_async: pipeline.timing must be 0 (use nkb_execute)");
+  if (ctx && ctx->async_pending) {
+    // the previous step's report is dropped: collect its P2P status first
+    NKB_CUDA(cudaStreamSynchronize(s));
+    NKB_TRY(collect_step(ctx, ctx->async_composite && ctx->p2p.ready));
+    ctx->async_pending = false;
+  }
+  StepPlan plan;
+  NKB_TRY(prepare_step(ctx, p, s, plan));
+  NKB_TRY(run_step(ctx, p, plan.fp, plan.cm, s, plan.composite, plan.ordered, false));
+  ctx->async_pending = true;
+  ctx->async_composite = plan.composite;
+  ctx->async_ordered = plan.ordered;
+  ctx->async_emit_meta = p->emit_meta != 0;
+  ctx->async_surface_pass = surface_pass_of(plan.fp);
+  ctx->image_valid = (!plan.composite || ctx->rank == 0);
+  return NKB_OK;
+}
+
+int nkb_execute_wait(nkb_ctx* ctx, nkb_report* out, void* stream) {
+  NKB_TRY(ctx_check(ctx));
+  if (!ctx->async_pending) return fail(NKB_ESTATE, "nkb_execute_wait without a pending nkb_execute_async");
+  cudaStream_t s = (cudaStream_t)stream;
+  NKB_CUDA(cudaStreamSynchronize(s));
+  ctx->async_pending = false;
+  const bool composite = ctx->async_composite;
+  NKB_TRY(collect_step(ctx, composite && ctx->p2p.ready));
+  const bool own_over = ctx->h_counters[6] != 0;
+  bool any_over = own_over;
+  if (composite) any_over = ctx->p2p.ready ? ctx->p2p.h_res[1 + kMaxRanks] != 0 : ctx->h_counters[7] != 0;
+  if (own_over) {                                  // grow for the next steps (this one stays incomplete)
+    const int64_t need = needed_capacity(ctx, ctx->async_ordered);
+    NKB_TRY(ensure_tri(ctx, std::max(need + need / 4 + 1024 * ctx->n_regions, ctx->tri_cap + ctx->tri_cap / 4),
+                       ctx->async_emit_meta));
+  }
+  const int64_t ntri = (int64_t)ctx->h_counters[0];
+  ctx->last_ntri = ntri;
+  NKB_TRY(checked_violations());
+  if (out) {
+    memset(out, 0, sizeof(*out));
+    out->n_triangles = ntri;
+    out->n_triangles_global = composite ? (int64_t)ctx->h_counters[3] : ntri;
+    out->tri_capacity = ctx->tri_cap;
+    double r[2];
+    memcpy(r, ctx->h_counters + 4, sizeof(r));
+    out->range[0] = r[0];
+    out->range[1] = r[1];
+    out->data_range[0] = ctx->h_counters[1] == ~0ULL ? NAN : dec_ordered_h(ctx->h_counters[1]);
+    out->data_range[1] = ctx->h_counters[2] == 0ULL ? NAN : dec_ordered_h(ctx->h_counters[2]);
+    out->geometry_cached = ctx->geo_used ? 1 : 0;
+    out->surface_pass = ctx->async_surface_pass;
+    out->overflowed = any_over ? 1 : 0;
   }
   return NKB_OK;
 }

@@ -139,6 +139,10 @@ struct nkb_ctx {
   bool geo_used = false;                     // last step used it
   bool geo_built = false;                    // last step (re)built it
   unsigned long long* prof = nullptr;        // debug phase profile (NKB_PROFILE_PHASES=1)
+  // nkb_execute_async: the enqueued step whose report nkb_execute_wait collects
+  bool async_pending = false;
+  bool async_composite = false, async_ordered = false, async_emit_meta = false;
+  int async_surface_pass = 0;
   std::map<std::vector<long long>, std::unique_ptr<StatsTables>> stats_cache;   // nkb_stats plans
   GsLocal gs;                                // DSSUM gather-scatter plan (nkb_mesh_set_global_ids)
   bool gs_ready = false;

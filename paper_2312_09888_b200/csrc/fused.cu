@@ -1092,6 +1092,11 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   for (int s = 0; s < NKB_MAX_SURFACES; ++s)
     sc_off[s] = (NP.s[s] == NK_SC) ? (slot_sc + p.surf_src[s] - SRC_SCALAR0) * kArr : 0;
   if (NP.c == NK_SC) sc_off_c = (slot_sc + p.color_src - SRC_SCALAR0) * kArr;
+  // a scalar colour read from the array of the program's (single) scalar surface
+  bool sc_col_same = false;
+#pragma unroll
+  for (int s = 0; s < NKB_MAX_SURFACES; ++s)
+    if (NP.s[s] == NK_SC && NP.c == NK_SC && sc_off[s] == sc_off_c) sc_col_same = true;
 
   for (long long it = 0; it < n_it; ++it) {
     const long long e = blockIdx.x + it * G;
@@ -1130,14 +1135,32 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
     // ---- node phase: nodes tid and tid + 256 ----
     const long long g0 = e * (long long)kNN;
     unsigned wand = ~0u, wor = 0u;
+    // compact: my two nodes share (i, j) -- their in-plane J^-1 entries are loaded once
+    double Jij[4] = {0.0, 0.0, 0.0, 0.0};
+    if (kCompact) {
+      const double* g = S_gc + b * kGeoCompactDoubles;
+      const int ij = tid & 63;
+      Jij[0] = g[ij];
+      Jij[1] = g[64 + ij];
+      Jij[2] = g[128 + ij];
+      Jij[3] = g[192 + ij];
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int n = tid + kG2Threads * h;
       const int q = h ? q1 : q0;
       NKB_DCHECK(n < kNN && q >= 0 && q < kArr);
       double J[9];
-      if (kCompact) {
-        geo_compact_node(S_gc + b * kGeoCompactDoubles, n, J);
+      if (kCompact) {                                  // geo_compact_node, with the shared (i, j) entries
+        J[0] = Jij[0];
+        J[1] = Jij[1];
+        J[2] = 0.0;
+        J[3] = Jij[2];
+        J[4] = Jij[3];
+        J[5] = 0.0;
+        J[6] = 0.0;
+        J[7] = 0.0;
+        J[8] = S_gc[b * kGeoCompactDoubles + 256 + (n >> 6)];
       } else {
 #pragma unroll
         for (int c = 0; c < 9; ++c) J[c] = h ? __ldg(p.geo + (e * 9 + c) * kNN + n) : J0[c];
@@ -1199,6 +1222,7 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       } else {                                        // node program: sources fixed at compile time
         if (prog_uses(kProg, NK_U))
           vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
+        double sc_val = 0.0;                            // the (last) scalar surface's value at this node
 #pragma unroll
         for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
           if (NP.s[s] == NK_NONE) continue;
@@ -1212,14 +1236,17 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
           else {
             NKB_DCHECK(sc_off[s] >= 0 && sc_off[s] + kArr <= nin * kArr);
             val = S_in[sc_off[s] + q];
+            sc_val = val;
           }
           bits |= (val >= p.surf_iso[s] ? 1u : 0u) << s;
         }
         if (NP.c != NK_NONE) {
-          const double c = (NP.c == NK_Q)   ? vq
-                           : (NP.c == NK_W) ? vw
-                           : (NP.c == NK_U) ? vu
-                                            : S_in[sc_off_c + q];
+          double c;
+          if (NP.c == NK_Q) c = vq;
+          else if (NP.c == NK_W) c = vw;
+          else if (NP.c == NK_U) c = vu;
+          else if (sc_col_same) c = sc_val;              // the colour is the scalar surface's field
+          else c = S_in[sc_off_c + q];
           cmin = fmin(cmin, c);
           cmax = fmax(cmax, c);
         }

@@ -45,6 +45,19 @@ def _image(rank, size, out_dir, steps=3, cuts=None, reran_out=None):
     params = {**c.params, "width": str(W), "height": str(H)}
     an = InsituAnalysis(pipeline_from_params(params))
     reran = []
+    if os.environ.get("NKB_TEST_ASYNC") == "1":
+        an.execute(da)                    # size the triangle buffers (synchronous, may re-run)
+        for _ in range(steps + 2):        # stream-ordered steps: device-side ordering across ranks only
+            an.execute_async(da)
+        rep = an.wait()
+        assert not rep.overflowed
+        if rank == 0:
+            rgba, dep = ctx.image(W, H, depth=True)
+            np.savez(os.path.join(out_dir, f"g{size}.npz"), rgba=rgba, dep=dep, n=rep.n_triangles_global,
+                     rng=np.array(rep.range))
+        dist.barrier()
+        comm.close()
+        return
     for _ in range(steps):            # several epochs: exercises the double-buffered key exchange
         res = an.execute(da, depth=True)
         reran.append(bool(res.report.reran))
@@ -105,6 +118,24 @@ def test_composite_ragged_partitions_p2p(tmp_path):
     mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), "p2p"), nprocs=1, join=True)
     mp.spawn(_worker, args=(3, _free_port(), str(tmp_path), "p2p", (0, 17, 17, E)), nprocs=3, join=True)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g3.npz")
+    assert int(a["n"]) == int(b["n"])
+    assert np.array_equal(a["rng"], b["rng"])
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_async_steps_composite_equals_single_gpu(tmp_path, mode, monkeypatch):
+    """Stream-ordered steps (nkb_execute_async, no host sync between steps)
+    on 2 ranks: the composited image equals the one-GPU image."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
+    monkeypatch.setenv("NKB_TEST_ASYNC", "1")
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode), nprocs=2, join=True)
+    a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
     assert np.array_equal(a["rgba"], b["rgba"])

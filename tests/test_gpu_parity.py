@@ -527,3 +527,55 @@ def test_stream_node_program_equals_generic(ctx, monkeypatch):
     assert np.array_equal(out["1"][0][1], out["0"][0][1])
     assert np.array_equal(out["1"][0][0].view(np.uint32), out["0"][0][0].view(np.uint32))
     assert np.array_equal(out["1"][1], out["0"][1]) and out["1"][2] == out["0"][2]
+
+
+# ------------------------------------------------------------ stream-ordered execute
+
+
+def test_execute_async_matches_execute(ctx):
+    """nkb_execute_async x 3 then nkb_execute_wait: the same image, triangle
+    set and report as the synchronous execute."""
+    case = synth.rbc_cylinder(nel=(4, 4, 4))
+    pipe = BOX_PIPES["prog_c2"]
+    da, ref = _run(ctx, case, pipe)
+    tri_ref = _rows(ctx.triangles())
+    an = InsituAnalysis(pipe)
+    for _ in range(3):
+        an.execute_async(da)
+    rep = an.wait()
+    assert not rep.overflowed and rep.n_triangles == ref.report.n_triangles
+    assert rep.range == ref.report.range and rep.surface_pass == ref.report.surface_pass
+    rgba, dep = ctx.image(pipe.width, pipe.height, depth=True)
+    assert np.array_equal(rgba, ref.rgba) and np.array_equal(dep.view(np.uint32), ref.depth.view(np.uint32))
+    assert _rows(ctx.triangles()) == tri_ref
+
+
+def test_execute_async_overflow_is_reported_then_grown(monkeypatch):
+    """An async step cannot re-run: with a tiny initial triangle buffer the
+    first step reports overflowed=True, the buffer grows, and the next async
+    step is complete (equal to the synchronous result)."""
+    from paper_2312_09888_b200.context import Context
+
+    monkeypatch.setenv("NKB_TRI_CAP0", "64")
+    c = Context(0)
+    case = synth.box(nel=(3, 3, 2))
+    pipe = BOX_PIPES["three_surfaces"]
+    da = SemDataAdaptor(c)
+    da.initialize(_snapshot(case))
+    an = InsituAnalysis(pipe)
+    an.execute_async(da)
+    r1 = an.wait()
+    assert r1.overflowed and r1.tri_capacity > 64
+    an.execute_async(da)
+    r2 = an.wait()
+    assert not r2.overflowed
+    rgba = c.image(pipe.width, pipe.height)
+    ref = InsituAnalysis(pipe).execute(da)
+    assert ref.report.n_triangles == r2.n_triangles and np.array_equal(ref.rgba, rgba)
+    with pytest.raises(RuntimeError, match="without a pending"):
+        c.wait()
+    an.execute_async(da)
+    with pytest.raises(RuntimeError, match="pending"):
+        c.execute(pipe.native(an.view_for(da)))
+    c.wait()
+    c.close()
