@@ -1017,7 +1017,11 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   double* S_ring = smem;                               // 2 * nin * 512
   double* S_dv = S_ring + 2 * nin * kArr;              // 9 * 512 u,v,w derivatives
   double* S_q = S_dv + 9 * kArr;                       // Q (and |w| with kWmag), swizzled
-  double* S_gc = S_q + (kWmag ? 2 : 1) * kArr;          // kCompact: 2 x kGeoCompactDoubles
+  // node programs colouring (or isosurfacing) by |u| keep it per node for the
+  // emission: one load per corner instead of three loads and a square root
+  constexpr bool kStoreU = prog_uses(kProg, NK_U);
+  double* S_u = S_q + (kWmag ? 2 : 1) * kArr;          // kStoreU: |u| (swizzled)
+  double* S_gc = S_u + (kStoreU ? 1 : 0) * kArr;       // kCompact: 2 x kGeoCompactDoubles
   // active-cell lists of the element being emitted: in S_dv's space, free
   // between the node-phase barrier and the next iteration's pencils
   unsigned* act_cases = reinterpret_cast<unsigned*>(S_dv);
@@ -1220,8 +1224,10 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
           cmax = fmax(cmax, c);
         }
       } else {                                        // node program: sources fixed at compile time
-        if (prog_uses(kProg, NK_U))
+        if (prog_uses(kProg, NK_U)) {
           vu = mag3(S_in[slot_vel * kArr + q], S_in[(slot_vel + 1) * kArr + q], S_in[(slot_vel + 2) * kArr + q]);
+          S_u[q] = vu;
+        }
         double sc_val = 0.0;                            // the (last) scalar surface's value at this node
 #pragma unroll
         for (int s = 0; s < NKB_MAX_SURFACES; ++s) {
@@ -1353,7 +1359,7 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       if (src >= SRC_PLANE) return plane_dist(p.surf_n[s], Sx[pn], Sy[pn], Sz[pn]);
       if (src == SRC_Q) return S_q[q];
       if (src == SRC_WMAG) return S_q[kArr + q];
-      if (src == SRC_UMAG) return mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
+      if (src == SRC_UMAG) return kStoreU ? S_u[q] : mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
       return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
     };
     // one task per triangle VERTEX over all 256 threads: triangle tt's cell
@@ -1444,8 +1450,8 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   }
 }
 
-static size_t fused2_smem_bytes(int nin, bool compact, bool wmag) {
-  return (size_t)(2 * nin + 10 + (wmag ? 1 : 0)) * kArr * sizeof(double) +
+static size_t fused2_smem_bytes(int nin, bool compact, bool wmag, bool umag = false) {
+  return (size_t)(2 * nin + 10 + (wmag ? 1 : 0) + (umag ? 1 : 0)) * kArr * sizeof(double) +
          (compact ? 2 * kGeoCompactDoubles * sizeof(double) : 0) + kNN;
 }
 
@@ -1475,13 +1481,13 @@ static F2Kernel f2_kernel(bool compact, int wo, int prog, int occ = 2) {
   return f2_kernel_co<false, 2>(wo, prog);
 }
 constexpr size_t kOcc3MaxSmem = 75u * 1024u - 512u;   // dynamic bytes per CTA that let 3 CTAs share an SM
-static int fused2_occ(int nin, bool compact, bool wmag) {
+static int fused2_occ(int nin, bool compact, bool wmag, bool umag) {
   static const int forced = [] {
     const char* v = getenv("NKB_K1G_OCC");               // A/B: NKB_K1G_OCC=2 forces two CTAs per SM
     return v ? atoi(v) : 0;
   }();
   if (!compact || forced == 2) return 2;
-  return fused2_smem_bytes(nin, true, wmag) <= kOcc3MaxSmem ? 3 : 2;
+  return fused2_smem_bytes(nin, true, wmag, umag) <= kOcc3MaxSmem ? 3 : 2;
 }
 static int fused2_prepare() {
   const char* v = getenv("NKB_EMIT_PREFETCH");
@@ -1489,7 +1495,7 @@ static int fused2_prepare() {
   NKB_CUDA(cudaMemcpyToSymbol(g_emit_prefetch, &on, sizeof(on)));
   for (int c = 0; c < 2; ++c)
     for (int occ = 2; occ <= (c == 1 ? 3 : 2); ++occ) {
-      const int bytes = (int)fused2_smem_bytes(occ == 3 ? 3 : kG2MaxIn, c == 1, true);
+      const int bytes = (int)fused2_smem_bytes(occ == 3 ? 3 : kG2MaxIn, c == 1, true, true);
       for (int wo = 0; wo < 4; ++wo)
         NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, wo, 0, occ), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       bytes));
@@ -1560,7 +1566,7 @@ int surface_pass_of(const FusedParams& p) {
 int fused_grid_for(const FusedParams& p, int64_t n_elements) {
   const int g = fused_grid(n_elements);                 // min(E, SMs)
   if (surface_pass_of(p) != 2) return g;
-  const int64_t g2 = (int64_t)fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0) * g_num_sms;
+  const int64_t g2 = (int64_t)fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0, prog_uses(node_prog_of(p), NK_U)) * g_num_sms;
   return (int)(n_elements < g2 ? (n_elements < 1 ? 1 : n_elements) : g2);
 }
 
@@ -1626,8 +1632,8 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     const int prog = node_prog_of(p);
     const int wm = p.need_wmag != 0 ? 1 : 0;
     const int out = (p.q_out != nullptr || p.wmag_out != nullptr || p.vort_out != nullptr) ? 1 : 0;
-    const size_t sh = fused2_smem_bytes(k2, compact, wm != 0);
-    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog, fused2_occ(k2, compact, wm != 0));
+    const size_t sh = fused2_smem_bytes(k2, compact, wm != 0, prog_uses(prog, NK_U));
+    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog, fused2_occ(k2, compact, wm != 0, prog_uses(prog, NK_U)));
     k<<<g2, kG2Threads, sh, s>>>(q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps);
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
@@ -1651,7 +1657,7 @@ int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long l
 
 // the kernel variant a step runs (CUDA-graph cache key; env switches change it)
 int fused_node_prog(const FusedParams& p) {
-  return node_prog_of(p) + 16 * stream_prog_of(p) + 64 * fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0);
+  return node_prog_of(p) + 16 * stream_prog_of(p) + 64 * fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0, prog_uses(node_prog_of(p), NK_U));
 }
 
 NKB_CHECKED_ACCESSOR(checked_read_fused)
