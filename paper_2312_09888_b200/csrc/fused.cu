@@ -1027,6 +1027,8 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   unsigned* act_cases = reinterpret_cast<unsigned*>(S_dv);
   unsigned short* act_cell = reinterpret_cast<unsigned short*>(act_cases + kNC);
   unsigned short* act_off = act_cell + kNC;
+  // triangle tt of the element -> its active cell (<= kMaxTriPerElem entries, 13.7 KB, also in S_dv's space)
+  unsigned short* tri_act = act_off + kNC;
   unsigned char* S_bits = reinterpret_cast<unsigned char*>(S_gc + (kCompact ? 2 * kGeoCompactDoubles : 0));
   __shared__ G2Scratch mc;
   __shared__ double s_mn[kG2Threads / 32], s_mx[kG2Threads / 32];
@@ -1327,6 +1329,7 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
         act_cell[act] = (unsigned short)(2 * tid + u);
         act_cases[act] = pk[u];
         act_off[act] = (unsigned short)tri_off;
+        for (int t2 = 0; t2 < nt[u]; ++t2) tri_act[tri_off + t2] = (unsigned short)act;
         ++act;
         tri_off += nt[u];
       }
@@ -1362,19 +1365,14 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       if (src == SRC_UMAG) return kStoreU ? S_u[q] : mag3(Su[q], Su[kArr + q], Su[2 * kArr + q]);
       return S_in[(slot_sc + src - SRC_SCALAR0) * kArr + q];
     };
-    // one task per triangle VERTEX over all 256 threads: triangle tt's cell
-    // by binary search of the active cells' offsets, then its (surface,
-    // table row) by walking the cell's case bytes
+    // one task per triangle VERTEX over all 256 threads: triangle tt's
+    // active cell from the per-triangle table the scan filled, then its
+    // (surface, table row) by walking the cell's case bytes
     const unsigned long long base = mc.base;
     for (int task = tid; task < 3 * total; task += kG2Threads) {
       const int tt = task / 3, r = task - 3 * (task / 3);
-      int lo = 0, hi = n_act - 1;                      // last active cell with act_off <= tt
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if ((int)act_off[mid] <= tt) lo = mid;
-        else hi = mid - 1;
-      }
-      NKB_DCHECK(lo >= 0 && lo < n_act && n_act <= kNC);
+      const int lo = tri_act[tt];                     // the active cell of triangle tt
+      NKB_DCHECK(tt < kMaxTriPerElem && lo >= 0 && lo < n_act && n_act <= kNC);
       const int c = act_cell[lo];
       const unsigned packed = act_cases[lo];
       int li = tt - (int)act_off[lo], s = 0;
