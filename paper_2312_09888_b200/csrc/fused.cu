@@ -1010,7 +1010,12 @@ __device__ __forceinline__ void l2_prefetch(const void* g, unsigned bytes) {
 // kProg: node program (0 = generic runtime dispatch).
 // kOcc: CTAs per SM the registers are budgeted for (2, or 3 for compact
 // pipelines staging <= 3 arrays).
-template <bool kCompact, bool kWmag, bool kOut, int kProg, int kOcc>
+// kTma (A/B of the staging, NKB_K1G_TMA=1): the element's field arrays and
+// J^-1 block arrive by TMA bulk copies (cp.async.bulk, one per 4 KB array,
+// completion on an mbarrier per ring buffer) in natural node order instead of
+// 8-byte cp.async into the XOR-swizzled layout; pencils, node phase and
+// emission then index shared memory naturally.
+template <bool kCompact, bool kWmag, bool kOut, int kProg, int kOcc, bool kTma = false>
 __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedParams p, int nin, int slot_sc,
                                                                  int slot_vel, int slot_xyz, int plane_slots) {
   extern __shared__ __align__(16) double smem[];
@@ -1044,13 +1049,46 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   for (int i = tid; i < 256; i += kG2Threads) mc.t_ntri[i] = g_mc_ntri[i];
   if (tid < 24) (&mc.t_edge[0][0])[tid] = (&g_mc_edge_v[0][0])[tid];
 
-  const int q0 = sw_node(tid), q1 = sw_node(tid + kG2Threads);
+  const int q0 = kTma ? tid : sw_node(tid), q1 = kTma ? tid + kG2Threads : sw_node(tid + kG2Threads);
   // staging of the next element by warps 6-7 (idle during the u,v,w pencils):
   // 64 threads x 8 nodes per field, coalesced 8-byte cp.async
   int qs[8];
 #pragma unroll
   for (int h = 0; h < 8; ++h) qs[h] = sw_node((tid & 63) + 64 * h);
+  __shared__ unsigned long long s_tma_bar[2];
+  if (kTma && tid == 192) {
+    mbar_init(&s_tma_bar[0], 1);
+    mbar_init(&s_tma_bar[1], 1);
+  }
+  if (kTma) __syncthreads();
+  auto prefetch_tma = [&](long long e, int b) {      // one thread: nin + 1 bulk copies, one mbarrier
+    if (tid != 192) return;
+    double* dst = S_ring + b * nin * kArr;
+    unsigned long long* bar = &s_tma_bar[b];
+    const unsigned total = (unsigned)(nin * kArr * sizeof(double) + (kCompact ? kGeoCompactDoubles * sizeof(double) : 0));
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    // the buffer was last read through the generic proxy (previous element)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(total) : "memory");
+    for (int f = 0; f < nin; ++f) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + f * kArr);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(d), "l"(p.in_ptr[f] + e * (long long)kNN), "r"((unsigned)(kArr * sizeof(double))), "r"(a)
+                   : "memory");
+    }
+    if (kCompact) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(S_gc + b * kGeoCompactDoubles);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(d), "l"(p.geo + e * kGeoCompactDoubles), "r"((unsigned)(kGeoCompactDoubles * sizeof(double))),
+                   "r"(a)
+                   : "memory");
+    }
+  };
   auto prefetch = [&](long long e, int b) {
+    if (kTma) {
+      prefetch_tma(e, b);
+      return;
+    }
     double* dst = S_ring + b * nin * kArr;
     const long long g0 = e * (long long)kNN + (tid & 63);
 #pragma unroll
@@ -1083,6 +1121,12 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
 
   int off[kNP];                                        // pencil offsets (threads < 192)
   pencil_offsets(tid >> 6 < 3 ? tid >> 6 : 0, tid & 7, (tid >> 3) & 7, off);
+  if (kTma) {                                          // natural node order
+    const int dir = tid >> 6 < 3 ? tid >> 6 : 0, pa = tid & 7, pb = (tid >> 3) & 7;
+#pragma unroll
+    for (int m = 0; m < kNP; ++m)
+      off[m] = dir == 0 ? m + 8 * pa + 64 * pb : dir == 1 ? pa + 8 * m + 64 * pb : pa + 8 * pb + 64 * m;
+  }
   // staged slot of x, y, z for the slice planes (-1: no plane has a nonzero
   // normal component there, so the coordinate is not staged and enters the
   // node-phase distance as 0; only the case bits use it, and a zero of either
@@ -1107,7 +1151,8 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   for (long long it = 0; it < n_it; ++it) {
     const long long e = blockIdx.x + it * G;
     const int b = (int)(it & 1);
-    cp_async_wait_all();
+    if (kTma) mbar_wait(&s_tma_bar[b], (unsigned)((it >> 1) & 1));
+    else cp_async_wait_all();
     if (tid == 0) {
       mc.band = ~0u;
       mc.bor = 0u;
@@ -1396,7 +1441,8 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       const int va = mc.t_edge[ed][0], vb = mc.t_edge[ed][1];
       const int ia = ca + voff_i(va), ja = cb + voff_j(va), ka = ck + voff_k(va);
       const int ib = ca + voff_i(vb), jb = cb + voff_j(vb), kb = ck + voff_k(vb);
-      const int qa = sw(ia, ja, ka), qb = sw(ib, jb, kb);
+      const int qa = kTma ? ia + kNP * ja + kNP * kNP * ka : sw(ia, ja, ka);
+      const int qb = kTma ? ib + kNP * jb + kNP * kNP * kb : sw(ib, jb, kb);
       const int pa = xyz_staged ? qa : ia + kNP * ja + kNP * kNP * ka;
       const int pb = xyz_staged ? qb : ib + kNP * jb + kNP * kNP * kb;
       NKB_DCHECK(c >= 0 && c < kNC && s >= 0 && s < p.n_surf && k >= 0 && k < NKB_MC_MAX_TRI);
@@ -1474,7 +1520,14 @@ static F2Kernel f2_kernel_co(int wo, int prog) {
     default: return fused2_kernel<C, true, true, 0, O>;
   }
 }
-static F2Kernel f2_kernel(bool compact, int wo, int prog, int occ = 2) {
+static bool fused2_tma() {
+  static const bool on = getenv("NKB_K1G_TMA") && getenv("NKB_K1G_TMA")[0] == '1';
+  return on;
+}
+static F2Kernel f2_kernel(bool compact, int wo, int prog, int occ = 2, bool tma = false) {
+  if (tma && compact && prog == 4 && occ == 2) return fused2_kernel<true, false, false, 4, 2, true>;
+  if (tma && compact && prog == 2 && occ == 3) return fused2_kernel<true, true, false, 2, 3, true>;
+  if (tma && compact && prog == 1 && occ == 3) return fused2_kernel<true, false, false, 1, 3, true>;
   if (compact) return occ == 3 ? f2_kernel_co<true, 3>(wo, prog) : f2_kernel_co<true, 2>(wo, prog);
   return f2_kernel_co<false, 2>(wo, prog);
 }
@@ -1501,6 +1554,12 @@ static int fused2_prepare() {
         NKB_CUDA(cudaFuncSetAttribute(f2_kernel(c == 1, 0, k, occ), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       bytes));
     }
+  NKB_CUDA(cudaFuncSetAttribute(f2_kernel(true, 0, 4, 2, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused2_smem_bytes(kG2MaxIn, true, true, true)));
+  NKB_CUDA(cudaFuncSetAttribute(f2_kernel(true, 0, 2, 3, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kOcc3MaxSmem));
+  NKB_CUDA(cudaFuncSetAttribute(f2_kernel(true, 0, 1, 3, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kOcc3MaxSmem));
   return NKB_OK;
 }
 
@@ -1631,7 +1690,11 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     const int wm = p.need_wmag != 0 ? 1 : 0;
     const int out = (p.q_out != nullptr || p.wmag_out != nullptr || p.vort_out != nullptr) ? 1 : 0;
     const size_t sh = fused2_smem_bytes(k2, compact, wm != 0, prog_uses(prog, NK_U));
-    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog, fused2_occ(k2, compact, wm != 0, prog_uses(prog, NK_U)));
+    // TMA staging (A/B only): bulk copies need 16-byte aligned sources
+    bool tma = fused2_tma();
+    for (int f = 0; f < k2; ++f) tma = tma && ((uintptr_t)q2.in_ptr[f] & 15u) == 0;
+    const F2Kernel k = f2_kernel(compact, prog == 0 ? 2 * wm + out : 0, prog,
+                                 fused2_occ(k2, compact, wm != 0, prog_uses(prog, NK_U)), tma);
     k<<<g2, kG2Threads, sh, s>>>(q2, k2, slot2_sc, slot2_vel, slot2_xyz, ps);
     NKB_CUDA(cudaGetLastError());
     return NKB_OK;
