@@ -116,7 +116,7 @@ typedef struct {
     float   ms_geometry;          /* time spent (re)building the cache this step (when timing) */
     int     surface_pass;         /* surface pass that ran: 0 = K1 fused (velocity gradient),
                                      1 = K1s stream (no gradient; NKB_STREAM=0 forces K1),
-                                     2 = K1g two-CTA gradient pass (geometry cache; NKB_FUSED2=0 forces K1) */
+                                     2 = K1g gradient pass, 2-3 CTAs per SM (geometry cache; NKB_FUSED2=0 forces K1) */
     int     overflowed;           /* nkb_execute_wait only: the step's triangles overflowed on some
                                      rank (its triangle set and image are incomplete; the buffer
                                      has grown for the steps enqueued from now on) */

@@ -188,7 +188,7 @@ int checked_violations();
 int checked_selftest(cudaStream_t s);          // NKB_CHECKED_SELFTEST=1: one failing check
 int fused_node_prog(const FusedParams& p);   // K1g + 16 x K1s node program (graph key)
 int stream_prog_of(const FusedParams& p);    // K1s node program
-int surface_pass_of(const FusedParams& p);     // 0 K1, 1 K1s (stream.cu), 2 K1g (two CTAs per SM)
+int surface_pass_of(const FusedParams& p);     // 0 K1, 1 K1s (stream.cu), 2 K1g (2-3 CTAs per SM)
 int fused_grid_for(const FusedParams& p, int64_t n_elements);   // triangle regions of that pass
 int launch_stream(const FusedParams& p, int grid, cudaStream_t s);
 int launch_stream_prepare();
