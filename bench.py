@@ -677,7 +677,9 @@ def next_rows(ctx, da, case, hcase, hbm_gbs, pipe=None):
         npts = case.n_points
         res["dssum"] = {"setup_ms": setup * 1e3, "ms": ms, "points": npts,
                         "gb_per_s_field": 16 * npts / ms / 1e6,
-                        "note": "in-place average of one f64 field: read + write 8 B/pt, plus the sorted index"}
+                        "frac_of_hbm": 16 * npts / ms / 1e6 / hbm_gbs,
+                        "kernel": "gs_avg_kernel: runs grouped by copy count, one launch",
+                        "note": "in-place average of one f64 field: read + write 8 B/pt (algorithmic)"}
         from dataclasses import replace as _rep
 
         if pipe is not None:

@@ -4,6 +4,7 @@
 // orchestration over NCCL.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <nccl.h>
 #include <string.h>
 
@@ -316,8 +317,9 @@ int nkb_transit_gather(nkb_ctx* ctx, int root, void* stream) {
 namespace nkb {
 int gs_apply(nkb_ctx* ctx, double* field, cudaStream_t s) {
   GsLocal& g = ctx->gs;
-  NKB_TRY(gs_sum(g, field, s));
   const int R = (ctx->comm && ctx->nranks > 1) ? ctx->nranks : 1;
+  if (R == 1 && !getenv("NKB_DSSUM_TWO_PASS")) return gs_average_local(g, field, s);
+  NKB_TRY(gs_sum(g, field, s));
   if (R > 1 && g.n_shared > 0) {
     for (int q = 0; q < R; ++q) NKB_TRY(gs_pack(g, q, s));
     NKB_NCCL(g_nccl.GroupStart());

@@ -16,6 +16,14 @@
 // increasing gid order.  Per call: sum kernel -> pack/exchange partials with
 // the neighbour ranks (grouped ncclSend/Recv, in abi.cu) -> combine in rank
 // order -> scatter.
+//
+// One rank (gs_average_local): the runs are regrouped once by copy count.
+// Runs of K = 2..kGroupMax copies are stored per K as K structure-of-arrays
+// rows of local indices (row j = every run's j-th copy, runs in gid order),
+// so one thread averages one run with K coalesced index loads, K independent
+// gathers, a left fold and K stores; single-copy runs are never touched
+// (v / 1 == v) and longer runs go through the CSR.  One launch covers every
+// group.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -30,6 +38,97 @@ inline unsigned grid_for(long long n, int threads) {
   if (b < 1) b = 1;
   if (b > 148 * 32) b = 148 * 32;
   return (unsigned)b;
+}
+
+constexpr int kRunBlock = 256;
+
+__global__ void run_key_kernel(const int* cnt, long long U, unsigned char* key, int* u_of, int* hist) {
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < U; u += (long long)gridDim.x * blockDim.x) {
+    const int c = cnt[u];
+    const int k = c > kGroupMax ? kGroupMax + 1 : c;
+    key[u] = (unsigned char)k;
+    u_of[u] = (int)u;
+    atomicAdd(&hist[k], 1);
+  }
+}
+
+// sorted run p (stable by key): run u = order[p] of K = key copies -> its group rows
+__global__ void run_fill_kernel(const unsigned char* key, const int* order, long long U, const int* idx,
+                                const int* off, GsGroups gr, int* lrun) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < U; p += (long long)gridDim.x * blockDim.x) {
+    const int k = key[p], u = order[p];
+    if (k < 2) continue;
+    const long long r = p - gr.first[k];
+    if (k > kGroupMax) {
+      lrun[r] = u;
+      continue;
+    }
+    int* rows = gr.idx + gr.base[k];
+    for (int j = 0; j < k; ++j) rows[(long long)j * gr.n[k] + r] = idx[off[u] + j];
+  }
+}
+
+// runs per thread for K copies: about eight gathers in flight per thread
+__host__ __device__ constexpr int runs_per_thread(int k) { return k <= 2 ? 4 : k <= 4 ? 2 : 1; }
+
+// runs r0 + i * kRunBlock (i < R) of group K: every index load, then every
+// gather, issued before the first use
+template <int K>
+__device__ __forceinline__ void avg_runs(double* __restrict__ v, const int* __restrict__ rows, long long nk,
+                                         long long r0) {
+  constexpr int R = runs_per_thread(K);
+  int id[R][K];
+  double x[R][K];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const long long r = r0 + (long long)i * kRunBlock;
+      id[i][j] = r < nk ? __ldg(rows + j * nk + r) : -1;
+    }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) x[i][j] = id[i][j] >= 0 ? v[id[i][j]] : 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    double t = x[i][0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) t = __dadd_rn(t, x[i][j]);
+    const double a = __ddiv_rn(t, (double)K);
+    if (id[i][0] >= 0)
+#pragma unroll
+      for (int j = 0; j < K; ++j) v[id[i][j]] = a;
+  }
+}
+
+// block b belongs to group k with gr.block[k] <= b < gr.block[k+1]; k = kGroupMax + 1: CSR runs
+__global__ void __launch_bounds__(kRunBlock) gs_avg_kernel(double* __restrict__ v, GsGroups gr,
+                                                           const int* __restrict__ lrun, const int* __restrict__ idx,
+                                                           const int* __restrict__ off) {
+  const int b = blockIdx.x;
+  int k = 2;
+#pragma unroll
+  for (int q = 3; q <= kGroupMax + 1; ++q) k += b >= gr.block[q];
+  const long long r = (long long)(b - gr.block[k]) * kRunBlock * runs_per_thread(k) + threadIdx.x;
+  if (r >= gr.n[k]) return;
+  const int* rows = gr.idx + (k <= kGroupMax ? gr.base[k < kGroupMax ? k : kGroupMax] : 0);
+  switch (k) {
+    case 2: avg_runs<2>(v, rows, gr.n[2], r); break;
+    case 3: avg_runs<3>(v, rows, gr.n[3], r); break;
+    case 4: avg_runs<4>(v, rows, gr.n[4], r); break;
+    case 5: avg_runs<5>(v, rows, gr.n[5], r); break;
+    case 6: avg_runs<6>(v, rows, gr.n[6], r); break;
+    case 7: avg_runs<7>(v, rows, gr.n[7], r); break;
+    case 8: avg_runs<8>(v, rows, gr.n[8], r); break;
+    default: {
+      const int u = lrun[r], a = off[u], e = off[u + 1];
+      double t = v[idx[a]];
+      for (int j = a + 1; j < e; ++j) t = __dadd_rn(t, v[idx[j]]);
+      const double m = __ddiv_rn(t, (double)(e - a));
+      for (int j = a; j < e; ++j) v[idx[j]] = m;
+    }
+  }
 }
 
 __global__ void iota_kernel(int* v, long long n) {
@@ -156,6 +255,7 @@ int gs_build_local(const long long* gid, long long n, GsLocal& g, cudaStream_t s
   NKB_CUDA(cudaMemcpyAsync(g.off + g.U, &nn, sizeof(int), cudaMemcpyHostToDevice, s));
   count_kernel<<<grid_for(g.U, 256), 256, 0, s>>>(g.off, g.U, g.mult);
   NKB_CUDA(cudaGetLastError());
+  NKB_TRY(gs_build_groups(g, s));
   NKB_CUDA(cudaFreeAsync(kout, s));
   NKB_CUDA(cudaFreeAsync(iota, s));
   NKB_CUDA(cudaFreeAsync(head, s));
@@ -165,7 +265,68 @@ int gs_build_local(const long long* gid, long long n, GsLocal& g, cudaStream_t s
   return NKB_OK;
 }
 
+// regroup the runs by copy count for the one-rank kernel (see the header)
+int gs_build_groups(GsLocal& g, cudaStream_t s) {
+  GsGroups& gr = g.groups;
+  gr = GsGroups();
+  if (g.U == 0) return NKB_OK;
+  unsigned char *key = nullptr, *key_s = nullptr;
+  int *u_of = nullptr, *order = nullptr, *hist = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  NKB_CUDA(cudaMallocAsync(&key, g.U, s));
+  NKB_CUDA(cudaMallocAsync(&key_s, g.U, s));
+  NKB_CUDA(cudaMallocAsync(&u_of, sizeof(int) * g.U, s));
+  NKB_CUDA(cudaMallocAsync(&order, sizeof(int) * g.U, s));
+  NKB_CUDA(cudaMallocAsync(&hist, sizeof(int) * (kGroupMax + 2), s));
+  NKB_CUDA(cudaMemsetAsync(hist, 0, sizeof(int) * (kGroupMax + 2), s));
+  run_key_kernel<<<grid_for(g.U, 256), 256, 0, s>>>(g.mult, g.U, key, u_of, hist);
+  NKB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key_s, u_of, order, (int)g.U, 0, 4, s));
+  NKB_CUDA(cudaMallocAsync(&tmp, tb, s));
+  NKB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key_s, u_of, order, (int)g.U, 0, 4, s));  // stable
+  int h[kGroupMax + 2];
+  NKB_CUDA(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, s));
+  NKB_CUDA(cudaStreamSynchronize(s));
+  long long first = 0, base = 0, blocks = 0;
+  for (int k = 0; k <= kGroupMax + 1; ++k) {
+    gr.first[k] = first;
+    gr.n[k] = h[k];
+    first += h[k];
+    if (k >= 2) {
+      gr.block[k] = (int)blocks;
+      const long long per = (long long)kRunBlock * runs_per_thread(k);
+      blocks += (h[k] + per - 1) / per;
+      if (k <= kGroupMax) {
+        gr.base[k] = base;
+        base += (long long)k * h[k];
+      }
+    }
+  }
+  if (blocks > 0x7fffffffLL) return fail(NKB_EINVAL, "too many shared GLL nodes for one rank");
+  gr.blocks = (int)blocks;
+  if (base) NKB_CUDA(cudaMalloc(&gr.idx, sizeof(int) * base));
+  if (h[kGroupMax + 1]) NKB_CUDA(cudaMalloc(&g.lrun, sizeof(int) * h[kGroupMax + 1]));
+  run_fill_kernel<<<grid_for(g.U, 256), 256, 0, s>>>(key_s, order, g.U, g.idx, g.off, gr, g.lrun);
+  NKB_CUDA(cudaGetLastError());
+  NKB_CUDA(cudaFreeAsync(key, s));
+  NKB_CUDA(cudaFreeAsync(key_s, s));
+  NKB_CUDA(cudaFreeAsync(u_of, s));
+  NKB_CUDA(cudaFreeAsync(order, s));
+  NKB_CUDA(cudaFreeAsync(hist, s));
+  NKB_CUDA(cudaFreeAsync(tmp, s));
+  return NKB_OK;
+}
+
+int gs_average_local(const GsLocal& g, double* v, cudaStream_t s) {
+  if (g.groups.blocks == 0) return NKB_OK;
+  gs_avg_kernel<<<g.groups.blocks, kRunBlock, 0, s>>>(v, g.groups, g.lrun, g.idx, g.off);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
 void gs_free(GsLocal& g) {
+  cudaFree(g.groups.idx);
+  cudaFree(g.lrun);
   cudaFree(g.idx);
   cudaFree(g.off);
   cudaFree(g.ugid);

@@ -261,6 +261,15 @@ int launch_be_cells(int64_t ncells, void* out, cudaStream_t s);
 int launch_be_types(int64_t ncells, void* out, cudaStream_t s);
 int launch_bswap64(void* p, int64_t n, cudaStream_t s);
 // ---- dssum.cu: gather-scatter (direct stiffness summation) ----
+constexpr int kGroupMax = 8;          // one-rank DSSUM: runs of 2..8 copies grouped by count
+struct GsGroups {                     // (kernel parameter: passed by value)
+  int* idx = nullptr;                 // per K: K rows of n[K] local indices (SoA) at base[K]
+  long long base[kGroupMax + 1] = {};
+  long long n[kGroupMax + 2] = {};    // runs per copy count; [kGroupMax + 1] = longer runs (CSR)
+  long long first[kGroupMax + 2] = {};  // first position of count k in the count-sorted run order
+  int block[kGroupMax + 2] = {};      // first block of each group (k >= 2)
+  int blocks = 0;
+};
 struct GsLocal {
   long long n = 0, U = 0;            // local GLL copies, unique global ids
   int* idx = nullptr;                // [n] local indices sorted by gid (stable)
@@ -268,6 +277,8 @@ struct GsLocal {
   long long* ugid = nullptr;         // [U] sorted unique gids
   int* mult = nullptr;               // [U] copies over all ranks
   double* part = nullptr;            // [U] partial / total sums
+  GsGroups groups;                   // one rank: runs grouped by copy count
+  int* lrun = nullptr;               // runs longer than kGroupMax (unique indices)
   // shared with other ranks (multi-rank only)
   int n_shared = 0;
   int* su = nullptr;                 // [n_shared] unique index of each shared gid (increasing gid)
@@ -282,6 +293,8 @@ struct GsLocal {
 int gs_build_local(const long long* gid, long long n, GsLocal& g, cudaStream_t s);
 void gs_free(GsLocal& g);
 int gs_sum(const GsLocal& g, const double* v, cudaStream_t s);
+int gs_build_groups(GsLocal& g, cudaStream_t s);
+int gs_average_local(const GsLocal& g, double* v, cudaStream_t s);   // one rank: sum + scatter in one pass
 int gs_pack(const GsLocal& g, int q, cudaStream_t s);
 int gs_combine(const GsLocal& g, int R, int me, cudaStream_t s);
 int gs_scatter(const GsLocal& g, double* v, cudaStream_t s);

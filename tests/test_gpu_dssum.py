@@ -76,3 +76,48 @@ def test_continuous_pipeline_equals_oracle_on_averaged_q(ctx):
     InsituAnalysis(Pipeline(**{**pipe.__dict__, "continuous": False})).execute(da)
     gt2 = ctx.triangles()
     assert len(gt2) != len(gt) or not np.array_equal(gt2.view(np.uint32), gt.view(np.uint32))
+
+
+def _irregular_ids(n, rng):
+    """Global ids with runs of 1..12 copies, some far longer (serial path of the
+    one-pass kernel), scattered over the local positions."""
+    lens = list(rng.integers(1, 13, size=n))
+    lens[3] = 40
+    lens[10] = 300
+    ids = np.repeat(np.arange(len(lens), dtype=np.int64), lens)[:n]
+    rng.shuffle(ids)
+    return ids * 7 + 3                       # sparse, non-contiguous ids
+
+
+@pytest.mark.parametrize("two_pass", [False, True])
+@pytest.mark.parametrize("kind", ["irregular", "one_id", "all_distinct", "pairs_on_warp_edges"])
+def test_dssum_irregular_runs_match_oracle(ctx, monkeypatch, kind, two_pass):
+    """One-rank DSSUM (one-pass warp kernel, and the two-pass sum/scatter
+    kernels) on id layouts that stress the warp windows: runs of 1..300
+    copies in random positions, a single id shared by every copy, no sharing
+    at all, and pairs straddling every warp boundary."""
+    import torch
+
+    if two_pass:
+        monkeypatch.setenv("NKB_DSSUM_TWO_PASS", "1")
+    case = synth.box(nel=(3, 2, 2))
+    n = case.n_points
+    rng = np.random.default_rng(7)
+    if kind == "irregular":
+        gid = _irregular_ids(n, rng)
+    elif kind == "one_id":
+        gid = np.full(n, 5, dtype=np.int64)
+    elif kind == "all_distinct":
+        gid = rng.permutation(n).astype(np.int64)
+    else:
+        gid = (np.arange(n, dtype=np.int64) + 1) // 2      # runs [0], [1,2], [3,4], ...: every 32nd pair splits
+    da = SemDataAdaptor(ctx)
+    da.initialize(_snapshot(case, gid=False))
+    ctx.mesh_set_global_ids(torch.from_numpy(gid).cuda())
+    v = rng.standard_normal(n)
+    d = DeviceArray.empty(ctx, (n,), np.float64)
+    d.upload(v)
+    ctx.dssum(d)
+    got = d.to_host()
+    exp = O.dssum(gid, v)
+    assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
