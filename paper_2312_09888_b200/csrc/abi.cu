@@ -76,6 +76,7 @@ using namespace nkb;
 
 
 static void p2p_release(nkb_ctx* ctx) {
+  if (ctx->comp_stream) cudaStreamSynchronize(ctx->comp_stream);   // composite halves still reading the buffers
   for (void* q : ctx->p2p.opened) cudaIpcCloseMemHandle(q);
   ctx->p2p.opened.clear();
   cudaFree(ctx->p2p.keys[0]);
@@ -95,6 +96,12 @@ static void p2p_release(nkb_ctx* ctx) {
     if (ctx->graph_exec[k]) cudaGraphExecDestroy(ctx->graph_exec[k]);
     ctx->graph_exec[k] = nullptr;
     ctx->graph_key[k].clear();
+    if (ctx->graph_exec_a[k]) cudaGraphExecDestroy(ctx->graph_exec_a[k]);
+    ctx->graph_exec_a[k] = nullptr;
+    ctx->graph_key_a[k].clear();
+    if (ctx->graph_exec_b[k]) cudaGraphExecDestroy(ctx->graph_exec_b[k]);
+    ctx->graph_exec_b[k] = nullptr;
+    ctx->graph_key_b[k].clear();
   }
 }
 
@@ -115,9 +122,10 @@ static int p2p_setup(nkb_ctx* ctx, int W, int H, cudaStream_t s) {
   NKB_CUDA(cudaMemset(P.flags, 0, 4 * kMaxRanks * sizeof(unsigned long long)));
   NKB_CUDA(cudaMalloc(&P.err, sizeof(int)));
   NKB_CUDA(cudaMemset(P.err, 0, sizeof(int)));
-  NKB_CUDA(cudaMalloc(&P.dev_epoch, sizeof(unsigned long long)));
-  NKB_CUDA(cudaMemset(P.dev_epoch, 0, sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&P.dev_epoch, 3 * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMemset(P.dev_epoch, 0, 3 * sizeof(unsigned long long)));
   NKB_CUDA(cudaMallocHost(&P.h_res, (2 + kMaxRanks) * sizeof(unsigned long long)));
+  memset(P.h_res, 0, (2 + kMaxRanks) * sizeof(unsigned long long));
   NKB_CUDA(cudaHostGetDevicePointer((void**)&P.h_res_dev, P.h_res, 0));
   constexpr int kH = 5;
   cudaIpcMemHandle_t mine[kH];
@@ -246,6 +254,7 @@ int nkb_ctx_create(int cuda_device, nkb_ctx** out) {
   c->ticket = reinterpret_cast<unsigned int*>(c->counters + 4);
   NKB_CUDA(cudaMalloc(&c->range_dev, 2 * sizeof(double)));
   NKB_CUDA(cudaMallocHost(&c->h_counters, (8 + kMaxRegions) * sizeof(unsigned long long)));
+  memset(c->h_counters, 0, (8 + kMaxRegions) * sizeof(unsigned long long));
   NKB_CUDA(cudaHostGetDevicePointer((void**)&c->h_counters_dev, c->h_counters, 0));
   NKB_CUDA(cudaMalloc(&c->region_count, kMaxRegions * sizeof(unsigned long long)));
   for (auto& e : c->ev) NKB_CUDA(cudaEventCreate(&e));
@@ -279,9 +288,16 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
     if (kv.second) stats_tables_free(*kv.second);
   gs_free(ctx->gs);
   cudaFree(ctx->tr_buf);
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 2; ++k) {
     if (ctx->graph_exec[k]) cudaGraphExecDestroy(ctx->graph_exec[k]);
+    if (ctx->graph_exec_a[k]) cudaGraphExecDestroy(ctx->graph_exec_a[k]);
+    if (ctx->graph_exec_b[k]) cudaGraphExecDestroy(ctx->graph_exec_b[k]);
+    if (ctx->ev_a[k]) cudaEventDestroy(ctx->ev_a[k]);
+    if (ctx->ev_b[k]) cudaEventDestroy(ctx->ev_b[k]);
+  }
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->comp_stream) cudaStreamDestroy(ctx->comp_stream);
+  cudaFree(ctx->csnap);
   cudaFree(ctx->dq);
   cudaFree(ctx->dw);
   cudaFree(ctx->rgb_dev);
@@ -765,10 +781,18 @@ static int ensure_tri(nkb_ctx* ctx, int64_t cap, bool meta) {
 // Enqueue one step on stream s (no host synchronisation): memsets -> K1
 // (or count/scan/ordered emit) -> zbuf clear -> raster -> range words ->
 // composite -> resolve -> D2H of the report words.
+// part 3: the whole step on `s`.  P2P steps may be enqueued in two halves
+// (run_step): part 1 = surface pass .. raster .. "keys ready" + the counter
+// report, part 2 = composite .. "done reading" + the range / P2P report on
+// the composite stream; part 2 then reads the step's epoch and counters from
+// their parity slots, which the next step's part 1 does not touch.
 static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm, cudaStream_t s,
-                        bool composite, bool ordered, unsigned long long ep) {
+                        bool composite, bool ordered, unsigned long long ep, int part = 3) {
   const bool timing = p->timing != 0;
   const int64_t npx = (int64_t)p->width * p->height;
+  const bool split = part != 3;
+  const int par = (int)(ep & 1);
+  if (part & 1) {
   fp.tri = ctx->tri;
   fp.meta = p->emit_meta ? ctx->meta : nullptr;
   fp.tri_cap = ctx->tri_cap;
@@ -805,6 +829,7 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     NKB_TRY(launch_fused(fp, s));
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[1], s));
+  }
   const bool p2p = composite && ctx->p2p.ready;
   unsigned long long* zbuf = ctx->zbuf;
   P2PParams pp;
@@ -832,10 +857,23 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     pp.dev_epoch = P.dev_epoch;
     pp.overflow = ctx->counters + 6;
     zbuf = P.keys[ep & 1];
-    NKB_TRY(launch_p2p_epoch(pp, s));                // device epoch := ep
-    // every peer has finished reading this key buffer (epoch ep-2) before it is cleared
-    NKB_TRY(launch_p2p_wait(pp, 1, 2, s));
+    {
+      const char* v = getenv("NKB_COMPOSITE_BULK");         // 0: the per-thread load kernel
+      pp.bulk = !(v && v[0] == '0');
+    }
+    if (split) {
+      if (part == 1) pp.ep_slot = P.dev_epoch + 1 + par;
+      else pp.dev_epoch = P.dev_epoch + 1 + par;
+      if (fp.sm_reserve > 0) pp.max_blocks = 2 * fp.sm_reserve;   // two bulk CTAs (96 KB smem each) per SM
+      pp.bulk = 1;
+    }
+    if (part & 1) {
+      NKB_TRY(launch_p2p_epoch(pp, s));              // device epoch := ep
+      // every peer has finished reading this key buffer (epoch ep-2) before it is cleared
+      NKB_TRY(launch_p2p_wait(pp, 1, 2, s));
+    }
   }
+  if (part & 1) {
   NKB_TRY(launch_zbuf_clear(zbuf, npx, s));
   RasterParams rp;
   rp.tri = ctx->tri;
@@ -855,18 +893,20 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   rp.zbuf = zbuf;
   NKB_TRY(launch_raster(rp, s));
   NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, rp.region_count == ctx->counters ? nullptr : rp.region_count,
-                             rp.n_regions, rp.region_cap, ctx->tri_cap, s));
+                             rp.n_regions, rp.region_cap, ctx->tri_cap, s,
+                             split ? ctx->csnap + 8 * par : nullptr));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[2], s));
-  if (p2p) {
+  if (p2p) NKB_TRY(launch_p2p_signal(pp, 0, nullptr, s));   // "keys ready" (+ this rank's overflow word)
+  if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[6], s));
+  }
+  if (p2p && (part & 2)) {
     // fused sort-last composite + resolve over NVLink peer memory
-    NKB_TRY(launch_p2p_signal(pp, 0, nullptr, s));
-    if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[6], s));
     NKB_TRY(launch_p2p_composite(pp, s));
     if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[7], s));
-    NKB_TRY(launch_p2p_signal(pp, 1, ctx->counters, s));
+    NKB_TRY(launch_p2p_signal(pp, 1, split ? ctx->csnap + 8 * par : ctx->counters, s));
     if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[8], s));
     if (ctx->rank == 0) NKB_TRY(launch_p2p_wait(pp, 1, 0, s));
-  } else if (composite) {
+  } else if (composite && !p2p) {
     NKB_NCCL(g_nccl.GroupStart());
     NKB_NCCL(g_nccl.Reduce(ctx->zbuf, ctx->zbuf, (size_t)npx + 2, ncclUint64, ncclMin, 0, ctx->comm, s));
     NKB_NCCL(g_nccl.AllReduce(ctx->counters, ctx->counters + 3, 1, ncclUint64, ncclSum, ctx->comm, s));
@@ -903,6 +943,7 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   rep.peer_overflow = p2p ? ctx->p2p.flags + 3 * kMaxRanks : nullptr;
   rep.nranks = ctx->nranks;
   rep.h_res = p2p ? ctx->p2p.h_res_dev : nullptr;
+  rep.part = part;
   NKB_TRY(launch_report(rep, s));
   return NKB_OK;
 }
@@ -938,57 +979,179 @@ static int collect_step(nkb_ctx* ctx, bool p2p) {
   return NKB_OK;
 }
 
+// the step's second half on the composite stream (P2P, NKB_COMPOSITE_OVERLAP != 0)
+static bool composite_overlap() {
+  static const bool on = !(getenv("NKB_COMPOSITE_OVERLAP") && strcmp(getenv("NKB_COMPOSITE_OVERLAP"), "0") == 0);
+  return on;
+}
+
+// SMs the surface pass of a split step leaves to the previous step's
+// composite (persistent K1g / K1s grids would otherwise hold every SM)
+static int composite_sms() {
+  static const int n = [] {
+    const char* v = getenv("NKB_COMPOSITE_SMS");
+    return v ? atoi(v) : 4;
+  }();
+  return n;
+}
+
+static int ensure_comp_stream(nkb_ctx* ctx) {
+  if (ctx->comp_stream) return NKB_OK;
+  NKB_CUDA(cudaStreamCreateWithFlags(&ctx->comp_stream, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    NKB_CUDA(cudaEventCreateWithFlags(&ctx->ev_a[k], cudaEventDisableTiming));
+    NKB_CUDA(cudaEventCreateWithFlags(&ctx->ev_b[k], cudaEventDisableTiming));
+  }
+  if (!ctx->csnap) NKB_CUDA(cudaMalloc(&ctx->csnap, 16 * sizeof(unsigned long long)));
+  return NKB_OK;
+}
+
+// order `s` after the last composite half (image, range and report words)
+static int join_composite(nkb_ctx* ctx, cudaStream_t s) {
+  if (ctx->last_b >= 0) NKB_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[ctx->last_b], 0));
+  return NKB_OK;
+}
+
+// NKB_SPLIT_TRACE=1: per-step event times of the two halves of split steps
+// (A start / end on the caller's stream, B start / end on the composite
+// stream), printed to stderr at the next synchronisation
+struct SplitTrace {
+  std::vector<cudaEvent_t> ev;   // 4 per step
+  int n = 0;
+};
+static SplitTrace g_trace;
+static bool split_trace() {
+  static const bool on = getenv("NKB_SPLIT_TRACE") != nullptr;
+  return on;
+}
+static void trace_mark(int k, cudaStream_t s) {
+  const size_t i = (size_t)g_trace.n * 4 + k;
+  while (g_trace.ev.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_trace.ev.push_back(e);
+  }
+  cudaEventRecord(g_trace.ev[i], s);
+}
+static void trace_flush(int rank) {
+  if (g_trace.n == 0) return;
+  float t[4];
+  for (int j = 0; j < g_trace.n; ++j) {
+    for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&t[k], g_trace.ev[0], g_trace.ev[4 * j + k]);
+    fprintf(stderr, "[nkb split rank %d] step %d A %.4f-%.4f B %.4f-%.4f (A %.4f, B %.4f ms)\n", rank, j, t[0], t[1],
+            t[2], t[3], t[1] - t[0], t[3] - t[2]);
+  }
+  g_trace.n = 0;
+}
+
+static int sync_step(nkb_ctx* ctx, cudaStream_t s) {
+  NKB_CUDA(cudaStreamSynchronize(s));
+  if (ctx->last_b >= 0) NKB_CUDA(cudaStreamSynchronize(ctx->comp_stream));
+  if (split_trace()) trace_flush(ctx->rank);
+  return NKB_OK;
+}
+
+// the sticky overflow words the report kernel ORs into (no device work pending)
+static void clear_overflow_words(nkb_ctx* ctx) {
+  ctx->h_counters[6] = ctx->h_counters[7] = 0;
+  if (ctx->p2p.h_res) ctx->p2p.h_res[1 + kMaxRanks] = 0;
+}
+
 static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const Colormap& cm,
                     cudaStream_t s, bool composite, bool ordered, bool sync = true) {
   const bool p2p = composite && ctx->p2p.ready;
+  if (sync) clear_overflow_words(ctx);
   const unsigned long long ep = p2p ? ++ctx->p2p.epoch : 0;   // the device counter follows in-stream
+  const int slot = (int)(ep & 1);
+  // P2P: the composite half of step k runs on ctx->comp_stream while step
+  // k+1's surface pass runs on `s`.  Step k+2 (same parity slots) waits for
+  // step k's composite half; the cross-GPU order stays with the epoch flags.
+  // (stream-ordered steps only: a synchronous step waits for its composite anyway)
+  const bool split = !sync && p2p && composite_overlap() && fp.prof == nullptr && !p->timing;
+  if (split) {
+    fp.sm_reserve = composite_sms();
+    NKB_TRY(ensure_comp_stream(ctx));
+    if (ctx->ev_b_live[slot]) NKB_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[slot], 0));
+  } else {
+    NKB_TRY(join_composite(ctx, s));               // a one-stream step after split ones
+  }
   // Steps replay a CUDA graph of the whole launch sequence (one launch
   // instead of ~10-14), re-captured whenever a parameter changes.  With the
   // P2P composite the epoch lives on the device and only the key-buffer
-  // parity alternates, so two graphs cover every step; the NCCL composite
-  // path stays eager.
+  // parity alternates, so two graphs (two pairs when split) cover every
+  // step; the NCCL composite path stays eager.
   static const bool graphs = !(getenv("NKB_GRAPHS") && strcmp(getenv("NKB_GRAPHS"), "0") == 0);
   // (per-stage timing keeps the eager path: its events bracket the stages)
-  if (graphs && (!composite || p2p) && fp.prof == nullptr && !p->timing) {
-    if (ordered && ctx->elem_cap < ctx->E) {       // (allocation happens outside the capture)
-      cudaFree(ctx->elem_count);
-      cudaFree(ctx->elem_offset);
-      ctx->elem_count = nullptr;
-      ctx->elem_offset = nullptr;
-      NKB_CUDA(cudaMalloc(&ctx->elem_count, sizeof(int) * ctx->E));
-      NKB_CUDA(cudaMalloc(&ctx->elem_offset, sizeof(long long) * ctx->E));
-      ctx->elem_cap = ctx->E;
+  const int parts[2] = {split ? 1 : 3, 2};
+  for (int h = 0; h < (split ? 2 : 1); ++h) {
+    const int part = parts[h];
+    cudaStream_t hs = h == 0 ? s : ctx->comp_stream;
+    if (h == 1) {
+      if (split_trace()) trace_mark(1, s);
+      NKB_CUDA(cudaEventRecord(ctx->ev_a[slot], s));
+      NKB_CUDA(cudaStreamWaitEvent(hs, ctx->ev_a[slot], 0));
+      if (split_trace()) trace_mark(2, hs);
+    } else if (split && split_trace()) {
+      trace_mark(0, s);
     }
-    NKB_TRY(launch_fused_prepare());
-    const int slot = (int)(ep & 1);
-    std::string key = step_key(ctx, p, fp, cm, ordered);
-    if (p2p) {
-      const void* pk[] = {ctx->p2p.keys[0], ctx->p2p.keys[1], ctx->p2p.flags, ctx->p2p.dev_epoch, ctx->p2p.h_res};
-      key.append(reinterpret_cast<const char*>(pk), sizeof(pk));
-      key.push_back((char)slot);
+    if (graphs && (!composite || p2p) && fp.prof == nullptr && !p->timing) {
+      if (ordered && ctx->elem_cap < ctx->E) {       // (allocation happens outside the capture)
+        cudaFree(ctx->elem_count);
+        cudaFree(ctx->elem_offset);
+        ctx->elem_count = nullptr;
+        ctx->elem_offset = nullptr;
+        NKB_CUDA(cudaMalloc(&ctx->elem_count, sizeof(int) * ctx->E));
+        NKB_CUDA(cudaMalloc(&ctx->elem_offset, sizeof(long long) * ctx->E));
+        ctx->elem_cap = ctx->E;
+      }
+      NKB_TRY(launch_fused_prepare());
+      std::string key = step_key(ctx, p, fp, cm, ordered);
+      if (p2p) {
+        const void* pk[] = {ctx->p2p.keys[0], ctx->p2p.keys[1], ctx->p2p.flags, ctx->p2p.dev_epoch, ctx->p2p.h_res,
+                            ctx->csnap};
+        key.append(reinterpret_cast<const char*>(pk), sizeof(pk));
+        key.push_back((char)slot);
+        key.push_back((char)part);
+      }
+      // whole steps, first halves and second halves keep separate graphs
+      // (synchronous and stream-ordered steps alternate without re-capture)
+      cudaGraphExec_t& gx = part == 3 ? ctx->graph_exec[slot] : part == 1 ? ctx->graph_exec_a[slot]
+                                                                          : ctx->graph_exec_b[slot];
+      std::string& gk = part == 3 ? ctx->graph_key[slot] : part == 1 ? ctx->graph_key_a[slot] : ctx->graph_key_b[slot];
+      if (!gx || key != gk) {
+        if (gx) cudaGraphExecDestroy(gx);
+        gx = nullptr;
+        if (!ctx->cap_stream) NKB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+        NKB_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+        const int rc = enqueue_step(ctx, p, fp, cm, ctx->cap_stream, composite, ordered, ep, part);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
+        NKB_TRY(rc);
+        NKB_CUDA(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&gx, g, 0);
+        cudaGraphDestroy(g);
+        NKB_CUDA(ie);
+        gk = key;
+      }
+      NKB_CUDA(cudaGraphLaunch(gx, hs));
+    } else {
+      NKB_TRY(enqueue_step(ctx, p, fp, cm, hs, composite, ordered, ep, part));
     }
-    if (!ctx->graph_exec[slot] || key != ctx->graph_key[slot]) {
-      if (ctx->graph_exec[slot]) cudaGraphExecDestroy(ctx->graph_exec[slot]);
-      ctx->graph_exec[slot] = nullptr;
-      if (!ctx->cap_stream) NKB_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
-      NKB_CUDA(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
-      const int rc = enqueue_step(ctx, p, fp, cm, ctx->cap_stream, composite, ordered, ep);
-      cudaGraph_t g = nullptr;
-      const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &g);
-      NKB_TRY(rc);
-      NKB_CUDA(ce);
-      const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec[slot], g, 0);
-      cudaGraphDestroy(g);
-      NKB_CUDA(ie);
-      ctx->graph_key[slot] = key;
+  }
+  if (split) {
+    if (split_trace()) {
+      trace_mark(3, ctx->comp_stream);
+      ++g_trace.n;
     }
-    NKB_CUDA(cudaGraphLaunch(ctx->graph_exec[slot], s));
+    NKB_CUDA(cudaEventRecord(ctx->ev_b[slot], ctx->comp_stream));
+    ctx->ev_b_live[slot] = true;
+    ctx->last_b = slot;
   } else {
-    NKB_TRY(enqueue_step(ctx, p, fp, cm, s, composite, ordered, ep));
+    ctx->last_b = -1;
   }
   ctx->last_fast = !ordered;
   if (!sync) return NKB_OK;                        // stream-ordered (nkb_execute_async): collected at the wait
-  NKB_CUDA(cudaStreamSynchronize(s));
+  NKB_TRY(sync_step(ctx, s));
   return collect_step(ctx, p2p);
 }
 
@@ -1237,12 +1400,11 @@ int nkb_execute_async(nkb_ctx* ctx, const nkb_pipeline* p, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (!p) return fail(NKB_EINVAL, "null pipeline");
   if (p->timing) return fail(NKB_EINVAL, "nkb_execute_async: pipeline.timing must be 0 (use nkb_execute)");
-  if (ctx && ctx->async_pending) {
-    // the previous step's report is dropped: collect its P2P status first
-    NKB_CUDA(cudaStreamSynchronize(s));
-    NKB_TRY(collect_step(ctx, ctx->async_composite && ctx->p2p.ready));
-    ctx->async_pending = false;
-  }
+  // No host synchronisation with a step still pending: its report is
+  // superseded, while its overflow and P2P timeout words stay sticky until
+  // nkb_execute_wait reports them.  The first step of a sequence starts
+  // from clear overflow words (nothing is in flight then).
+  if (ctx && !ctx->async_pending && ctx->h_counters) clear_overflow_words(ctx);
   StepPlan plan;
   NKB_TRY(prepare_step(ctx, p, s, plan));
   NKB_TRY(run_step(ctx, p, plan.fp, plan.cm, s, plan.composite, plan.ordered, false));
@@ -1259,13 +1421,14 @@ int nkb_execute_wait(nkb_ctx* ctx, nkb_report* out, void* stream) {
   NKB_TRY(ctx_check(ctx));
   if (!ctx->async_pending) return fail(NKB_ESTATE, "nkb_execute_wait without a pending nkb_execute_async");
   cudaStream_t s = (cudaStream_t)stream;
-  NKB_CUDA(cudaStreamSynchronize(s));
+  NKB_TRY(sync_step(ctx, s));
   ctx->async_pending = false;
   const bool composite = ctx->async_composite;
   NKB_TRY(collect_step(ctx, composite && ctx->p2p.ready));
   const bool own_over = ctx->h_counters[6] != 0;
   bool any_over = own_over;
   if (composite) any_over = ctx->p2p.ready ? ctx->p2p.h_res[1 + kMaxRanks] != 0 : ctx->h_counters[7] != 0;
+  clear_overflow_words(ctx);
   if (own_over) {                                  // grow for the next steps (this one stays incomplete)
     const int64_t need = needed_capacity(ctx, ctx->async_ordered);
     NKB_TRY(ensure_tri(ctx, std::max(need + need / 4 + 1024 * ctx->n_regions, ctx->tri_cap + ctx->tri_cap / 4),
@@ -1339,6 +1502,10 @@ int nkb_composite_partitions(nkb_ctx* root, nkb_ctx* const* parts, int n, const 
   pp.root_depth = root->depth;
   pp.range_out = root->range_dev;
   pp.err = err;
+  {
+    const char* v = getenv("NKB_COMPOSITE_BULK");           // 0: the per-thread load kernel
+    pp.bulk = !(v && v[0] == '0');
+  }
   pp.dev_epoch = flags + 4 * kMaxRanks;
   int rc = NKB_OK;
   for (int r = 0; r < n && rc == NKB_OK; ++r) {   // each "rank" resolves its band of rows
@@ -1374,6 +1541,7 @@ int nkb_image_copy(nkb_ctx* ctx, unsigned char* rgba, float* depth, void* stream
   if (!ctx->image_valid) return fail(NKB_ESTATE, "no image (execute not run, or not the composite root)");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npx = (size_t)ctx->W * ctx->H;
+  NKB_TRY(join_composite(ctx, s));
   if (rgba) NKB_CUDA(cudaMemcpyAsync(rgba, ctx->rgba, npx * 4, cudaMemcpyDeviceToHost, s));
   if (depth) NKB_CUDA(cudaMemcpyAsync(depth, ctx->depth, npx * sizeof(float), cudaMemcpyDeviceToHost, s));
   NKB_CUDA(cudaStreamSynchronize(s));
@@ -1400,6 +1568,7 @@ int nkb_image_ppm(nkb_ctx* ctx, const unsigned char** ppm, int64_t* nbytes, void
     ctx->ppm_cap = total;
   }
   memcpy(ctx->h_ppm, hdr, hn);
+  NKB_TRY(join_composite(ctx, s));
   NKB_TRY(launch_pack_rgb(ctx->rgba, ctx->rgb_dev, npx, s));
   NKB_CUDA(cudaMemcpyAsync(ctx->h_ppm + hn, ctx->rgb_dev, (size_t)(3 * npx), cudaMemcpyDeviceToHost, s));
   NKB_CUDA(cudaStreamSynchronize(s));
@@ -1491,6 +1660,7 @@ int nkb_render_structured(nkb_ctx* ctx, int n_blocks, const double* const* value
   if (width < 1 || height < 1) return fail(NKB_EINVAL, "image size must be positive");
   if (!rgb_out) return fail(NKB_EINVAL, "null output");
   cudaStream_t s = (cudaStream_t)stream;
+  NKB_TRY(join_composite(ctx, s));                // a composite half may still write the image / range
   if (ctx->s_cap < n_blocks) {
     cudaFree(ctx->s_ptrs);
     cudaFree(ctx->s_col0);

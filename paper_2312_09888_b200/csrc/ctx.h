@@ -152,6 +152,16 @@ struct nkb_ctx {
   cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};   // captured steps (by key-buffer parity)
   std::string graph_key[2];
   cudaStream_t cap_stream = nullptr;
+  // P2P steps in two halves (run_step): A = surface pass .. raster .. "keys
+  // ready" on the caller's stream, B = composite .. report on comp_stream,
+  // so step k's composite overlaps step k+1's surface pass
+  cudaStream_t comp_stream = nullptr;
+  cudaEvent_t ev_a[2] = {}, ev_b[2] = {};    // by key-buffer parity
+  bool ev_b_live[2] = {false, false};
+  int last_b = -1;                           // parity of the last B enqueued (image / range writer)
+  cudaGraphExec_t graph_exec_a[2] = {nullptr, nullptr}, graph_exec_b[2] = {nullptr, nullptr};
+  std::string graph_key_a[2], graph_key_b[2];
+  unsigned long long* csnap = nullptr;       // [2][8] counters of the step, by parity (range_words_kernel)
   double* dq = nullptr;                      // continuous pipeline: DSSUM'd Q / |w| scratch
   double* dw = nullptr;
   int64_t dcap = 0;
@@ -168,7 +178,7 @@ struct nkb_ctx {
     unsigned char* root_rgba = nullptr;
     float* root_depth = nullptr;
     unsigned long long epoch = 0;            // host copy of the step epoch
-    unsigned long long* dev_epoch = nullptr; // device counter read by the P2P kernels
+    unsigned long long* dev_epoch = nullptr; // [0] device counter, [1 + parity] the composite stream's copy
     unsigned long long* h_res = nullptr;     // pinned: [0] timeout flag, [1..] per-rank triangles
     unsigned long long* h_res_dev = nullptr; // its mapped device pointer (report_kernel writes it)
   } p2p;

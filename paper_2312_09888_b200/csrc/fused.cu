@@ -795,14 +795,14 @@ __global__ void __launch_bounds__(1024) count_scan_kernel(const int* __restrict_
 
 static int g_num_sms = 0;
 
-int fused_grid(int64_t n_elements) {
+int fused_grid(int64_t n_elements, int sm_reserve) {
   if (g_num_sms <= 0) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       g_num_sms = 148;
   }
-  int64_t g = g_num_sms;
+  int64_t g = g_num_sms - (sm_reserve > 0 && sm_reserve < g_num_sms / 2 ? sm_reserve : 0);
   if (g > n_elements) g = n_elements;
   return (int)(g < 1 ? 1 : g);
 }
@@ -1621,9 +1621,9 @@ int surface_pass_of(const FusedParams& p) {
 
 // triangle regions (CTAs) of the pass that runs `p`
 int fused_grid_for(const FusedParams& p, int64_t n_elements) {
-  const int g = fused_grid(n_elements);                 // min(E, SMs)
+  const int g = fused_grid(n_elements, p.sm_reserve);   // min(E, SMs - reserved)
   if (surface_pass_of(p) != 2) return g;
-  const int64_t g2 = (int64_t)fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0, prog_uses(node_prog_of(p), NK_U)) * g_num_sms;
+  const int64_t g2 = (int64_t)fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0, prog_uses(node_prog_of(p), NK_U)) * fused_grid(1LL << 40, p.sm_reserve);
   return (int)(n_elements < g2 ? (n_elements < 1 ? 1 : n_elements) : g2);
 }
 
@@ -1655,7 +1655,7 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
                                             "scalars exceed 8)");
   const size_t shm = fused_smem_bytes(nin);
   NKB_TRY(launch_fused_prepare());
-  const int grid = fused_grid(p.n_elements);
+  const int grid = fused_grid(p.n_elements, p.sm_reserve);
   const unsigned gx = (unsigned)grid;
   const int pass = surface_pass_of(p);
   if (pass == 1) return launch_stream(p, grid, s);

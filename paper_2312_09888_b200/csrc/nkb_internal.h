@@ -96,6 +96,7 @@ struct FusedParams {
   const double* geo;                // optional geometry cache d(r,s,t)/d(x,y,z): [E][9][512] (full)
   int geo_compact;                  // 1: geo is the compact layout [E][kGeoCompactDoubles]
   unsigned long long* prof;         // debug: [role 3][phase 6] cycle sums (NKB_PROFILE_PHASES=1)
+  int sm_reserve;                   // SMs the surface pass leaves free (the previous step's composite)
 };
 enum FusedMode : int { FUSED_FAST = 0, FUSED_COUNT = 1, FUSED_ORDERED = 2 };
 
@@ -132,8 +133,12 @@ struct P2PParams {
   unsigned char* root_rgba;                           // rank 0's image (IPC-mapped)
   float* root_depth;
   double* range_out;                                  // local [2]
+  int max_blocks = 0;                                 // composite grid cap (0: fill the GPU)
+  int bulk = 0;                                       // 1: bulk-copy (TMA) composite kernel
   int* err;                                           // local: 1 = peer timeout
   unsigned long long* dev_epoch;                      // local: step epoch (device counter, graph-safe)
+  unsigned long long* ep_slot = nullptr;              // epoch_kernel also stores the new epoch here: the
+                                                      // parity slot the composite stream's kernels read
 };
 // the epoch lives on the device, so a step's launches are identical every
 // step (CUDA-graph replayable); only the key-buffer parity alternates
@@ -155,6 +160,7 @@ struct ReportParams {
   int nranks;
   unsigned long long* h_res;                // P2P host words [0] timeout, [1..kMaxRanks] counts,
                                             // [1+kMaxRanks] any rank overflowed; or null
+  int part = 3;                             // 1: counters + regions, 2: range + P2P words, 3: both
 };
 int launch_report(const ReportParams& p, cudaStream_t s);
 
@@ -173,7 +179,7 @@ struct ResolveParams {
 
 // ---- kernel launchers (defined in .cu files) --------------------------------
 int set_dmat_constant(const double* dmat);
-int fused_grid(int64_t n_elements);       // CTAs (= triangle regions) of launch_fused
+int fused_grid(int64_t n_elements, int sm_reserve = 0);       // CTAs (= triangle regions) of launch_fused
 int launch_fused(const FusedParams& p, cudaStream_t s);
 int launch_fused_prepare();
 // K1s (stream.cu): pipelines without a velocity gradient (no exports, fields
@@ -206,7 +212,7 @@ int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
 int launch_raster(const RasterParams& p, cudaStream_t s);
 int launch_range_words(unsigned long long* counters, unsigned long long* words,
                        const unsigned long long* region_count, int n_regions, int64_t region_cap, int64_t tri_cap,
-                       cudaStream_t s);
+                       cudaStream_t s, unsigned long long* snap = nullptr);   // snap: copy of counters[0..7]
 int launch_resolve(const ResolveParams& p, cudaStream_t s);
 // ---- stats.cu: numpy-exact min / max / mean ----
 constexpr long long kChunk = 32768;      // values per CTA subtree (<= 640 leaves of 57..128)

@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
 // whether the step must grow and re-run.
 __global__ void __launch_bounds__(256) range_words_kernel(unsigned long long* counters, unsigned long long* words,
                                                           const unsigned long long* region_count, int n_regions,
-                                                          long long region_cap, long long tri_cap) {
+                                                          long long region_cap, long long tri_cap,
+                                                          unsigned long long* snap) {
   __shared__ int s_over;
   if (threadIdx.x == 0) {
     words[0] = counters[1];
@@ -68,24 +69,34 @@ __global__ void __launch_bounds__(256) range_words_kernel(unsigned long long* co
   }
   if (over) s_over = 1;
   __syncthreads();
-  if (threadIdx.x == 0) counters[6] = (unsigned long long)s_over;
+  if (threadIdx.x == 0) {
+    counters[6] = (unsigned long long)s_over;
+    // the step's counters for the composite stream (the next step resets them meanwhile)
+    if (snap)
+      for (int i = 0; i < 8; ++i) snap[i] = i == 6 ? (unsigned long long)s_over : counters[i];
+  }
 }
 
 // the step's report words straight into mapped pinned host memory: one
 // kernel instead of 3-5 small D2H copies at the tail of every step
 __global__ void __launch_bounds__(256) report_kernel(const ReportParams p) {
   const int t = threadIdx.x;
-  if (t < 4 || t == 6 || t == 7) p.h_counters[t] = p.counters[t];
+  if (p.part & 1) {
+    if (t < 4) p.h_counters[t] = p.counters[t];
+    // overflow words are sticky across stream-ordered steps: the host clears them
+    if (t == 6 || t == 7) p.h_counters[t] |= p.counters[t];
+    if (p.region_count)
+      for (int i = t; i < p.n_regions; i += blockDim.x) p.h_counters[8 + i] = p.region_count[i];
+  }
+  if (!(p.part & 2)) return;
   if (t == 4 || t == 5) p.h_counters[t] = (unsigned long long)__double_as_longlong(p.range[t - 4]);
-  if (p.region_count)
-    for (int i = t; i < p.n_regions; i += blockDim.x) p.h_counters[8 + i] = p.region_count[i];
   if (p.h_res) {
     if (t == 0) p.h_res[0] = (unsigned long long)(unsigned)*p.err;
     if (t < kMaxRanks) p.h_res[1 + t] = *(volatile const unsigned long long*)(p.peer_counts + t);
     if (t == 32) {      // any rank overflowed (its flag was written before its "keys ready" release)
       unsigned long long any = 0;
       for (int q = 0; q < p.nranks; ++q) any |= *(volatile const unsigned long long*)(p.peer_overflow + q);
-      p.h_res[1 + kMaxRanks] = any;
+      p.h_res[1 + kMaxRanks] |= any;                 // sticky, like h_counters[6..7]
     }
   }
 }
@@ -248,9 +259,9 @@ int launch_raster(const RasterParams& p, cudaStream_t s) {
 
 int launch_range_words(unsigned long long* counters, unsigned long long* words,
                        const unsigned long long* region_count, int n_regions, int64_t region_cap, int64_t tri_cap,
-                       cudaStream_t s) {
+                       cudaStream_t s, unsigned long long* snap) {
   range_words_kernel<<<1, 256, 0, s>>>(counters, words, region_count, n_regions, (long long)region_cap,
-                                       (long long)tri_cap);
+                                       (long long)tri_cap, snap);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

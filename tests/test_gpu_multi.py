@@ -45,6 +45,25 @@ def _image(rank, size, out_dir, steps=3, cuts=None, reran_out=None):
     params = {**c.params, "width": str(W), "height": str(H)}
     an = InsituAnalysis(pipeline_from_params(params))
     reran = []
+    if os.environ.get("NKB_TEST_ASYNC") == "over":
+        # rank 0 starts too small: every step of the first stream-ordered
+        # sequence overflows there; the sticky overflow word reaches the wait
+        # on every rank, the buffer grows, and the next sequence is complete
+        for _ in range(steps + 2):
+            an.execute_async(da)
+        rep = an.wait()
+        assert rep.overflowed
+        for _ in range(steps + 2):
+            an.execute_async(da)
+        rep = an.wait()
+        assert not rep.overflowed
+        if rank == 0:
+            rgba, dep = ctx.image(W, H, depth=True)
+            np.savez(os.path.join(out_dir, f"g{size}.npz"), rgba=rgba, dep=dep, n=rep.n_triangles_global,
+                     rng=np.array(rep.range))
+        dist.barrier()
+        comm.close()
+        return
     if os.environ.get("NKB_TEST_ASYNC") == "1":
         an.execute(da)                    # size the triangle buffers (synchronous, may re-run)
         for _ in range(steps + 2):        # stream-ordered steps: device-side ordering across ranks only
@@ -138,6 +157,24 @@ def test_async_steps_composite_equals_single_gpu(tmp_path, mode, monkeypatch):
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
+    assert np.array_equal(a["rgba"], b["rgba"])
+    assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_async_overflow_is_reported_at_the_wait(tmp_path, mode, monkeypatch):
+    """Stream-ordered steps that overflow on rank 0 only: the overflow is
+    sticky until nkb_execute_wait, which reports it on both ranks; the next
+    sequence (grown buffer) equals the one-GPU image."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
+    monkeypatch.setenv("NKB_TEST_ASYNC", "over")
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode, None, 64), nprocs=2, join=True)
+    a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
+    assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rgba"], b["rgba"])
     assert np.array_equal(a["dep"].view(np.uint32), b["dep"].view(np.uint32))
 

@@ -1,4 +1,5 @@
-"""R16 on ONE GPU: the sort-last composite kernel (p2p_composite_kernel) over
+"""R16 on ONE GPU: the sort-last composite kernels (p2p_composite_bulk_kernel,
+the default, and p2p_composite_kernel) over
 R in-process partition contexts, each owning a contiguous element range of
 the mesh (the NekRS partition), must give the 1-partition
 image bit for bit -- min over packed depth|colour keys is associative and
@@ -50,8 +51,47 @@ def one(cyl):
     ctx.close()
 
 
+def _composite(cyl, pipe, R):
+    parts = []
+    for r in range(R):
+        e0, e1 = synth.partition(cyl.n_elements, r, R)
+        ctx = Context(0)
+        da = SemDataAdaptor(ctx)
+        da.initialize(Snapshot(0.0, 0, r, (_block(cyl, e0, e1),)))
+        InsituAnalysis(pipe).execute(da, fetch_image=False)
+        parts.append((ctx, da))
+    root = parts[0][0]
+    root.composite_partitions([c for c, _ in parts], pipe.native(pipe.view))
+    rgba, depth = root.image(pipe.width, pipe.height, depth=True)
+    for c, _ in parts:
+        c.close()
+    return rgba, depth
+
+
+@pytest.mark.parametrize("R", [3, 8])
+def test_bulk_and_load_kernels_agree_on_odd_bands(cyl, monkeypatch, R):
+    """191 x 157 pixels: bands start and end on odd pixels, so the bulk-copy
+    kernel's aligned tiles plus its end pixels must cover every band exactly;
+    both composite kernels and the one-partition step agree bit for bit."""
+    pipe = _pipe(cyl, W=191, H=157)
+    ctx = Context(0)
+    da = SemDataAdaptor(ctx)
+    da.initialize(Snapshot(0.0, 0, 0, (_block(cyl, 0, cyl.n_elements),)))
+    ref = InsituAnalysis(pipe).execute(da, depth=True)
+    ctx.close()
+    monkeypatch.setenv("NKB_COMPOSITE_BULK", "1")
+    a_rgba, a_depth = _composite(cyl, pipe, R)
+    monkeypatch.setenv("NKB_COMPOSITE_BULK", "0")
+    b_rgba, b_depth = _composite(cyl, pipe, R)
+    for rgba, depth in ((a_rgba, a_depth), (b_rgba, b_depth)):
+        assert np.array_equal(rgba, ref.rgba)
+        assert np.array_equal(depth.view(np.uint32), ref.depth.view(np.uint32))
+
+
+@pytest.mark.parametrize("kernel", ["bulk", "loads"])
 @pytest.mark.parametrize("R", [2, 3, 4, 5, 8])
-def test_partition_composite_equals_one_partition(cyl, one, R):
+def test_partition_composite_equals_one_partition(cyl, one, monkeypatch, R, kernel):
+    monkeypatch.setenv("NKB_COMPOSITE_BULK", "1" if kernel == "bulk" else "0")
     pipe = _pipe(cyl)
     parts, ranges = [], []
     for r in range(R):
