@@ -589,12 +589,14 @@ def run_ours(a):
                            f"{geo_build_ms:.3f} ms during warm-up") if cached else "off/not needed",
         "execute": "stream-ordered nkb_execute_async x K, one nkb_execute_wait (ms_per_step); "
                    "synchronous nkb_execute per step (ms_per_step_sync)",
-        # libnekb200 kernels per step on rank 0: K1g|K1|K1s, zbuf clear, K2
-        # raster, range words, K3 resolve, report (1 GPU or the NCCL
-        # composite, whose reduce kernels are NCCL's); the P2P composite adds
-        # epoch, two waits, two signals and the composite kernel and drops K3;
-        # stream-ordered P2P steps report in both halves (one more report)
-        "gpu_launches": (6 if world == 1 or os.environ.get("NKB_COMPOSITE") == "nccl" else
+        # libnekb200 kernels per step on rank 0.  1 GPU: K1g|K1|K1s, K2
+        # raster, K3 resolve (+ next key-buffer clear, range words and
+        # report in its last CTA).  NCCL composite: K1g, zbuf clear, K2,
+        # range words, K3, report (the reduce kernels are NCCL's).  P2P
+        # composite: K1g, epoch, wait, zbuf clear, K2, range words, signal,
+        # composite, signal, wait, report; stream-ordered P2P steps report in
+        # both halves (one more report)
+        "gpu_launches": (3 if world == 1 else 6 if os.environ.get("NKB_COMPOSITE") == "nccl" else
                          11 if os.environ.get("NKB_COMPOSITE_OVERLAP") == "0" else 12) * a.steps,
         "host_ms_per_async_launch": host_launch_ms,
         "clocks": clk,

@@ -277,7 +277,8 @@ int nkb_ctx_destroy(nkb_ctx* ctx) {
   cudaFree(ctx->region_count);
   cudaFree(ctx->tri_export);
   cudaFree(ctx->meta_export);
-  cudaFree(ctx->zbuf);
+  cudaFree(ctx->zbufs[0]);
+  cudaFree(ctx->rticket);
   cudaFree(ctx->rgba);
   cudaFree(ctx->depth);
   cudaFree(ctx->range_dev);
@@ -746,14 +747,23 @@ static int build_colormap(const nkb_pipeline* p, Colormap& cm) {
 
 static int ensure_image(nkb_ctx* ctx, int W, int H) {
   if (ctx->W == W && ctx->H == H && ctx->zbuf) return NKB_OK;
-  cudaFree(ctx->zbuf);
+  cudaFree(ctx->zbufs[0]);
   cudaFree(ctx->rgba);
   cudaFree(ctx->depth);
-  ctx->zbuf = nullptr;
+  ctx->zbuf = ctx->zbufs[0] = ctx->zbufs[1] = nullptr;
   ctx->rgba = nullptr;
   ctx->depth = nullptr;
   const size_t npx = (size_t)W * H;
-  NKB_CUDA(cudaMalloc(&ctx->zbuf, (npx + 2) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMalloc(&ctx->zbufs[0], 2 * (npx + 2) * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMemset(ctx->zbufs[0], 0xff, 2 * (npx + 2) * sizeof(unsigned long long)));
+  ctx->zbufs[1] = ctx->zbufs[0] + npx + 2;
+  ctx->zbuf = ctx->zbufs[0];
+  ctx->zpar_next = 0;
+  ctx->znext_clean = true;
+  if (!ctx->rticket) {
+    NKB_CUDA(cudaMalloc(&ctx->rticket, sizeof(unsigned int)));
+    NKB_CUDA(cudaMemset(ctx->rticket, 0, sizeof(unsigned int)));
+  }
   NKB_CUDA(cudaMalloc(&ctx->rgba, npx * 4));
   NKB_CUDA(cudaMalloc(&ctx->depth, npx * sizeof(float)));
   ctx->W = W;
@@ -874,7 +884,8 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     }
   }
   if (part & 1) {
-  NKB_TRY(launch_zbuf_clear(zbuf, npx, s));
+  // (a one-GPU step's key buffer was cleared by the previous step's resolve)
+  if (composite || ctx->step_clear) NKB_TRY(launch_zbuf_clear(zbuf, npx, s));
   RasterParams rp;
   rp.tri = ctx->tri;
   if (ordered) {          // one contiguous region; its count is the scan total
@@ -892,9 +903,10 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   rp.height = p->height;
   rp.zbuf = zbuf;
   NKB_TRY(launch_raster(rp, s));
-  NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, rp.region_count == ctx->counters ? nullptr : rp.region_count,
-                             rp.n_regions, rp.region_cap, ctx->tri_cap, s,
-                             split ? ctx->csnap + 8 * par : nullptr));
+  if (composite)                                   // (one GPU: in the resolve tail)
+    NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, rp.region_count == ctx->counters ? nullptr : rp.region_count,
+                               rp.n_regions, rp.region_cap, ctx->tri_cap, s,
+                               split ? ctx->csnap + 8 * par : nullptr));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[2], s));
   if (p2p) NKB_TRY(launch_p2p_signal(pp, 0, nullptr, s));   // "keys ready" (+ this rank's overflow word)
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[6], s));
@@ -915,7 +927,47 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     NKB_NCCL(g_nccl.GroupEnd());
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[3], s));
-  if (!p2p && (!composite || ctx->rank == 0)) {
+  ReportParams rep;
+  rep.counters = ctx->counters;
+  rep.range = ctx->range_dev;
+  rep.region_count = ordered ? nullptr : ctx->region_count;
+  rep.n_regions = ordered ? 0 : ctx->n_regions;
+  rep.h_counters = ctx->h_counters_dev;
+  rep.err = p2p ? ctx->p2p.err : nullptr;
+  rep.peer_counts = p2p ? ctx->p2p.flags + 2 * kMaxRanks : nullptr;
+  rep.peer_overflow = p2p ? ctx->p2p.flags + 3 * kMaxRanks : nullptr;
+  rep.nranks = ctx->nranks;
+  rep.h_res = p2p ? ctx->p2p.h_res_dev : nullptr;
+  rep.part = part;
+  if (!composite) {
+    // one GPU: resolve, clear the other key buffer for the next step, and
+    // (last CTA) range words + overflow word + report -- one launch
+    ResolveParams rs;
+    rs.zbuf = zbuf;
+    rs.width = p->width;
+    rs.height = p->height;
+    rs.lo = rs.hi = 0.0;
+    rs.range_words = nullptr;
+    rs.vmin = p->vmin;
+    rs.vmax = p->vmax;
+    rs.cmap = cm;
+    memcpy(rs.bg, p->background, 4);
+    rs.rgba = ctx->rgba;
+    rs.depth = ctx->depth;
+    rs.range_out = ctx->range_dev;
+    rs.counters = ctx->counters;
+    rs.clear_next = zbuf == ctx->zbufs[0] ? ctx->zbufs[1] : ctx->zbufs[0];
+    rs.words = zbuf + npx;
+    rs.region_count = ordered ? nullptr : ctx->region_count;
+    rs.n_regions = ctx->n_regions;
+    rs.region_cap = ctx->region_cap;
+    rs.tri_cap = ctx->tri_cap;
+    rs.ticket = ctx->rticket;
+    NKB_TRY(launch_resolve_tail(rs, rep, s));
+    if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[4], s));
+    return NKB_OK;
+  }
+  if (!p2p && ctx->rank == 0) {
     ResolveParams rs;
     rs.zbuf = ctx->zbuf;
     rs.width = p->width;
@@ -932,18 +984,6 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
     NKB_TRY(launch_resolve(rs, s));
   }
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[4], s));
-  ReportParams rep;
-  rep.counters = ctx->counters;
-  rep.range = ctx->range_dev;
-  rep.region_count = ordered ? nullptr : ctx->region_count;
-  rep.n_regions = ordered ? 0 : ctx->n_regions;
-  rep.h_counters = ctx->h_counters_dev;
-  rep.err = p2p ? ctx->p2p.err : nullptr;
-  rep.peer_counts = p2p ? ctx->p2p.flags + 2 * kMaxRanks : nullptr;
-  rep.peer_overflow = p2p ? ctx->p2p.flags + 3 * kMaxRanks : nullptr;
-  rep.nranks = ctx->nranks;
-  rep.h_res = p2p ? ctx->p2p.h_res_dev : nullptr;
-  rep.part = part;
   NKB_TRY(launch_report(rep, s));
   return NKB_OK;
 }
@@ -1062,7 +1102,20 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   const bool p2p = composite && ctx->p2p.ready;
   if (sync) clear_overflow_words(ctx);
   const unsigned long long ep = p2p ? ++ctx->p2p.epoch : 0;   // the device counter follows in-stream
-  const int slot = (int)(ep & 1);
+  int slot = (int)(ep & 1);
+  if (!composite) {
+    // one GPU: alternate the two key buffers (graph slot = buffer); the
+    // step's resolve clears the other one for the next step
+    slot = ctx->zpar_next;
+    ctx->zbuf = ctx->zbufs[slot];
+    ctx->step_clear = !ctx->znext_clean;
+    ctx->zpar_next = slot ^ 1;
+    ctx->znext_clean = true;
+  } else {
+    ctx->step_clear = true;
+    // the NCCL composite reduces into ctx->zbuf: the next one-GPU step must clear it first
+    if (!p2p && ctx->zbuf == ctx->zbufs[ctx->zpar_next]) ctx->znext_clean = false;
+  }
   // P2P: the composite half of step k runs on ctx->comp_stream while step
   // k+1's surface pass runs on `s`.  Step k+2 (same parity slots) waits for
   // step k's composite half; the cross-GPU order stays with the epoch flags.
@@ -1113,6 +1166,7 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
         key.push_back((char)slot);
         key.push_back((char)part);
       }
+      key.push_back(ctx->step_clear ? 'c' : 'n');
       // whole steps, first halves and second halves keep separate graphs
       // (synchronous and stream-ordered steps alternate without re-capture)
       cudaGraphExec_t& gx = part == 3 ? ctx->graph_exec[slot] : part == 1 ? ctx->graph_exec_a[slot]

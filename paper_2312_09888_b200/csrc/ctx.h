@@ -105,7 +105,14 @@ struct nkb_ctx {
   float4* tri_export = nullptr;             // compacted FAST-mode triangles (on request)
   unsigned long long* meta_export = nullptr;
   int64_t export_cap = 0;
-  unsigned long long* zbuf = nullptr;       // W*H + 2 range words
+  unsigned long long* zbuf = nullptr;       // W*H + 2 range words: the last step's key buffer
+  // one-GPU steps alternate two key buffers: each step's resolve clears the
+  // other one for the next step (launch_resolve_tail)
+  unsigned long long* zbufs[2] = {nullptr, nullptr};   // one allocation
+  int zpar_next = 0;
+  bool znext_clean = false;                 // zbufs[zpar_next] is all ~0
+  unsigned int* rticket = nullptr;          // the tail's last-CTA ticket
+  bool step_clear = true;                   // the step being enqueued clears its key buffer first
   unsigned char* rgba = nullptr;
   float* depth = nullptr;
   unsigned char* rgb_dev = nullptr;         // packed RGB for the PPM payload

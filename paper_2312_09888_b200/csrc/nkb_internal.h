@@ -175,6 +175,16 @@ struct ResolveParams {
   unsigned char* rgba;
   float* depth;
   double* range_out;      // [2] device, range used
+  // one-GPU step tail (all null otherwise): the range from the step's
+  // counters, the next step's key buffer cleared in the same pass, and the
+  // range words + overflow word + report done by the last CTA (ticket)
+  unsigned long long* counters = nullptr;     // [1] enc(min) [2] enc(max); [6] := overflow
+  unsigned long long* clear_next = nullptr;   // [W*H + 2] := ~0
+  unsigned long long* words = nullptr;        // this step's range words (zbuf + W*H)
+  const unsigned long long* region_count = nullptr;
+  int n_regions = 0;
+  long long region_cap = 0, tri_cap = 0;
+  unsigned int* ticket = nullptr;             // zero between launches
 };
 
 // ---- kernel launchers (defined in .cu files) --------------------------------
@@ -214,6 +224,8 @@ int launch_range_words(unsigned long long* counters, unsigned long long* words,
                        const unsigned long long* region_count, int n_regions, int64_t region_cap, int64_t tri_cap,
                        cudaStream_t s, unsigned long long* snap = nullptr);   // snap: copy of counters[0..7]
 int launch_resolve(const ResolveParams& p, cudaStream_t s);
+// the one-GPU tail: resolve + next key-buffer clear + range words + report in one launch
+int launch_resolve_tail(const ResolveParams& p, const ReportParams& rep, cudaStream_t s);
 // ---- stats.cu: numpy-exact min / max / mean ----
 constexpr long long kChunk = 32768;      // values per CTA subtree (<= 640 leaves of 57..128)
 constexpr int kWin = 128;                // boundary window (one pairwise leaf)

@@ -49,10 +49,9 @@ __global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
 // region in FAST mode, the whole buffer in ordered mode).  Multi-rank steps
 // share this word (P2P flags / an NCCL max) so that every rank decides alike
 // whether the step must grow and re-run.
-__global__ void __launch_bounds__(256) range_words_kernel(unsigned long long* counters, unsigned long long* words,
-                                                          const unsigned long long* region_count, int n_regions,
-                                                          long long region_cap, long long tri_cap,
-                                                          unsigned long long* snap) {
+__device__ void range_words_body(unsigned long long* counters, unsigned long long* words,
+                                 const unsigned long long* region_count, int n_regions, long long region_cap,
+                                 long long tri_cap, unsigned long long* snap) {
   __shared__ int s_over;
   if (threadIdx.x == 0) {
     words[0] = counters[1];
@@ -77,9 +76,16 @@ __global__ void __launch_bounds__(256) range_words_kernel(unsigned long long* co
   }
 }
 
+__global__ void __launch_bounds__(256) range_words_kernel(unsigned long long* counters, unsigned long long* words,
+                                                          const unsigned long long* region_count, int n_regions,
+                                                          long long region_cap, long long tri_cap,
+                                                          unsigned long long* snap) {
+  range_words_body(counters, words, region_count, n_regions, region_cap, tri_cap, snap);
+}
+
 // the step's report words straight into mapped pinned host memory: one
 // kernel instead of 3-5 small D2H copies at the tail of every step
-__global__ void __launch_bounds__(256) report_kernel(const ReportParams p) {
+__device__ void report_body(const ReportParams& p) {
   const int t = threadIdx.x;
   if (p.part & 1) {
     if (t < 4) p.h_counters[t] = p.counters[t];
@@ -101,9 +107,16 @@ __global__ void __launch_bounds__(256) report_kernel(const ReportParams p) {
   }
 }
 
-__global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
+__global__ void __launch_bounds__(256) report_kernel(const ReportParams p) { report_body(p); }
+
+template <bool kTail>
+__global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p, const ReportParams rep) {
   double lo = p.vmin, hi = p.vmax;
-  if (p.range_words) {
+  if (kTail) {                                       // the range straight from the step's counters
+    const unsigned long long w0 = p.counters[1], w1 = p.counters[2];
+    if (!(lo == lo)) lo = (w0 == ~0ULL) ? 0.0 : rdev::dec_ordered(w0);
+    if (!(hi == hi)) hi = (w1 == 0ULL) ? 0.0 : rdev::dec_ordered(w1);
+  } else if (p.range_words) {
     const unsigned long long w0 = p.range_words[0], w1 = ~p.range_words[1];
     if (!(lo == lo)) lo = (w0 == ~0ULL) ? 0.0 : rdev::dec_ordered(w0);
     if (!(hi == hi)) hi = (w1 == 0ULL) ? 0.0 : rdev::dec_ordered(w1);
@@ -131,7 +144,23 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p) {
     }
     reinterpret_cast<uchar4*>(p.rgba)[i] = o;
     if (p.depth) p.depth[i] = dep;
+    if (kTail) p.clear_next[i] = ~0ULL;
   }
+  if (!kTail) return;
+  if (blockIdx.x == 0 && threadIdx.x < 2) p.clear_next[n + threadIdx.x] = ~0ULL;
+  // the last CTA to finish: range words, overflow word and the step report
+  // (every CTA's writes, block 0's range_out included, are fenced before its ticket)
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  range_words_body(p.counters, p.words, p.region_count, p.n_regions, p.region_cap, p.tri_cap, nullptr);
+  __syncthreads();
+  report_body(rep);
+  if (threadIdx.x == 0) *p.ticket = 0u;
 }
 
 // ---- reference 2D renderer (sinks.render) ---------------------------------
@@ -281,7 +310,13 @@ int launch_report(const ReportParams& p, cudaStream_t s) {
 }
 
 int launch_resolve(const ResolveParams& p, cudaStream_t s) {
-  resolve_kernel<<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p);
+  resolve_kernel<false><<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p, ReportParams{});
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
+int launch_resolve_tail(const ResolveParams& p, const ReportParams& rep, cudaStream_t s) {
+  resolve_kernel<true><<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p, rep);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
