@@ -37,6 +37,15 @@ def main():
     for cfg in a.configs:
         scale = a.elements if cfg == "c5" else 1
         case = synth_device.make_case(cfg, 0, 1, scale=scale, device="cuda:0")
+        if case is None:                  # c1: the numpy generator's case, copied to the device
+            from types import SimpleNamespace
+
+            from paper_2312_09888_b200 import synth
+
+            h = synth.make_case(cfg, 0, 1)
+            dev = lambda a_: torch.from_numpy(a_).to("cuda:0")
+            case = SimpleNamespace(n_elements=h.n_elements, n_points=h.n_points, x=dev(h.x), y=dev(h.y), z=dev(h.z),
+                                   fields={k: dev(v) for k, v in h.fields.items()}, params=h.params)
         torch.cuda.synchronize()
         fields = tuple(FieldArray(k, POINT, v.shape[0], v.reshape(-1), comp_stride=case.n_points)
                        for k, v in case.fields.items())
