@@ -309,6 +309,37 @@ def _make_cases(wl: Workload, rank: int, world: int, local: int):
     return dc, None
 
 
+WORK_TRI_WEIGHT = 0.021   # K1s: one triangle costs 0.021 element passes (C4, 4 ranks: per-rank time = a E + b T)
+
+
+def _work_cuts(ctx, case, rank, world, dist, width):
+    """Contiguous element ranges of equal surface-pass cost (--partition work):
+    one ordered step on the equal partition gives every element's triangle
+    count, the ranks all-gather them, and the cuts split the prefix sum of
+    1 + WORK_TRI_WEIGHT x triangles into equal parts (what a solver's
+    partitioner does with element weights; the step itself is untimed)."""
+    import numpy as np
+
+    from dataclasses import replace
+
+    from paper_2312_09888_b200.analysis import InsituAnalysis
+
+    pipe = _pipeline(case.params, width)
+    da = _sem_adaptor(ctx, case, rank)
+    InsituAnalysis(replace(pipe, emit_meta=True, composite=False)).execute(da, fetch_image=False)
+    _, meta = ctx.triangles(with_meta=True)
+    tris = np.bincount((np.asarray(meta) >> np.uint64(32)).astype(np.int64), minlength=case.n_elements)
+    parts = [None] * world
+    dist.all_gather_object(parts, (case.e0, tris[:case.n_elements]))
+    tri_g = np.concatenate([t for _, t in sorted(parts, key=lambda p: p[0])]).astype(np.float64)
+    cs = np.cumsum(1.0 + WORK_TRI_WEIGHT * tri_g)
+    cuts = [0] + [int(np.searchsorted(cs, cs[-1] * k / world)) + 1 for k in range(1, world)] + [len(cs)]
+    for k in range(1, world + 1):                     # non-empty, increasing
+        cuts[k] = max(cuts[k], cuts[k - 1] + 1) if k < world else len(cs)
+    del da
+    return cuts
+
+
 def _host_sample(dcase, e_s: int):
     """Host copy of the first e_s elements of a device case (the oracle's input)."""
     from paper_2312_09888_b200 import synth
@@ -370,6 +401,18 @@ def run_ours(a):
     # the workload lives in HBM before timing starts
     case, hcase = _make_cases(wl, rank, world, local)
     torch.cuda.synchronize()
+    cuts = None
+    if a.partition == "work" and world > 1 and not wl.host_generated:
+        from paper_2312_09888_b200 import synth_device
+
+        cuts = _work_cuts(ctx, case, rank, world, dist, a.width)
+        del case
+        torch.cuda.empty_cache()
+        case = synth_device.make_case(wl.config, rank, world, scale=wl.scale, device=f"cuda:{local}", cuts=cuts)
+        torch.cuda.synchronize()
+        config["partition"] = {"kind": "contiguous element ranges balancing the surface-pass cost",
+                               "cost_per_element": f"1 + {WORK_TRI_WEIGHT} x triangles (K1s cost model, C4)",
+                               "cuts": [int(c) for c in cuts]}
     npts = case.n_points
     pipe = _pipeline(case.params, a.width)
     comps = {k: v.shape[0] for k, v in case.fields.items()}
@@ -864,6 +907,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--csv", default="", help="directory for timings.csv / phases.csv")
     ap.add_argument("--e2e-max-gb", type=float, default=12.0)
+    ap.add_argument("--partition", default="equal", choices=["equal", "work"],
+                    help="N>1 device-generated configs: equal contiguous element ranges (the solver's "
+                         "partition) or ranges balancing the surface-pass cost")
     ap.add_argument("--e2e-sync-write", action="store_true", help="write each PPM inside consume() (no writer thread)")
     a = ap.parse_args()
     if a.warmup < 3:

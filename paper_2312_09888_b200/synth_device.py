@@ -137,10 +137,11 @@ def c5_box(e0, e1, n_elements, device):
                       dict(synth.PARAMS["c5"]))
 
 
-def make_case(name: str, rank: int = 0, nranks: int = 1, scale: int = 1, device="cuda"):
-    """Device partition `rank` of config `name` (see synth.make_case)."""
+def make_case(name: str, rank: int = 0, nranks: int = 1, scale: int = 1, device="cuda", cuts=None):
+    """Device partition `rank` of config `name` (see synth.make_case); `cuts`
+    (nranks + 1 element indices) overrides the equal contiguous ranges."""
     E = synth.global_elements(name, scale)
-    e0, e1 = synth.partition(E, rank, nranks)
+    e0, e1 = (int(cuts[rank]), int(cuts[rank + 1])) if cuts is not None else synth.partition(E, rank, nranks)
     if name == "c2":
         return rbc_cylinder(e0, e1, (32, 32, 32 * scale), device)
     if name == "c3":
