@@ -231,13 +231,16 @@ int nkb_execute(nkb_ctx* ctx, const nkb_pipeline* p, nkb_report* out, void* stre
  * composite) are ordered on the device only and host jitter does not couple
  * the ranks.  nkb_execute_wait synchronises and fills the report of the
  * last enqueued step.  The triangle buffer cannot grow behind an enqueued
- * step: a step that overflows is reported (overflowed = 1, triangles and image
- * incomplete) and the buffer grows for later steps; nkb_execute (which
- * re-runs an overflowing step) guarantees a complete result.  pipeline.timing
- * must be 0. */
+ * step: a step that overflows is reported (overflowed = 1 if any step of the
+ * sequence overflowed on any rank; triangles and image incomplete) and the
+ * buffer grows for later steps; nkb_execute (which re-runs an overflowing
+ * step) guarantees a complete result.  pipeline.timing must be 0.  With the
+ * P2P composite each step's composite runs on a library stream beside the
+ * next step's surface pass (NKB_COMPOSITE_OVERLAP=0: one stream). */
 int nkb_execute_async(nkb_ctx* ctx, const nkb_pipeline* p, void* stream);
 int nkb_execute_wait(nkb_ctx* ctx, nkb_report* out, void* stream);
-/* results of the last execute (device pointers, library-owned) */
+/* results of the last execute (device pointers, library-owned; after
+ * nkb_execute_async, valid once nkb_execute_wait returned) */
 int nkb_image_device(nkb_ctx* ctx, const unsigned char** rgba, const float** depth,
                      const uint64_t** zbuf);
 /* copy the last image to host memory (rgba: W*H*4, depth: W*H floats, either may be NULL) */
