@@ -43,13 +43,18 @@ inline unsigned grid_for(long long n, int threads) {
 constexpr int kRunBlock = 256;
 
 __global__ void run_key_kernel(const int* cnt, long long U, unsigned char* key, int* u_of, int* hist) {
+  __shared__ int h[kGroupMax + 2];                  // block histogram: one global atomic per bin per block
+  if (threadIdx.x < kGroupMax + 2) h[threadIdx.x] = 0;
+  __syncthreads();
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < U; u += (long long)gridDim.x * blockDim.x) {
     const int c = cnt[u];
     const int k = c > kGroupMax ? kGroupMax + 1 : c;
     key[u] = (unsigned char)k;
     u_of[u] = (int)u;
-    atomicAdd(&hist[k], 1);
+    atomicAdd(&h[k], 1);
   }
+  __syncthreads();
+  if (threadIdx.x < kGroupMax + 2 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
 }
 
 // sorted run p (stable by key): run u = order[p] of K = key copies -> its group rows
@@ -202,8 +207,13 @@ __global__ void gs_combine_kernel(double* __restrict__ part, const int* __restri
 // ---- multi-rank discovery helpers ----
 
 __global__ void dest_hist_kernel(const long long* ugid, long long U, int R, int* hist) {
+  __shared__ int h[kMaxRanks];                      // block histogram: one global atomic per rank per block
+  if (threadIdx.x < kMaxRanks) h[threadIdx.x] = 0;
+  __syncthreads();
   for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < U; u += (long long)gridDim.x * blockDim.x)
-    atomicAdd(&hist[(int)(ugid[u] % R)], 1);
+    atomicAdd(&h[(int)(ugid[u] % R)], 1);
+  __syncthreads();
+  if (threadIdx.x < R && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
 }
 
 // bucket (gid, count) pairs by owner rank; cursor[q] starts at the bucket offset
