@@ -100,6 +100,10 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -907,6 +911,7 @@ int launch_geometry(const double* x, const double* y, const double* z, int64_t E
 
 // A/B switch (NKB_EMIT_PREFETCH=0): L2 prefetch of an emitting element's coordinates in K1g
 __constant__ int g_emit_prefetch = 1;
+__constant__ int g_emit_stage = 1;          // K1g: an emitting element's x,y,z copied into dead S_dv space
 
 // ---- node programs: compile-time surface / colour sources of a pipeline ----
 // The node phase's per-surface source dispatch (Q, |w|, |u|, a staged scalar
@@ -1136,6 +1141,14 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
   const int psz = ((plane_slots >> 16) & 0xff) == 0xff ? -1 : ((plane_slots >> 16) & 0xff);
   constexpr NodeProg NP = node_prog(kProg);
   const bool kEmitPrefetch = g_emit_prefetch;
+  // an emitting element's coordinates (not staged): copied by 16-byte
+  // cp.async into S_dv's space above the active-cell lists, which is dead
+  // from the node-phase barrier to the next iteration's pencils
+  // (two-CTA kernels only: the three-CTA ones have no registers to spare at 80)
+  const bool emit_stage =
+      kOcc == 2 && g_emit_stage && slot_xyz < 0 && ((plane_slots >> 24) & 1) && p.mode != FUSED_COUNT;
+  double* const S_xyz = S_dv + 6 * kArr;
+  static_assert(kNC * 8 + kMaxTriPerElem * 2 <= 6 * kArr * 8, "active-cell lists overlap the emission coordinates");
   // node programs: staged-array offset of each scalar surface and of a scalar colour
   int sc_off[NKB_MAX_SURFACES], sc_off_c = 0;
 #pragma unroll
@@ -1323,8 +1336,17 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
     }
     // the element emits: its corner coordinates (never staged unless a slice
     // uses them) are read by the emission a few hundred cycles from now --
-    // pull the three 4 KB blocks toward L2 while classification runs
-    if (kEmitPrefetch && tid == 0 && p.mode != FUSED_COUNT) {
+    // copy them into shared memory (or pull them toward L2) while
+    // classification runs
+    if (emit_stage) {
+      const long long gx = e * (long long)kNN;
+      for (int i = tid; i < 3 * (kNN / 2); i += kG2Threads) {
+        const int f = i / (kNN / 2), o = 2 * (i - f * (kNN / 2));
+        NKB_DCHECK(f < 3 && o + 1 < kArr);
+        cp_async16(S_xyz + f * kArr + o, (f == 0 ? p.x : f == 1 ? p.y : p.z) + gx + o);
+      }
+      cp_async_commit();
+    } else if (kEmitPrefetch && tid == 0 && p.mode != FUSED_COUNT) {
       const long long gx = e * (long long)kNN;
       l2_prefetch(p.x + gx, kNN * sizeof(double));
       l2_prefetch(p.y + gx, kNN * sizeof(double));
@@ -1391,14 +1413,15 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       mc.base = base;
     }
     cta_fill += (unsigned long long)total;             // every thread keeps the same count
+    if (emit_stage) cp_async_wait_all();              // the element's coordinates have landed
     __syncthreads();
     if (p.mode == FUSED_COUNT || total == 0) continue;
 
     // ---- emit: one thread per active cell, (surface, table) order ----
     const bool xyz_staged = slot_xyz >= 0;
-    const double* Sx = xyz_staged ? S_in + slot_xyz * kArr : p.x + g0;
-    const double* Sy = xyz_staged ? S_in + (slot_xyz + 1) * kArr : p.y + g0;
-    const double* Sz = xyz_staged ? S_in + (slot_xyz + 2) * kArr : p.z + g0;
+    const double* Sx = xyz_staged ? S_in + slot_xyz * kArr : emit_stage ? S_xyz : p.x + g0;
+    const double* Sy = xyz_staged ? S_in + (slot_xyz + 1) * kArr : emit_stage ? S_xyz + kArr : p.y + g0;
+    const double* Sz = xyz_staged ? S_in + (slot_xyz + 2) * kArr : emit_stage ? S_xyz + 2 * kArr : p.z + g0;
     const double* Su = S_in + slot_vel * kArr;
     // pn: the node's index in Sx/Sy/Sz (swizzled when staged, natural in global
     // memory otherwise); the edge's plane distances always use all three
@@ -1544,6 +1567,9 @@ static int fused2_prepare() {
   const char* v = getenv("NKB_EMIT_PREFETCH");
   const int on = !(v && v[0] == '0');
   NKB_CUDA(cudaMemcpyToSymbol(g_emit_prefetch, &on, sizeof(on)));
+  const char* vs = getenv("NKB_EMIT_STAGE");
+  const int st = !(vs && vs[0] == '0');
+  NKB_CUDA(cudaMemcpyToSymbol(g_emit_stage, &st, sizeof(st)));
   for (int c = 0; c < 2; ++c)
     for (int occ = 2; occ <= (c == 1 ? 3 : 2); ++occ) {
       const int bytes = (int)fused2_smem_bytes(occ == 3 ? 3 : kG2MaxIn, c == 1, true, true);
@@ -1684,6 +1710,7 @@ int launch_fused(const FusedParams& p, cudaStream_t s) {
     }
     const int slot2_sc = k2;
     for (int c = 0; c < p.n_scalars; ++c) q2.in_ptr[k2++] = p.scalar[c];
+    if ((((uintptr_t)p.x | (uintptr_t)p.y | (uintptr_t)p.z) & 15u) == 0) ps |= 1 << 24;   // 16-byte copies allowed
     const unsigned g2 = (unsigned)fused_grid_for(p, p.n_elements);
     const bool compact = p.geo_compact != 0;
     const int prog = node_prog_of(p);
