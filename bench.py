@@ -331,12 +331,23 @@ def _work_cuts(ctx, case, rank, world, dist, width):
     tris = np.bincount((np.asarray(meta) >> np.uint64(32)).astype(np.int64), minlength=case.n_elements)
     parts = [None] * world
     dist.all_gather_object(parts, (case.e0, tris[:case.n_elements]))
-    tri_g = np.concatenate([t for _, t in sorted(parts, key=lambda p: p[0])]).astype(np.float64)
-    cs = np.cumsum(1.0 + WORK_TRI_WEIGHT * tri_g)
-    cuts = [0] + [int(np.searchsorted(cs, cs[-1] * k / world)) + 1 for k in range(1, world)] + [len(cs)]
-    for k in range(1, world + 1):                     # non-empty, increasing
-        cuts[k] = max(cuts[k], cuts[k - 1] + 1) if k < world else len(cs)
+    tri_g = np.concatenate([t for _, t in sorted(parts, key=lambda p: p[0])])
     del da
+    return balanced_cuts(tri_g, world)
+
+
+def balanced_cuts(tri_per_element, world, weight=None):
+    """world + 1 element indices: contiguous ranges whose costs 1 + weight x
+    triangles per element are as equal as the element granularity allows
+    (every range non-empty when there are at least `world` elements)."""
+    import numpy as np
+
+    w = WORK_TRI_WEIGHT if weight is None else weight
+    cs = np.cumsum(1.0 + w * np.asarray(tri_per_element, dtype=np.float64))
+    n = len(cs)
+    cuts = [0] + [int(np.searchsorted(cs, cs[-1] * k / world)) + 1 for k in range(1, world)] + [n]
+    for k in range(1, world):                          # increasing, room for the ranks after k
+        cuts[k] = min(max(cuts[k], cuts[k - 1] + 1), n - (world - k))
     return cuts
 
 

@@ -384,3 +384,27 @@ def test_insitu_sink_without_composite_writes_one_file_per_rank(tmp_path):
     assert s1.per_rank and d.is_dir()
     s0 = InsituSink({"dir": str(tmp_path / "one"), "iso": "Q=1"}, comm=_Comm(1, 2))
     assert not s0.per_rank and not (tmp_path / "one").exists()      # composite: rank 0 writes
+
+
+def test_bench_balanced_cuts():
+    """bench.py --partition work: contiguous ranges of equal surface-pass cost."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    # uniform work: the equal partition
+    assert bench.balanced_cuts(np.zeros(100, np.int64), 4) == [0, 25, 50, 75, 100]
+    # all triangles at the end: the last rank gets few elements
+    t = np.zeros(1000, np.int64)
+    t[900:] = 1000
+    cuts = bench.balanced_cuts(t, 4, weight=0.1)
+    cost = 1.0 + 0.1 * t
+    parts = [cost[cuts[k]:cuts[k + 1]].sum() for k in range(4)]
+    assert cuts[0] == 0 and cuts[-1] == 1000 and all(b > a for a, b in zip(cuts, cuts[1:]))
+    assert max(parts) / min(parts) < 1.05
+    # more ranks than heavy elements, and the degenerate tiny case: ranges stay non-empty
+    cuts = bench.balanced_cuts(np.array([0, 0, 10**6, 0, 0]), 4)
+    assert all(b > a for a, b in zip(cuts, cuts[1:])) and cuts[-1] == 5
+    assert bench.balanced_cuts(np.zeros(4, np.int64), 4) == [0, 1, 2, 3, 4]
