@@ -1209,12 +1209,19 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   return collect_step(ctx, p2p);
 }
 
-// capacity the step needed (per-region maximum in FAST mode)
+// capacity the step needed (per-region maximum in FAST mode; the region
+// counts are read from the device only here, after an overflow -- the step
+// report carries the 8 counter words alone)
 static int64_t needed_capacity(nkb_ctx* ctx, bool ordered) {
   const int64_t total = (int64_t)ctx->h_counters[0];
   if (ordered) return total;
+  std::vector<unsigned long long> rc(ctx->n_regions > 0 ? ctx->n_regions : 1, 0ULL);
+  if (ctx->n_regions > 0 &&
+      cudaMemcpy(rc.data(), ctx->region_count, sizeof(unsigned long long) * ctx->n_regions,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 2 * ctx->tri_cap;                           // (unreachable in practice) grow generously
   int64_t mx = 0;
-  for (int r = 0; r < ctx->n_regions; ++r) mx = std::max<int64_t>(mx, (int64_t)ctx->h_counters[8 + r]);
+  for (int r = 0; r < ctx->n_regions; ++r) mx = std::max<int64_t>(mx, (int64_t)rc[r]);
   return mx * ctx->n_regions;
 }
 

@@ -153,7 +153,7 @@ struct ReportParams {
   const double* range;                      // [2]
   const unsigned long long* region_count;   // [n_regions] or null (ordered mode)
   int n_regions;
-  unsigned long long* h_counters;           // host words [0..3] counters, [4..5] range bits, [8..] regions
+  unsigned long long* h_counters;           // host words [0..3] counters, [4..5] range bits, [6..7] overflow
   const int* err;                           // P2P: timeout flag, or null
   const unsigned long long* peer_counts;    // P2P: [kMaxRanks] per-rank triangle counts
   const unsigned long long* peer_overflow;  // P2P: [kMaxRanks] per-rank overflow words

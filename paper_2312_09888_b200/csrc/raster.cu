@@ -91,8 +91,6 @@ __device__ void report_body(const ReportParams& p) {
     if (t < 4) p.h_counters[t] = p.counters[t];
     // overflow words are sticky across stream-ordered steps: the host clears them
     if (t == 6 || t == 7) p.h_counters[t] |= p.counters[t];
-    if (p.region_count)
-      for (int i = t; i < p.n_regions; i += blockDim.x) p.h_counters[8 + i] = p.region_count[i];
   }
   if (!(p.part & 2)) return;
   if (t == 4 || t == 5) p.h_counters[t] = (unsigned long long)__double_as_longlong(p.range[t - 4]);
