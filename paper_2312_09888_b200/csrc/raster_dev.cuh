@@ -114,6 +114,17 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
     C[q] = (double)v.w;
   }
   if (!ok) return;
+  // the pixel-centre box first: most triangles of a fine mesh cover no pixel
+  // centre and leave here, before the area, the edge set-up and 1 / area
+  const long long xmin = min(X[0], min(X[1], X[2])), xmax = max(X[0], max(X[1], X[2]));
+  const long long ymin = min(Y[0], min(Y[1], Y[2])), ymax = max(Y[0], max(Y[1], Y[2]));
+  long long px0 = -floordiv(-(xmin - 128), 256), px1 = floordiv(xmax - 128, 256);
+  long long py0 = -floordiv(-(ymin - 128), 256), py1 = floordiv(ymax - 128, 256);
+  if (px0 < 0) px0 = 0;
+  if (py0 < 0) py0 = 0;
+  if (px1 > W - 1) px1 = W - 1;
+  if (py1 > H - 1) py1 = H - 1;
+  if (px0 > px1 || py0 > py1) return;
   long long area = (X[1] - X[0]) * (Y[2] - Y[0]) - (Y[1] - Y[0]) * (X[2] - X[0]);
   if (area == 0) return;
   if (area < 0) {
@@ -123,14 +134,6 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
     double tc = C[1]; C[1] = C[2]; C[2] = tc;
     area = -area;
   }
-  const long long xmin = min(X[0], min(X[1], X[2])), xmax = max(X[0], max(X[1], X[2]));
-  const long long ymin = min(Y[0], min(Y[1], Y[2])), ymax = max(Y[0], max(Y[1], Y[2]));
-  long long px0 = -floordiv(-(xmin - 128), 256), px1 = floordiv(xmax - 128, 256);
-  long long py0 = -floordiv(-(ymin - 128), 256), py1 = floordiv(ymax - 128, 256);
-  if (px0 < 0) px0 = 0;
-  if (py0 < 0) py0 = 0;
-  if (px1 > W - 1) px1 = W - 1;
-  if (py1 > H - 1) py1 = H - 1;
   // edge (a->b) opposite vertex i: w_i(P) = (Xb-Xa)(Py-Ya) - (Yb-Ya)(Px-Xa)
   const int ea[3] = {1, 2, 0}, eb[3] = {2, 0, 1};
   long long bias[3];
