@@ -1,0 +1,13 @@
+O=gpurun_out/rdef; rm -rf $O; mkdir -p $O
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_render.py tests/test_gpu_partitions.py tests/test_gpu_fullsize.py -m gpu -q -x > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -n 2 $O/pytest.log
+for r in 1 2; do
+  NKB_RASTER_DEFER=0 python tools/kbench.py c1 c2 c5 c4 --reps 20 --tag inplace >> $O/kb.jsonl 2>> $O/kb.err
+  python tools/kbench.py c1 c2 c5 c4 --reps 20 --tag defer >> $O/kb.jsonl 2>> $O/kb.err
+done
+python - <<'PY'
+import json, collections
+d = collections.defaultdict(list)
+for l in open('gpurun_out/rdef/kb.jsonl'):
+    j = json.loads(l); d[(j['config'], j['tag'])].append(j['raster'])
+for k in sorted(d): print(k, d[k])
+PY
