@@ -455,6 +455,19 @@ def run_ours(a):
         if dist is not None:
             dist.barrier()
 
+    # N > 1: the ranks leave the host barrier up to ~1 ms apart; a device-side
+    # barrier (an NCCL all-reduce on the timed stream) right before the start
+    # event starts every rank's clock once all GPUs are there, so the max over
+    # ranks measures the job, not the host barrier's skew
+    dev_group = dist.new_group(backend="nccl") if dist is not None else None
+    dev_token = torch.zeros(1, device=f"cuda:{local}")
+
+    def start(ev):
+        barrier()
+        if dev_group is not None:
+            dist.all_reduce(dev_token, group=dev_group)
+        ev.record(stream)
+
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
@@ -474,11 +487,13 @@ def run_ours(a):
     barrier()
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dev_group is not None:                          # the device barrier's first call (communicator set-up)
+        dist.all_reduce(dev_token, group=dev_group)
     # the timed steps use the stream-ordered Execute (nkb_execute_async): no
     # host synchronisation between steps, so host jitter on one rank does not
     # hold up the composite of the others; the last step's report is waited
     # for inside the timed region and must not have overflowed
-    e0.record(stream)
+    start(e0)
     import time as _time
     th0 = _time.perf_counter()
     for _ in range(a.steps):
@@ -494,8 +509,7 @@ def run_ours(a):
     total_points = sum_over_ranks(float(npts))
     value = total_points / (ms / 1e3)
     # the same steps through the synchronous Execute (host sync + report per step)
-    barrier()
-    e0.record(stream)
+    start(e0)
     for _ in range(a.steps):
         an.execute(da, fetch_image=False)
     e1.record(stream)
@@ -603,8 +617,7 @@ def run_ours(a):
         for _ in range(2):
             sink.consume(Snapshot(0.0, step, rank, (hblk,)))
             step += 1
-        barrier()
-        e0.record(stream)
+        start(e0)
         for _ in range(e2e_steps):
             sink.consume(Snapshot(0.0, step, rank, (hblk,)))
             step += 1
@@ -643,6 +656,9 @@ def run_ours(a):
                            f"{geo_build_ms:.3f} ms during warm-up") if cached else "off/not needed",
         "execute": "stream-ordered nkb_execute_async x K, one nkb_execute_wait (ms_per_step); "
                    "synchronous nkb_execute per step (ms_per_step_sync)",
+        "timed_region": ("host barrier, then a device barrier (NCCL all-reduce on the timed stream), then the "
+                         "start event on every rank; CUDA events, max over ranks") if world > 1 else
+                        "CUDA events on the launch stream, synchronised on both sides",
         # libnekb200 kernels per step on rank 0.  1 GPU: K1g|K1|K1s, K2
         # raster, K3 resolve (+ next key-buffer clear, range words and
         # report in its last CTA).  NCCL composite: K1g, zbuf clear, K2,
@@ -651,7 +667,8 @@ def run_ours(a):
         # composite, signal, wait, report; stream-ordered P2P steps report in
         # both halves (one more report)
         "gpu_launches": (3 if world == 1 else 6 if os.environ.get("NKB_COMPOSITE") == "nccl" else
-                         11 if os.environ.get("NKB_COMPOSITE_OVERLAP") == "0" else 12) * a.steps,
+                         12 if rep_last.composite_overlapped else 11) * a.steps,
+        "composite_overlapped": bool(rep_last.composite_overlapped),
         "host_ms_per_async_launch": host_launch_ms,
         "clocks": clk,
     }

@@ -120,6 +120,8 @@ typedef struct {
     int     overflowed;           /* nkb_execute_wait only: the step's triangles overflowed on some
                                      rank (its triangle set and image are incomplete; the buffer
                                      has grown for the steps enqueued from now on) */
+    int     composite_overlapped; /* nkb_execute_wait only: the last step's P2P composite ran
+                                     on the library's stream beside the next surface pass */
 } nkb_report;
 
 typedef struct {

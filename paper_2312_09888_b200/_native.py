@@ -75,6 +75,7 @@ class NkbReport(C.Structure):
         ("ms_geometry", C.c_float),
         ("surface_pass", C.c_int),
         ("overflowed", C.c_int),
+        ("composite_overlapped", C.c_int),
     ]
 
 

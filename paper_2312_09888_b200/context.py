@@ -29,6 +29,7 @@ class Report:
     ms_geometry: float = 0.0
     surface_pass: int = 0          # 0: K1 fused, 1: K1s stream (no gradient), 2: K1g (cached geometry)
     overflowed: bool = False       # execute_async steps only: triangles overflowed (result incomplete)
+    composite_overlapped: bool = False   # execute_async P2P steps: composite beside the next surface pass
 
     @classmethod
     def from_native(cls, r: N.NkbReport) -> "Report":
@@ -38,7 +39,7 @@ class Report:
             (float(r.data_range[0]), float(r.data_range[1])),
             float(r.ms_fused), float(r.ms_raster), float(r.ms_composite), float(r.ms_resolve),
             bool(r.reran), bool(r.geometry_cached), float(r.ms_geometry), int(r.surface_pass),
-            bool(r.overflowed),
+            bool(r.overflowed), bool(r.composite_overlapped),
         )
 
 

@@ -1027,6 +1027,11 @@ static bool composite_overlap() {
 
 // SMs the surface pass of a split step leaves to the previous step's
 // composite (persistent K1g / K1s grids would otherwise hold every SM)
+static bool composite_overlap_forced() {            // NKB_COMPOSITE_OVERLAP=2: also beside 3-CTA K1g
+  static const bool on = getenv("NKB_COMPOSITE_OVERLAP") && strcmp(getenv("NKB_COMPOSITE_OVERLAP"), "2") == 0;
+  return on;
+}
+
 static int composite_sms() {
   static const int n = [] {
     const char* v = getenv("NKB_COMPOSITE_SMS");
@@ -1119,8 +1124,11 @@ static int run_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, const C
   // P2P: the composite half of step k runs on ctx->comp_stream while step
   // k+1's surface pass runs on `s`.  Step k+2 (same parity slots) waits for
   // step k's composite half; the cross-GPU order stays with the epoch flags.
-  // (stream-ordered steps only: a synchronous step waits for its composite anyway)
-  const bool split = !sync && p2p && composite_overlap() && fp.prof == nullptr && !p->timing;
+  // (stream-ordered steps only: a synchronous step waits for its composite
+  // anyway; and not beside three-CTA K1g grids, whose SMs have no room left
+  // for the composite's CTAs -- measured unstable / slower)
+  const bool split = !sync && p2p && composite_overlap() && fp.prof == nullptr && !p->timing &&
+                     (composite_overlap_forced() || fused_ctas_per_sm(fp) <= 2);
   if (split) {
     fp.sm_reserve = composite_sms();
     NKB_TRY(ensure_comp_stream(ctx));
@@ -1512,6 +1520,7 @@ int nkb_execute_wait(nkb_ctx* ctx, nkb_report* out, void* stream) {
     out->geometry_cached = ctx->geo_used ? 1 : 0;
     out->surface_pass = ctx->async_surface_pass;
     out->overflowed = any_over ? 1 : 0;
+    out->composite_overlapped = ctx->last_b >= 0 ? 1 : 0;
   }
   return NKB_OK;
 }

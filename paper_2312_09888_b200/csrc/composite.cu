@@ -72,7 +72,7 @@ __device__ int wait_flags(const unsigned long long* flags, int first, int n, uns
 }
 
 // ---- bulk-copy composite ----
-constexpr int kBulkStages = 3;
+constexpr int kBulkStages = 2;         // 64 KB per CTA: fits beside two three-CTA K1g CTAs (146 KB)
 constexpr int kBulkStageBytes = 32768;
 inline __host__ __device__ int bulk_tile_px(int nranks) { return (kBulkStageBytes / 8 / nranks) & ~255; }
 

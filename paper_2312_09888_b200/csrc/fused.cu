@@ -1748,6 +1748,12 @@ int fused_node_prog(const FusedParams& p) {
   return node_prog_of(p) + 16 * stream_prog_of(p) + 64 * fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0, prog_uses(node_prog_of(p), NK_U));
 }
 
+// CTAs per SM of the surface pass (K1g: 2 or 3; K1s and K1: 1)
+int fused_ctas_per_sm(const FusedParams& p) {
+  if (surface_pass_of(p) != 2) return 1;
+  return fused2_occ(k1g_nin(p), p.geo_compact != 0, p.need_wmag != 0, prog_uses(node_prog_of(p), NK_U));
+}
+
 NKB_CHECKED_ACCESSOR(checked_read_fused)
 
 }  // namespace nkb

@@ -202,6 +202,7 @@ unsigned long long checked_read_raster(int* line);
 unsigned long long checked_read_composite(int* line);
 int checked_violations();
 int checked_selftest(cudaStream_t s);          // NKB_CHECKED_SELFTEST=1: one failing check
+int fused_ctas_per_sm(const FusedParams& p);   // surface pass CTAs per SM (composite overlap policy)
 int fused_node_prog(const FusedParams& p);   // K1g + 16 x K1s node program (graph key)
 int stream_prog_of(const FusedParams& p);    // K1s node program
 int surface_pass_of(const FusedParams& p);     // 0 K1, 1 K1s (stream.cu), 2 K1g (2-3 CTAs per SM)

@@ -22,6 +22,22 @@ def _free_port():
     return p
 
 
+def _spawn(fn, size, *rest):
+    """mp.spawn(fn, (size, port, *rest)) on a fresh port; a rendezvous that
+    lost its port to another socket between the probe and the bind
+    (EADDRINUSE) is retried on a new port -- a test-harness race, not a
+    library result."""
+    import torch.multiprocessing as mp
+
+    for attempt in range(3):
+        try:
+            mp.spawn(fn, args=(size, _free_port(), *rest), nprocs=size, join=True)
+            return
+        except Exception as exc:                          # ProcessRaisedException
+            if "EADDRINUSE" not in str(exc) or attempt == 2:
+                raise
+
+
 def _image(rank, size, out_dir, steps=3, cuts=None, reran_out=None):
     import torch.distributed as dist
 
@@ -116,8 +132,8 @@ def test_composite_equals_single_gpu(tmp_path, size, mode):
         pytest.skip(f"needs {size} GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
-    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), mode), nprocs=size, join=True)
+    _spawn(_worker, 1, str(tmp_path), mode)
+    _spawn(_worker, size, str(tmp_path), mode)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / f"g{size}.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
@@ -134,8 +150,8 @@ def test_composite_ragged_partitions_p2p(tmp_path):
     import torch.multiprocessing as mp
 
     E = 4 * 4 * 6
-    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), "p2p"), nprocs=1, join=True)
-    mp.spawn(_worker, args=(3, _free_port(), str(tmp_path), "p2p", (0, 17, 17, E)), nprocs=3, join=True)
+    _spawn(_worker, 1, str(tmp_path), "p2p")
+    _spawn(_worker, 3, str(tmp_path), "p2p", (0, 17, 17, E))
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g3.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
@@ -151,9 +167,9 @@ def test_async_steps_composite_equals_single_gpu(tmp_path, mode, monkeypatch):
         pytest.skip("needs 2 GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
+    _spawn(_worker, 1, str(tmp_path), mode)
     monkeypatch.setenv("NKB_TEST_ASYNC", "1")
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode), nprocs=2, join=True)
+    _spawn(_worker, 2, str(tmp_path), mode)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rng"], b["rng"])
@@ -170,9 +186,9 @@ def test_async_overflow_is_reported_at_the_wait(tmp_path, mode, monkeypatch):
         pytest.skip("needs 2 GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
+    _spawn(_worker, 1, str(tmp_path), mode)
     monkeypatch.setenv("NKB_TEST_ASYNC", "over")
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode, None, 64), nprocs=2, join=True)
+    _spawn(_worker, 2, str(tmp_path), mode, None, 64)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rgba"], b["rgba"])
@@ -189,8 +205,8 @@ def test_overflow_on_one_rank_reruns_every_rank(tmp_path, mode):
         pytest.skip("needs 2 GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(1, _free_port(), str(tmp_path), mode), nprocs=1, join=True)
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), mode, None, 64), nprocs=2, join=True)
+    _spawn(_worker, 1, str(tmp_path), mode)
+    _spawn(_worker, 2, str(tmp_path), mode, None, 64)
     a, b = np.load(tmp_path / "g1.npz"), np.load(tmp_path / "g2.npz")
     assert int(a["n"]) == int(b["n"])
     assert np.array_equal(a["rgba"], b["rgba"])
@@ -243,7 +259,7 @@ def test_collective_stats_equal_numpy_on_concatenation(tmp_path, size):
         pytest.skip(f"needs {size} GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_stats_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    _spawn(_stats_worker, size, str(tmp_path))
     sizes = _STAT_SIZES[size]
     rng = np.random.default_rng(99)
     glob = rng.standard_normal(sum(sizes)) * 10.0 ** rng.integers(-4, 5, sum(sizes))
@@ -299,7 +315,7 @@ def test_dssum_across_ranks_matches_oracle(tmp_path, size):
     from oracle import oracle as O
     from paper_2312_09888_b200 import synth
 
-    mp.spawn(_dssum_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    _spawn(_dssum_worker, size, str(tmp_path))
     nel = (3, 3, 5)
     E = nel[0] * nel[1] * nel[2]
     rng = np.random.default_rng(7)
@@ -354,8 +370,8 @@ def test_transit_endpoint_image_equals_single_gpu(tmp_path, size):
         pytest.skip(f"needs {size} GPUs")
     import torch.multiprocessing as mp
 
-    mp.spawn(_transit_worker, args=(1, _free_port(), str(tmp_path)), nprocs=1, join=True)
-    mp.spawn(_transit_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    _spawn(_transit_worker, 1, str(tmp_path))
+    _spawn(_transit_worker, size, str(tmp_path))
     for step in range(3):
         name = f"step{step:06d}_temperature.ppm"
         a = (tmp_path / "insitu1" / name).read_bytes()
