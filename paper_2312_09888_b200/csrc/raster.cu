@@ -30,7 +30,9 @@ __global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
 // the device).  The region's warps take 32 consecutive triangles each
 // (coalesced reads) and are dealt round-robin over the region's blocks, so a
 // region with few triangles still spreads over several SMs.
-__global__ void __launch_bounds__(256) raster_kernel(const RasterParams p) {
+// (four CTAs per SM: 64 registers with a few bytes of spills beat three at
+// 68 -- the kernel is issue- and latency-bound, profiles/r2/raster_lb4_ab.txt)
+__global__ void __launch_bounds__(256, 4) raster_kernel(const RasterParams p) {
   const int r = blockIdx.y;
   long long ntri = (long long)p.region_count[r];
   if (ntri > p.region_cap) ntri = p.region_cap;
