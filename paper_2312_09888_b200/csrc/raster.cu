@@ -109,6 +109,8 @@ __device__ void report_body(const ReportParams& p) {
 
 __global__ void __launch_bounds__(256) report_kernel(const ReportParams p) { report_body(p); }
 
+constexpr int kResolvePx = 4;
+
 template <bool kTail>
 __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p, const ReportParams rep) {
   double lo = p.vmin, hi = p.vmax;
@@ -127,10 +129,22 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p, con
     p.range_out[1] = hi;
   }
   const double span = __dsub_rn(hi, lo);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
+  // kResolvePx pixels per thread per pass, every key load issued before the
+  // first is used (the loop is load-latency-bound)
+  const long long stride = (long long)gridDim.x * blockDim.x * kResolvePx;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x * kResolvePx + threadIdx.x; i0 < n; i0 += stride) {
+    unsigned long long keys[kResolvePx];
+#pragma unroll
+    for (int k = 0; k < kResolvePx; ++k) {
+      const long long i = i0 + (long long)k * blockDim.x;
+      keys[k] = i < n ? p.zbuf[i] : ~0ULL;
+    }
+#pragma unroll
+    for (int k = 0; k < kResolvePx; ++k) {
+    const long long i = i0 + (long long)k * blockDim.x;
+    if (i >= n) break;
     NKB_DCHECK(i >= 0 && i < n);
-    const unsigned long long key = p.zbuf[i];
+    const unsigned long long key = keys[k];
     uchar4 o;
     float dep;
     if (key == ~0ULL) {
@@ -145,15 +159,20 @@ __global__ void __launch_bounds__(256) resolve_kernel(const ResolveParams p, con
     reinterpret_cast<uchar4*>(p.rgba)[i] = o;
     if (p.depth) p.depth[i] = dep;
     if (kTail) p.clear_next[i] = ~0ULL;
+    }
   }
   if (!kTail) return;
   if (blockIdx.x == 0 && threadIdx.x < 2) p.clear_next[n + threadIdx.x] = ~0ULL;
-  // the last CTA to finish: range words, overflow word and the step report
-  // (every CTA's writes, block 0's range_out included, are fenced before its ticket)
+  // the last CTA to finish: range words, overflow word and the step report.
+  // It reads only what earlier kernels wrote plus block 0's range_out, which
+  // block 0's thread 0 wrote itself and fences before its ticket -- one fence
+  // per CTA, not per thread
   __shared__ int s_last;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(p.ticket, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -310,13 +329,15 @@ int launch_report(const ReportParams& p, cudaStream_t s) {
 }
 
 int launch_resolve(const ResolveParams& p, cudaStream_t s) {
-  resolve_kernel<false><<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p, ReportParams{});
+  resolve_kernel<false><<<grid_for(((long long)p.width * p.height + kResolvePx - 1) / kResolvePx, 256, 148 * 8), 256,
+                          0, s>>>(p, ReportParams{});
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
 
 int launch_resolve_tail(const ResolveParams& p, const ReportParams& rep, cudaStream_t s) {
-  resolve_kernel<true><<<grid_for((long long)p.width * p.height, 256, 148 * 16), 256, 0, s>>>(p, rep);
+  resolve_kernel<true><<<grid_for(((long long)p.width * p.height + kResolvePx - 1) / kResolvePx, 256, 148 * 8), 256, 0,
+                         s>>>(p, rep);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }
