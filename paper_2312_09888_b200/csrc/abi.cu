@@ -754,9 +754,12 @@ static int ensure_image(nkb_ctx* ctx, int W, int H) {
   ctx->rgba = nullptr;
   ctx->depth = nullptr;
   const size_t npx = (size_t)W * H;
-  NKB_CUDA(cudaMalloc(&ctx->zbufs[0], 2 * (npx + 2) * sizeof(unsigned long long)));
-  NKB_CUDA(cudaMemset(ctx->zbufs[0], 0xff, 2 * (npx + 2) * sizeof(unsigned long long)));
-  ctx->zbufs[1] = ctx->zbufs[0] + npx + 2;
+  // the second buffer starts 256-byte aligned whatever W*H is (bulk copies of
+  // a key buffer -- the partition composite -- need 16-byte alignment)
+  const size_t zstride = (npx + 2 + 31) & ~size_t(31);
+  NKB_CUDA(cudaMalloc(&ctx->zbufs[0], 2 * zstride * sizeof(unsigned long long)));
+  NKB_CUDA(cudaMemset(ctx->zbufs[0], 0xff, 2 * zstride * sizeof(unsigned long long)));
+  ctx->zbufs[1] = ctx->zbufs[0] + zstride;
   ctx->zbuf = ctx->zbufs[0];
   ctx->zpar_next = 0;
   ctx->znext_clean = true;

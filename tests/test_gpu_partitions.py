@@ -51,14 +51,15 @@ def one(cyl):
     ctx.close()
 
 
-def _composite(cyl, pipe, R):
+def _composite(cyl, pipe, R, steps=1):
     parts = []
     for r in range(R):
         e0, e1 = synth.partition(cyl.n_elements, r, R)
         ctx = Context(0)
         da = SemDataAdaptor(ctx)
         da.initialize(Snapshot(0.0, 0, r, (_block(cyl, e0, e1),)))
-        InsituAnalysis(pipe).execute(da, fetch_image=False)
+        for _ in range(steps):            # one-GPU steps alternate two key buffers
+            InsituAnalysis(pipe).execute(da, fetch_image=False)
         parts.append((ctx, da))
     root = parts[0][0]
     root.composite_partitions([c for c, _ in parts], pipe.native(pipe.view))
@@ -81,9 +82,10 @@ def test_bulk_and_load_kernels_agree_on_odd_bands(cyl, monkeypatch, R):
     ctx.close()
     monkeypatch.setenv("NKB_COMPOSITE_BULK", "1")
     a_rgba, a_depth = _composite(cyl, pipe, R)
+    c_rgba, c_depth = _composite(cyl, pipe, R, steps=2)   # the second key buffer (odd W*H: padded)
     monkeypatch.setenv("NKB_COMPOSITE_BULK", "0")
     b_rgba, b_depth = _composite(cyl, pipe, R)
-    for rgba, depth in ((a_rgba, a_depth), (b_rgba, b_depth)):
+    for rgba, depth in ((a_rgba, a_depth), (b_rgba, b_depth), (c_rgba, c_depth)):
         assert np.array_equal(rgba, ref.rgba)
         assert np.array_equal(depth.view(np.uint32), ref.depth.view(np.uint32))
 
