@@ -1,0 +1,15 @@
+# final 4-GPU validation at HEAD: full GPU suite, checked multi/partitions, C2 1/2/4 lines
+O=gpurun_out/m4final; rm -rf $O; mkdir -p $O
+python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/pytest.log; tail -n 2 $O/pytest.log
+NKB_LIB=paper_2312_09888_b200/lib/libnekb200_checked.so python -m pytest tests/test_gpu_multi.py tests/test_gpu_partitions.py -m gpu -q -p no:cacheprovider > $O/pytest_checked_multi.log 2>&1; echo "checked rc=$?" >> $O/pytest_checked_multi.log; tail -n 2 $O/pytest_checked_multi.log
+run() { local n=$1; shift; timeout 600 python bench.py "$@" --no-cpu-baseline --e2e-max-gb 0 > $O/$n.json 2> $O/$n.err; echo "$n rc=$?"; }
+run c2_1 --steps 30 --warmup 5
+run c2_2 --gpus 2 --steps 30 --warmup 5
+run c2_4 --gpus 4 --steps 30 --warmup 5
+run c3s_4 --config c3 --scaling strong --gpus 4 --steps 20 --warmup 3
+run c5_4 --config c5 --gpus 4 --steps 20 --warmup 3
+run c4_4 --config c4 --gpus 4 --steps 10 --warmup 3
+for f in $O/c*.json; do python -c "
+import json
+l=[x for x in open('$f').read().splitlines() if x.startswith('{')][-1]
+d=json.loads(l);print('$f', d['n_gpus'], round(d['value']/1e9,2), round(d['ms_per_step'],4), round(d.get('ms_per_step_sync',0),4), d.get('composite_overlapped'), d.get('gpu_launches'))"; done
