@@ -774,6 +774,22 @@ static int ensure_image(nkb_ctx* ctx, int W, int H) {
   return NKB_OK;
 }
 
+// threads per triangle in K2: four when the image has >= 256 pixels per
+// element of the whole mesh -- few, large triangles (C1: 2048 px per element,
+// raster 0.051 -> 0.027 ms) -- else one (C2-C5: 1-32 px per element, where
+// splitting rows only adds set-up work; profiles/r2/raster_lanes_ab.txt).
+// NKB_RASTER_LANES=1|2|4 overrides.
+static int raster_lanes(const nkb_ctx* ctx, const nkb_pipeline* p) {
+  static const int forced = [] {
+    const char* v = getenv("NKB_RASTER_LANES");
+    const int k = v ? atoi(v) : 0;
+    return k == 1 || k == 2 || k == 4 ? k : 0;
+  }();
+  if (forced) return forced;
+  const long long e = ctx->E_global > 0 ? ctx->E_global : ctx->E;
+  return e > 0 && (long long)p->width * p->height >= 256 * e ? 4 : 1;
+}
+
 static int ensure_tri(nkb_ctx* ctx, int64_t cap, bool meta) {
   if (cap <= ctx->tri_cap && (!meta || ctx->meta_alloc)) return NKB_OK;
   cap = std::max(cap, ctx->tri_cap);
@@ -905,6 +921,7 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   rp.width = p->width;
   rp.height = p->height;
   rp.zbuf = zbuf;
+  rp.lanes_per_tri = raster_lanes(ctx, p);
   NKB_TRY(launch_raster(rp, s));
   if (composite)                                   // (one GPU: in the resolve tail)
     NKB_TRY(launch_range_words(ctx->counters, zbuf + npx, rp.region_count == ctx->counters ? nullptr : rp.region_count,
@@ -1002,7 +1019,8 @@ static std::string step_key(nkb_ctx* ctx, const nkb_pipeline* p, const FusedPara
   const void* ptrs[] = {ctx->tri, ctx->meta, ctx->zbuf, ctx->rgba, ctx->depth, ctx->counters, ctx->region_count,
                         ctx->elem_count, ctx->elem_offset, ctx->range_dev, ctx->h_counters};
   add(ptrs, sizeof(ptrs));
-  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0, surface_pass_of(fp), fused_node_prog(fp)};
+  const int64_t v[] = {ctx->tri_cap, ctx->E, ordered ? 1 : 0, surface_pass_of(fp), fused_node_prog(fp),
+                       raster_lanes(ctx, p)};
   add(v, sizeof(v));
   return k;
 }

@@ -108,6 +108,7 @@ struct RasterParams {
   double view[16];                  // 3x4 view rows + perspective row (all zero: orthographic)
   int width, height;
   unsigned long long* zbuf;
+  int lanes_per_tri = 1;            // 1, 2 or 4 threads per triangle (pixel rows split)
 };
 
 struct Colormap {

@@ -32,17 +32,22 @@ __global__ void zbuf_clear_kernel(unsigned long long* z, long long n) {
 // region with few triangles still spreads over several SMs.
 // (four CTAs per SM: 64 registers with a few bytes of spills beat three at
 // 68 -- the kernel is issue- and latency-bound, profiles/r2/raster_lb4_ab.txt)
+// kL lanes per triangle (each takes every kL-th pixel row): more warps with
+// work when a step has few, large triangles (C1)
+template <int kL>
 __global__ void __launch_bounds__(256, 4) raster_kernel(const RasterParams p) {
   const int r = blockIdx.y;
   long long ntri = (long long)p.region_count[r];
   if (ntri > p.region_cap) ntri = p.region_cap;
   const float4* tri = p.tri + 3 * (long long)r * p.region_cap;
   const int W = p.width, H = p.height;
+  constexpr int kPerWarp = 32 / kL;
   const long long gw = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;   // region-local warp
   const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long t = gw * 32 + (threadIdx.x & 31); t < ntri; t += nw * 32) {
+  const int lane = threadIdx.x & 31;
+  for (long long t = gw * kPerWarp + lane / kL; t < ntri; t += nw * kPerWarp) {
     NKB_DCHECK(t >= 0 && t < p.region_cap && r < p.n_regions);
-    rdev::raster_triangle(p.view, W, H, tri + 3 * t, p.zbuf);
+    rdev::raster_triangle(p.view, W, H, tri + 3 * t, p.zbuf, lane % kL, kL);
   }
 }
 
@@ -300,7 +305,9 @@ int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s) {
 
 int launch_raster(const RasterParams& p, cudaStream_t s) {
   const int bx = p.n_regions >= 148 ? 8 : (148 * 8 + p.n_regions - 1) / p.n_regions;
-  raster_kernel<<<dim3(bx, p.n_regions), 256, 0, s>>>(p);
+  if (p.lanes_per_tri == 4) raster_kernel<4><<<dim3(bx, p.n_regions), 256, 0, s>>>(p);
+  else if (p.lanes_per_tri == 2) raster_kernel<2><<<dim3(bx, p.n_regions), 256, 0, s>>>(p);
+  else raster_kernel<1><<<dim3(bx, p.n_regions), 256, 0, s>>>(p);
   NKB_CUDA(cudaGetLastError());
   return NKB_OK;
 }

@@ -87,8 +87,10 @@ __device__ __forceinline__ long long floordiv(long long a, long long b) {  // b 
 }
 
 
+// sub / nsub: this thread draws rows py0 + sub, py0 + sub + nsub, ... (nsub
+// threads share a triangle; the edge values stay exact integers)
 __device__ __forceinline__ void raster_triangle(const double* view, int W, int H, const float4* tri,
-                                                unsigned long long* zbuf) {
+                                                unsigned long long* zbuf, int sub = 0, int nsub = 1) {
   long long X[3], Y[3];
   double Z[3], C[3];
   bool ok = true;
@@ -156,7 +158,14 @@ __device__ __forceinline__ void raster_triangle(const double* view, int W, int H
       wrow[i] = (X[eb[i]] - X[ea[i]]) * (cy0 - Y[ea[i]]) - (Y[eb[i]] - Y[ea[i]]) * (cx0 - X[ea[i]]);
     }
   }
-  for (long long py = py0; py <= py1; ++py) {
+  if (nsub > 1) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      wrow[i] += (long long)sub * dwy[i];
+      dwy[i] *= nsub;
+    }
+  }
+  for (long long py = py0 + sub; py <= py1; py += nsub) {
     long long w[3] = {wrow[0], wrow[1], wrow[2]};
     for (long long px = px0; px <= px1; ++px) {
       if (w[0] + bias[0] >= 0 && w[1] + bias[1] >= 0 && w[2] + bias[2] >= 0) {
