@@ -829,7 +829,9 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   ctx->region_cap = ctx->tri_cap / ctx->n_regions;
   fp.region_cap = ctx->region_cap;
   fp.region_count = ctx->region_count;
-  NKB_CUDA(cudaMemsetAsync(ctx->region_count, 0, sizeof(unsigned long long) * ctx->n_regions, s));
+  // every surface-pass CTA assigns its region's count (FAST mode); only an
+  // empty partition (no launch) needs the zero
+  if (ctx->E <= 0) NKB_CUDA(cudaMemsetAsync(ctx->region_count, 0, sizeof(unsigned long long) * ctx->n_regions, s));
   // counters {0, enc(+max), 0, 0}
   NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
   NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
