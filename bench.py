@@ -659,15 +659,15 @@ def run_ours(a):
         "timed_region": ("host barrier, then a device barrier (NCCL all-reduce on the timed stream), then the "
                          "start event on every rank; CUDA events, max over ranks") if world > 1 else
                         "CUDA events on the launch stream, synchronised on both sides",
-        # libnekb200 kernels per step on rank 0.  1 GPU: K1g|K1|K1s, K2
-        # raster, K3 resolve (+ next key-buffer clear, range words and
-        # report in its last CTA).  NCCL composite: K1g, zbuf clear, K2,
-        # range words, K3, report (the reduce kernels are NCCL's).  P2P
-        # composite: K1g, epoch, wait, zbuf clear, K2, range words, signal,
-        # composite, signal, wait, report; stream-ordered P2P steps report in
-        # both halves (one more report)
-        "gpu_launches": (3 if world == 1 else 6 if os.environ.get("NKB_COMPOSITE") == "nccl" else
-                         12 if rep_last.composite_overlapped else 11) * a.steps,
+        # libnekb200 kernels per step on rank 0, counter init included.  1 GPU:
+        # counters, K1g|K1|K1s, K2 raster, K3 resolve (+ next key-buffer
+        # clear, range words and report in its last CTA).  NCCL composite:
+        # counters, K1g, zbuf clear, K2, range words, K3, report (the reduce
+        # kernels are NCCL's).  P2P composite: counters, K1g, epoch, wait, zbuf
+        # clear, K2, range words, signal, composite, signal, wait, report;
+        # stream-ordered P2P steps report in both halves (one more report)
+        "gpu_launches": (4 if world == 1 else 7 if os.environ.get("NKB_COMPOSITE") == "nccl" else
+                         13 if rep_last.composite_overlapped else 12) * a.steps,
         "composite_overlapped": bool(rep_last.composite_overlapped),
         "host_ms_per_async_launch": host_launch_ms,
         "clocks": clk,

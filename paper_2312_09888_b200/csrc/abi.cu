@@ -833,8 +833,7 @@ static int enqueue_step(nkb_ctx* ctx, const nkb_pipeline* p, FusedParams fp, con
   // empty partition (no launch) needs the zero
   if (ctx->E <= 0) NKB_CUDA(cudaMemsetAsync(ctx->region_count, 0, sizeof(unsigned long long) * ctx->n_regions, s));
   // counters {0, enc(+max), 0, 0}
-  NKB_CUDA(cudaMemsetAsync(ctx->counters, 0, 64, s));
-  NKB_CUDA(cudaMemsetAsync(ctx->counters + 1, 0xff, 8, s));
+  NKB_TRY(launch_init_counters(ctx->counters, s));
   if (timing) NKB_CUDA(cudaEventRecord(ctx->ev[0], s));
   if (ordered) {
     // deterministic (element, cell, surface, table) order: count, scan, emit

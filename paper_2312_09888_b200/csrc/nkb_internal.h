@@ -221,6 +221,7 @@ int launch_compact(const float4* tri, const unsigned long long* meta, const unsi
                    int64_t n_total, cudaStream_t s);
 int launch_count_scan(const int* cnt, int64_t n, long long* off, unsigned long long* total, cudaStream_t s);
 int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s);
+int launch_init_counters(unsigned long long* counters, cudaStream_t s);   // [8] step counters
 int launch_raster(const RasterParams& p, cudaStream_t s);
 int launch_range_words(unsigned long long* counters, unsigned long long* words,
                        const unsigned long long* region_count, int n_regions, int64_t region_cap, int64_t tri_cap,

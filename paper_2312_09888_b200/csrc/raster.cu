@@ -297,6 +297,15 @@ inline unsigned grid_for(long long n, int threads, int max_blocks) {
 
 }  // namespace
 
+// the step's counter words {0, enc(+max) = ~0, 0, ...}: one graph node
+__global__ void init_counters_kernel(unsigned long long* c) { c[threadIdx.x] = threadIdx.x == 1 ? ~0ULL : 0ULL; }
+
+int launch_init_counters(unsigned long long* counters, cudaStream_t s) {
+  init_counters_kernel<<<1, 8, 0, s>>>(counters);
+  NKB_CUDA(cudaGetLastError());
+  return NKB_OK;
+}
+
 int launch_zbuf_clear(unsigned long long* zbuf, int64_t n, cudaStream_t s) {
   zbuf_clear_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(zbuf, n);
   NKB_CUDA(cudaGetLastError());
