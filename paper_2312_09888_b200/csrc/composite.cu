@@ -26,7 +26,7 @@
 // pixel pair from every rank (many CTAs, latency hidden by parallelism).
 // p2p_composite_bulk_kernel: tiles of the band move into shared memory by
 // bulk copies (cp.async.bulk, one per rank and tile, from peer memory over
-// NVLink), three tiles in flight per CTA on mbarriers, so a few CTAs on the
+// NVLink), two tiles in flight per CTA on mbarriers, so a few CTAs on the
 // SMs a split step leaves free (run_step) sustain the band while the next
 // step's surface pass holds the rest of the GPU.
 #include <cuda_runtime.h>
