@@ -1209,6 +1209,13 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       Jij[2] = g[128 + ij];
       Jij[3] = g[192 + ij];
     }
+    // two-CTA kernels: the second node's derivatives are loaded before the
+    // first node's arithmetic (both nodes' shared-memory loads in flight)
+    double U1[9];
+    if (kOcc == 2) {
+#pragma unroll
+      for (int c = 0; c < 9; ++c) U1[c] = S_dv[c * kArr + q1];
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int n = tid + kG2Threads * h;
@@ -1231,7 +1238,7 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       }
       double U[9];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) U[c] = S_dv[c * kArr + q];
+      for (int c = 0; c < 9; ++c) U[c] = (kOcc == 2 && h) ? U1[c] : S_dv[c * kArr + q];
       double A[9];
       if (kCompact) chain_rule_block(U, J, A);           // every compact node is block diagonal
       else chain_rule(U, J, A);
