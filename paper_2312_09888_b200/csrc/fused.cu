@@ -1211,8 +1211,10 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
     }
     // two-CTA kernels: the second node's derivatives are loaded before the
     // first node's arithmetic (both nodes' shared-memory loads in flight)
+    // (two-CTA kernels and node program 2 (C3): measured faster; C5's program 1 slower)
+    constexpr bool kPreU = kOcc == 2 || kProg == 2;
     double U1[9];
-    if (kOcc == 2) {
+    if (kPreU) {
 #pragma unroll
       for (int c = 0; c < 9; ++c) U1[c] = S_dv[c * kArr + q1];
     }
@@ -1238,7 +1240,7 @@ __global__ void __launch_bounds__(kG2Threads, kOcc) fused2_kernel(const FusedPar
       }
       double U[9];
 #pragma unroll
-      for (int c = 0; c < 9; ++c) U[c] = (kOcc == 2 && h) ? U1[c] : S_dv[c * kArr + q];
+      for (int c = 0; c < 9; ++c) U[c] = (kPreU && h) ? U1[c] : S_dv[c * kArr + q];
       double A[9];
       if (kCompact) chain_rule_block(U, J, A);           // every compact node is block diagonal
       else chain_rule(U, J, A);
